@@ -1,0 +1,167 @@
+/*
+ * sqr.h -- C ABI of libsqr.so, the B200 (sm_100a) implementation of the
+ * randomized column-pivoted QR hot path of the reference package `sketchqr`
+ * (Duersch & Gu, arXiv 2008.04447).
+ *
+ * The reference is pure Python; it has no FFI.  Its drop-in boundary is the
+ * Python functions rqrcp / trqrcp / tuxv (pkg/src/sketchqr/randomized.py:227,
+ * 250, 353).  This header is what a binding of those functions needs
+ * underneath: every pointer is a DEVICE pointer to column-major fp64 (or
+ * int64 / int32) storage, every size is an int64, and every call is
+ * asynchronous on the given cudaStream_t (passed as void*).  No torch or
+ * Python types cross this boundary.  INTEGRATION.md shows the ctypes stub.
+ *
+ * Return codes: SQR_OK, SQR_EINVAL (bad argument), SQR_ECUDA (CUDA error;
+ * sqr_last_error() has the text).  Rank exhaustion is NOT an error: it shows
+ * up as achieved < k in the status block, like the reference's achieved_rank.
+ */
+#ifndef SQR_H
+#define SQR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SQR_OK 0
+#define SQR_EINVAL 1
+#define SQR_ECUDA 2
+
+#define SQR_MAX_BLOCKS 65536
+
+/* Device-resident progress / termination record of one factorization.
+ * Mirrors the reference's loop state: achieved (randomized.py:183,211),
+ * the list of ReflectorBlock widths (randomized.py:202), and the reason the
+ * loop stopped (randomized.py:189-190,192-193,197-198,212-213,217-219). */
+typedef struct sqr_status {
+  int32_t stop;           /* 1 once the loop has terminated                       */
+  int32_t reason;         /* SQR_STOP_* below                                     */
+  int32_t achieved;       /* factored columns (achieved_rank)                     */
+  int32_t nblocks;        /* completed ReflectorBlocks                            */
+  int32_t sample_achieved;/* pivots found by the current block's sample QRCP      */
+  int32_t bhat;           /* reflectors produced by the current block's panel     */
+  int32_t nmoves;         /* column moves of the current block                    */
+  int32_t pad_;
+  double floor_sq;        /* SAMPLE_FLOOR^2 * max initial sample column norm^2     */
+  double aux[4];
+} sqr_status;
+
+#define SQR_STOP_NONE 0
+#define SQR_STOP_K_REACHED 1      /* achieved >= k                                   */
+#define SQR_STOP_SAMPLE_FLOOR 2   /* max sample col norm^2 <= floor (randomized.py:189) */
+#define SQR_STOP_SAMPLE_RANK 3    /* sample QRCP found 0 pivots (randomized.py:192)  */
+#define SQR_STOP_PANEL_ZERO 4     /* panel beta == 0 at column 0 (randomized.py:197) */
+#define SQR_STOP_SHORT_BLOCK 5    /* bhat < bb (randomized.py:212)                   */
+#define SQR_STOP_NO_TRAILING 6    /* ncols == 0 (randomized.py:212)                  */
+#define SQR_STOP_R11_SINGULAR 7   /* _diag_ok false (randomized.py:217-219)          */
+
+/* ---------------------------------------------------------------- info */
+const char* sqr_version(void);
+const char* sqr_last_error(void);
+int sqr_device_sm_count(void);
+
+/* ------------------------------------------------------------ RNG (L0)
+ * Omega[i, t] = normal(seed, offset + i + t*rows) for a rows x cols matrix
+ * filled column-major (rng.py:49-70, NormalStream.matrix rng.py:90-93).
+ * transpose=0 writes Omega (ld >= rows); transpose=1 writes Omega^T
+ * (cols x rows, ld >= cols), the K-major operand the sketch GEMM reads. */
+int sqr_gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
+                 uint64_t offset, int transpose, void* stream);
+
+/* ----------------------------------------------------------- GEMMs (K1, K6, K8-K11)
+ * D(M x N) = alpha * X^T C + beta * E     X: K x M (ldx), C: K x N (ldc), E,D: M x N
+ * (np: `Y.T @ C` sites: randomized.py:206,322,325; sketch.py:71 with X = Omega^T).
+ * fp64 DMMA (mma.sync f64) tiles; deterministic split-K; E may alias D or be NULL. */
+int sqr_gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+                const double* C, int64_t ldc, double beta, const double* E, int64_t lde,
+                double* D, int64_t ldd, double* workspace, int64_t workspace_bytes, void* stream);
+
+/* D(M x N) = alpha * X Y + beta * E         X: M x K (ldx), Y: K x N (ldy)
+ * (np: `C -= Y @ W` sites: randomized.py:207,305,330,384). */
+int sqr_gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+                const double* Y, int64_t ldy, double beta, const double* E, int64_t lde,
+                double* D, int64_t ldd, void* stream);
+
+/* ------------------------------------------------- sample QRCP (K2, K12)
+ * Halted pivoted QR of the l x nt sample B (sketch.py:97-119 -> reference.py
+ * _qrcp_core:107-150) on a persistent cooperative kernel.  Writes the
+ * factored sample in pivoted order to Bf (l x nt, ldbf), the local
+ * permutation lperm[pos] = source column (int64, nt), the list of moved
+ * positions moves[2*i] = dst, moves[2*i+1] = src (int32, <= 2*bb pairs) and
+ * st->sample_achieved / st->nmoves.  first != 0 also sets st->floor_sq from
+ * this sample (randomized.py:179-180).  Skipped when st->stop is set. */
+int sqr_sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb,
+                    double* Bf, int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus,
+                    int first, sqr_status* st, void* stream);
+
+/* Apply the block's column moves to rows [0, rows) of X (ld) starting at
+ * column col0, and to the int64 vector perm (may be NULL) starting at col0
+ * (randomized.py:194-195; trqrcp also permutes Wg, Rg at :301-302). */
+int sqr_apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm,
+                    const int32_t* moves, const sqr_status* st, int64_t max_moves, void* stream);
+
+/* ----------------------------------------------------------- panel (K4, K5)
+ * Unpivoted Householder QR of P (mr x w, ldp) in place (randomized.py:107-130,
+ * householder.py:28-49), stopping at the first zero column when stop_at_zero
+ * (the qr_blocked variant, reference.py:281-291, keeps identity reflectors).
+ * w = st->sample_achieved when w < 0.  Outputs: the packed panel in P, the
+ * explicit unit-lower Y (mr x w, ldy), taus, the compact-WY T (w x w, ldt,
+ * householder.py:52-61) and st->bhat. */
+int sqr_panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, double* Y, int64_t ldy,
+                 double* taus, double* T, int64_t ldt, int stop_at_zero, sqr_status* st,
+                 void* stream);
+
+/* T factor only, from an explicit unit-lower Y (m x j) and taus. */
+int sqr_build_t(const double* Y, int64_t ldy, int64_t m, int64_t j, const double* taus,
+                double* T, int64_t ldt, double* workspace, int64_t workspace_bytes, void* stream);
+
+/* ----------------------------------------------------- sample update (K7)
+ * Bnext = [S12 - S11 R11^{-1} R12 ; S22] (sketch.py:122-149) for the nt
+ * trailing columns, after the R11 diagonal guard (randomized.py:133-135,
+ * 217-219).  Bf is the factored sample from sqr_sample_qrcp (l x (nt+b)). */
+int sqr_sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr,
+                      int64_t nt, double* Bnext, int64_t ldbn, sqr_status* st, void* stream);
+
+/* ------------------------------------------------------------- drivers
+ * Full RQRCP (randomized.py:166-224, resample=0) / RSRQRCP (resample=1) on the
+ * m x n device matrix A (lda), in place: R in the upper trapezoid of the
+ * first `achieved` rows, reflector tails below the diagonal.  Omega^T (m x l,
+ * ldo) is the sketch draw (or NULL to draw it from seed on the device).
+ * Outputs: perm (int64, n), taus (k), T blocks (nblk x b x b, block J at
+ * T + J*b*b, ld b), status.  All work is enqueued on `stream` with no host
+ * synchronisation: early exits are device-side flags.  Workspace from
+ * sqr_rqrcp_workspace(). */
+int64_t sqr_rqrcp_workspace(int64_t m, int64_t n, int64_t k, int64_t b, int64_t p);
+int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+              uint64_t seed, const double* omegaT, int64_t ldo, int resample, int64_t* perm,
+              double* taus, double* T, sqr_status* st, void* workspace, int64_t workspace_bytes,
+              void* stream);
+
+/* Truncated RQRCP (randomized.py:250-341).  A is permuted in place but never
+ * updated.  Outputs Yg (m x k, ldy), Wg (k x n, ldw: W^T rows), Rg (k x n,
+ * ldr), perm, taus, T blocks, status. */
+int64_t sqr_trqrcp_workspace(int64_t m, int64_t n, int64_t k, int64_t b, int64_t p);
+int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+               uint64_t seed, const double* omegaT, int64_t ldo, double* Yg, int64_t ldy,
+               double* Wg, int64_t ldw, double* Rg, int64_t ldr, int64_t* perm, double* taus,
+               double* T, sqr_status* st, void* workspace, int64_t workspace_bytes, void* stream);
+
+/* Unpivoted blocked QR (reference.py:266-311) in place on A (m x n), first k
+ * columns; used by TUXV (randomized.py:375,387).  Outputs taus (k), T blocks
+ * (ld b, block J at T + J*b*b). */
+int64_t sqr_qr_blocked_workspace(int64_t m, int64_t n, int64_t k, int64_t b);
+int sqr_qr_blocked(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b,
+                   double* taus, double* T, void* workspace, int64_t workspace_bytes,
+                   void* stream);
+
+/* C := Q C (transpose=0) or Q^T C (transpose=1) for Q = I - Y T Y^T, Y m x j
+ * explicit unit-lower (householder.py:107-120). */
+int sqr_apply_wy(const double* Y, int64_t ldy, const double* T, int64_t ldt, int64_t m, int64_t j,
+                 double* C, int64_t ldc, int64_t ncols, int transpose, double* workspace,
+                 int64_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SQR_H */

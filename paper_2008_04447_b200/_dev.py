@@ -1,0 +1,126 @@
+"""Device plumbing: torch tensors as column-major fp64 storage, workspaces, streams.
+
+torch provides device memory, the current stream and (for multi-GPU)
+torch.distributed; every floating-point operation of the factorizations runs
+in libsqr's kernels.  There is no CPU path: without a CUDA device these
+helpers raise.
+"""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2008_04447_b200 needs a CUDA device (sm_100a); there is no CPU fallback")
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    if dev.type != "cuda":
+        raise RuntimeError(f"device {dev} is not a CUDA device")
+    return dev
+
+
+def ptr(t) -> int | None:
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def even(x: int) -> int:
+    return x + (x & 1)
+
+
+class ColMajor:
+    """An m x n fp64 column-major matrix stored as a torch tensor of shape (n, ld)."""
+
+    __slots__ = ("t", "m", "n", "ld")
+
+    def __init__(self, t: torch.Tensor, m: int, n: int, ld: int):
+        self.t, self.m, self.n, self.ld = t, m, n, ld
+
+    @classmethod
+    def empty(cls, m: int, n: int, device, zero: bool = False, ld: int | None = None) -> "ColMajor":
+        ld = even(max(m, 1)) if ld is None else ld
+        alloc = torch.zeros if zero else torch.empty
+        return cls(alloc((max(n, 1), ld), dtype=torch.float64, device=device), m, n, ld)
+
+    @property
+    def ptr(self) -> int:
+        return self.t.data_ptr()
+
+    def col_ptr(self, row: int, col: int) -> int:
+        return self.t.data_ptr() + 8 * (col * self.ld + row)
+
+    def view(self) -> torch.Tensor:
+        """m x n logical matrix (a transposed, strided view)."""
+        return self.t[: self.n, : self.m].T
+
+    def numpy(self) -> np.ndarray:
+        return np.asfortranarray(self.view().cpu().numpy())
+
+
+def upload(A, device, copy: bool = True) -> ColMajor:
+    """Copy a 2-D numpy array / torch tensor into fresh column-major device storage."""
+    if isinstance(A, torch.Tensor):
+        src = A.detach()
+        if src.dim() != 2:
+            raise ValueError(f"A must be 2-dimensional, got ndim={src.dim()}")
+        m, n = src.shape
+        out = ColMajor.empty(m, n, device)
+        if m and n:
+            out.view().copy_(src.to(device=device, dtype=torch.float64))
+        return out
+    arr = np.asarray(A)
+    if arr.ndim != 2:
+        raise ValueError(f"A must be 2-dimensional, got ndim={arr.ndim}")
+    arr = np.asfortranarray(arr, dtype=np.float64)
+    m, n = arr.shape
+    out = ColMajor.empty(m, n, device)
+    if m and n:
+        host = torch.from_numpy(arr.T)  # (n, m) C-contiguous view of the Fortran array
+        if out.ld == m:
+            out.t[:n].copy_(host, non_blocking=False)
+        else:
+            out.t[:n, :m].copy_(host)
+    return out
+
+
+def check_finite(M: ColMajor, name: str = "A") -> None:
+    if M.m and M.n:
+        v = M.view()
+        bad = int((~torch.isfinite(v)).sum().item())
+        if bad:
+            raise ValueError(f"{name} contains {bad} non-finite entries")
+
+
+class Workspace:
+    """Grow-only zero-initialised scratch per device (barrier / semaphore words
+    inside it are left at zero by every kernel that uses them)."""
+
+    _cache: dict = {}
+
+    @classmethod
+    def get(cls, nbytes: int, device) -> torch.Tensor:
+        key = (str(device),)
+        buf = cls._cache.get(key)
+        if buf is None or buf.numel() < nbytes:
+            cls._cache[key] = None
+            torch.cuda.synchronize(device)
+            buf = torch.zeros(int(nbytes) + 4096, dtype=torch.uint8, device=device)
+            cls._cache[key] = buf
+        return buf
+
+
+def status_new(device) -> torch.Tensor:
+    return torch.zeros(_lib.STATUS_BYTES, dtype=torch.uint8, device=device)
+
+
+def status_read(st: torch.Tensor) -> np.void:
+    host = st.cpu().numpy()
+    return np.frombuffer(host.tobytes(), dtype=_lib.STATUS_DTYPE)[0]

@@ -1,0 +1,182 @@
+// Shared device helpers for libsqr (sm_100a): fp64 DMMA wrappers, cp.async,
+// a reusable grid barrier for cooperative persistent kernels, reductions.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/sqr.h"
+
+namespace sqr {
+
+constexpr int kWarp = 32;
+
+// ----------------------------------------------------------------- error state
+void set_error(const char* fmt, ...);
+int check_cuda(cudaError_t e, const char* what);
+int sm_count();
+int max_smem_optin();
+
+#define SQR_CUDA(call)                                              \
+  do {                                                              \
+    cudaError_t e__ = (call);                                       \
+    if (e__ != cudaSuccess) return ::sqr::check_cuda(e__, #call);   \
+  } while (0)
+#define SQR_LAUNCH(what)                                            \
+  do {                                                              \
+    cudaError_t e__ = cudaGetLastError();                           \
+    if (e__ != cudaSuccess) return ::sqr::check_cuda(e__, what);    \
+  } while (0)
+
+// ------------------------------------------------------------------- fp64 MMA
+// m16n8k4 f64 tensor-core MMA (SASS: 2x DMMA.8x8x4).  Fragment layout
+// (lane = 4*g + t):  a0 = A[g][t], a1 = A[g+8][t];  b0 = B[t][g];
+// d0,d1 = D[g][2t,2t+1];  d2,d3 = D[g+8][2t,2t+1].
+__device__ __forceinline__ void dmma16x8x4(double (&d)[4], double a0, double a1, double b0) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, "
+      "{%0,%1,%2,%3};\n"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b0));
+}
+
+// ------------------------------------------------------------------ cp.async
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src, bool pred) {
+  const int sz = pred ? BYTES : 0;  // src-size 0 => zero fill
+  if constexpr (BYTES == 16) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "r"(sz));
+  } else {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(smem_u32(dst)), "l"(src),
+                 "n"(BYTES), "r"(sz));
+  }
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ------------------------------------------------------ memory-model helpers
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+// L1-bypassing loads for data other CTAs wrote during this launch.
+__device__ __forceinline__ double ld_cg(const double* p) { return __ldcg(p); }
+__device__ __forceinline__ int ld_cg(const int* p) { return __ldcg(p); }
+
+// Sense-reversing grid barrier, reusable across launches without a reset:
+// bar[0] = arrival count, bar[1] = sense word.  Every CTA reads the sense
+// word at kernel entry (no barrier is in flight between stream-ordered
+// launches) and flips its local sense at every barrier.
+struct GridBarrier {
+  unsigned* bar;
+  unsigned sense;
+  unsigned nblocks;
+  __device__ void init(unsigned* b) {
+    bar = b;
+    nblocks = gridDim.x * gridDim.y * gridDim.z;
+    __shared__ unsigned s0;
+    if (threadIdx.x == 0) s0 = ld_acquire_u32(bar + 1);
+    __syncthreads();
+    sense = s0;
+  }
+  __device__ void sync() {
+    __syncthreads();
+    sense ^= 1u;
+    if (threadIdx.x == 0) {
+      __threadfence();
+      unsigned old = atomicAdd(bar, 1u);
+      if (old == nblocks - 1) {
+        atomicExch(bar, 0u);
+        __threadfence();
+        st_release_u32(bar + 1, sense);
+      } else {
+        while (ld_acquire_u32(bar + 1) != sense) {
+        }
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+};
+
+// ---------------------------------------------------------------- reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree): every thread gets the result.
+// `red` must hold >= 32 doubles.  Contains __syncthreads.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double r = 0.0;
+  if (wid == 0) {
+    r = lane < nw ? red[lane] : 0.0;
+    r = warp_sum(r);
+    if (lane == 0) red[0] = r;
+  }
+  __syncthreads();
+  r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// Device-side dynamic shape for GEMMs enqueued ahead of the data that sizes
+// them: skip when *stop != 0; shrink N by *shift and advance the flagged
+// operands by *shift columns (trailing update after a panel of bhat columns).
+constexpr int kShiftB = 1;  // tn: C operand, nn: Y operand
+constexpr int kShiftD = 2;  // D and E
+struct GemmDyn {
+  const int32_t* stop = nullptr;
+  const int32_t* shift = nullptr;
+  int flags = 0;
+};
+
+__host__ __device__ constexpr int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+__host__ __device__ constexpr int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
+
+}  // namespace sqr
+
+// ------------------------------------------------------ internal entry points
+namespace sqr {
+int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx, const double* C,
+            int64_t ldc, double beta, const double* E, int64_t lde, double* D, int64_t ldd, double* ws,
+            int64_t ws_bytes, cudaStream_t s, GemmDyn dyn);
+int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx, const double* Y,
+            int64_t ldy, double beta, const double* E, int64_t lde, double* D, int64_t ldd, cudaStream_t s,
+            GemmDyn dyn);
+int64_t sample_qrcp_workspace(int64_t ell, int64_t nt);
+int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf, int64_t ldbf,
+                int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st, void* ws,
+                int64_t ws_bytes, cudaStream_t s);
+int64_t panel_workspace(int64_t w);
+int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
+             double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s);
+int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
+            const int32_t* gate, cudaStream_t s);
+int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed, uint64_t offset,
+             int transpose, const int32_t* gate, cudaStream_t s);
+int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm, const int32_t* moves,
+                const sqr_status* st, int64_t max_moves, cudaStream_t s);
+int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
+                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, cudaStream_t s);
+int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s);
+int iota(int64_t* p, int64_t n, cudaStream_t s);
+int copy_upper(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, const int32_t* gate,
+               cudaStream_t s);
+}  // namespace sqr

@@ -1,0 +1,393 @@
+// Host-side drivers of libsqr: the whole factorization loop is enqueued on
+// one stream with NO host synchronisation.  Every early exit of the
+// reference loop (randomized.py:185-221, 287-336) is a device-side flag in
+// sqr_status that the downstream kernels of the same and later blocks test,
+// so the loop shape is static and can be captured in a CUDA graph.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sqr {
+namespace {
+
+// Bump allocator over the caller's workspace; with base == nullptr it only
+// measures (used by the *_workspace queries).
+struct Carve {
+  char* base;
+  int64_t off = 0;
+  explicit Carve(void* b) : base(static_cast<char*>(b)) {}
+  template <typename T>
+  T* take(int64_t count) {
+    off = rup(off, 256);
+    T* p = base ? reinterpret_cast<T*>(base + off) : nullptr;
+    off += std::max<int64_t>(count, 1) * (int64_t)sizeof(T);
+    return p;
+  }
+};
+
+constexpr int64_t kGemmWsBytes = (int64_t)8 * 148 * 72 * 256 * 8 + 8 * 148 * 8 * 4 + 4096;
+
+struct RqrcpWs {
+  double *Bcur, *Bnext, *Bf, *stau, *Ypan, *Gm, *Wt, *W, *OmT, *gemm;
+  int64_t* lperm;
+  int32_t* moves;
+  void *sample, *panel;
+  int64_t sample_bytes, panel_bytes;
+  int64_t total;
+};
+
+RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool need_omega, bool resample) {
+  const int64_t ell = b + p;
+  Carve c(ws);
+  RqrcpWs w;
+  w.gemm = c.take<double>(kGemmWsBytes / 8);
+  w.sample_bytes = sample_qrcp_workspace(ell, n);
+  w.sample = c.take<char>(w.sample_bytes);
+  w.panel_bytes = panel_workspace(b);
+  w.panel = c.take<char>(w.panel_bytes);
+  w.Bcur = c.take<double>(ell * n);
+  w.Bnext = c.take<double>(ell * n);
+  w.Bf = c.take<double>(ell * n);
+  w.lperm = c.take<int64_t>(n);
+  w.moves = c.take<int32_t>(4 * b + 8);
+  w.stau = c.take<double>(b);
+  w.Ypan = c.take<double>(m * b);
+  w.Gm = c.take<double>(b * b);
+  w.Wt = c.take<double>(b * n);
+  w.W = c.take<double>(b * n);
+  w.OmT = (need_omega || resample) ? c.take<double>(m * ell) : nullptr;
+  w.total = c.off + 256;
+  return w;
+}
+
+// One compact-WY block reflection of the trailing matrix (randomized.py:203-210):
+// Wt = Y^T C;  W = -T^T Wt;  C += Y W, with C starting bhat columns right of P.
+int trailing_update(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, const double* Y,
+                    int64_t ldy, const double* T, int64_t ldt, double* Wt, double* W, int64_t ldw,
+                    sqr_status* st, double* gws, cudaStream_t s) {
+  if (nt <= 1) return SQR_OK;
+  GemmDyn d1{&st->stop, &st->bhat, kShiftB};
+  GemmDyn d2{&st->stop, &st->bhat, 0};
+  GemmDyn d3{&st->stop, &st->bhat, kShiftD};
+  int rc = gemm_tn(bb, nt, mr, 1.0, Y, ldy, P, lda, 0.0, nullptr, 0, Wt, ldw, gws, kGemmWsBytes, s, d1);
+  if (rc) return rc;
+  rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, Wt, ldw, 0.0, nullptr, 0, W, ldw, gws, kGemmWsBytes, s, d2);
+  if (rc) return rc;
+  return gemm_nn(mr, nt, bb, 1.0, Y, ldy, W, ldw, 1.0, P, lda, P, lda, s, d3);
+}
+
+}  // namespace
+}  // namespace sqr
+
+using namespace sqr;
+static_assert(sizeof(sqr_status) == 72, "sqr_status layout is part of the ABI");
+
+extern "C" int64_t sqr_rqrcp_workspace(int64_t m, int64_t n, int64_t /*k*/, int64_t b, int64_t p) {
+  return carve_rqrcp(nullptr, m, n, b, p, true, true).total;
+}
+
+extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+                         uint64_t seed, const double* omegaT, int64_t ldo, int resample, int64_t* perm,
+                         double* taus, double* T, sqr_status* st, void* workspace, int64_t workspace_bytes,
+                         void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t ell = b + p;
+  if (m <= 0 || n <= 0 || k < 1 || k > std::min(m, n) || b < 1 || p < 0 || ell >= m || lda < m) {
+    set_error("sqr_rqrcp: invalid arguments m=%lld n=%lld k=%lld b=%lld p=%lld", (long long)m, (long long)n,
+              (long long)k, (long long)b, (long long)p);
+    return SQR_EINVAL;
+  }
+  if (b > 128 || ell > 144) {
+    set_error("sqr_rqrcp: b=%lld / l=%lld exceed the kernel limits (b<=128, b+p<=144)", (long long)b,
+              (long long)ell);
+    return SQR_EINVAL;
+  }
+  RqrcpWs w = carve_rqrcp(workspace, m, n, b, p, omegaT == nullptr, resample != 0);
+  if (workspace == nullptr || workspace_bytes < w.total) {
+    set_error("sqr_rqrcp: workspace %lld < %lld bytes", (long long)workspace_bytes, (long long)w.total);
+    return SQR_EINVAL;
+  }
+  SQR_CUDA(cudaMemsetAsync(st, 0, sizeof(sqr_status), s));
+  int rc = iota(perm, n, s);
+  if (rc) return rc;
+  if (omegaT == nullptr) {
+    rc = gaussian(w.OmT, m, ell, m, seed, 0, 1, nullptr, s);
+    if (rc) return rc;
+    omegaT = w.OmT;
+    ldo = m;
+  }
+  // Sketch B = Omega A (sketch.py:70-71).
+  rc = gemm_tn(ell, n, m, 1.0, omegaT, ldo, A, lda, 0.0, nullptr, 0, w.Bcur, ell, w.gemm, kGemmWsBytes, s,
+               GemmDyn{});
+  if (rc) return rc;
+  uint64_t stream_pos = (uint64_t)(ell * m);
+  const int64_t nblk = cdiv(k, b);
+  double* Bc = w.Bcur;
+  double* Bn = w.Bnext;
+  for (int64_t J = 0; J < nblk; ++J) {
+    const int64_t i0 = J * b, bb = std::min(b, k - i0), nt = n - i0, mr = m - i0;
+    double* P = A + i0 + i0 * lda;
+    double* TJ = T + J * b * b;
+    if ((rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
+                          w.sample_bytes, s)))
+      return rc;
+    if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
+    if ((rc = panel_qr(P, lda, mr, -1, bb, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, s))) return rc;
+    if ((rc = gemm_tn(bb, bb, mr, 1.0, w.Ypan, m, w.Ypan, m, 0.0, nullptr, 0, w.Gm, bb, w.gemm, kGemmWsBytes,
+                      s, GemmDyn{&st->stop, nullptr, 0})))
+      return rc;
+    if ((rc = build_t(w.Gm, bb, taus + i0, bb, TJ, b, &st->stop, s))) return rc;
+    if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, TJ, b, w.Wt, w.W, b, st, w.gemm, s))) return rc;
+    if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
+    if (J + 1 < nblk) {
+      const int64_t a1 = i0 + bb;  // achieved if the block completed
+      if (resample) {
+        // Fresh draw of the trailing sample (randomized.py:214-215; rng.py:85-93).
+        if ((rc = gaussian(w.OmT, m - a1, ell, m - a1, seed, stream_pos, 1, &st->stop, s))) return rc;
+        if ((rc = gemm_tn(ell, n - a1, m - a1, 1.0, w.OmT, m - a1, A + a1 + a1 * lda, lda, 0.0, nullptr, 0, Bn,
+                          ell, w.gemm, kGemmWsBytes, s, GemmDyn{&st->stop, nullptr, 0})))
+          return rc;
+        stream_pos += (uint64_t)(ell * (m - a1));
+      } else {
+        if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, b, Bn, ell, st, s))) return rc;
+      }
+      std::swap(Bc, Bn);
+    }
+  }
+  return SQR_OK;
+}
+
+// ------------------------------------------------------------ TRQRCP
+namespace {
+struct TrqrcpWs {
+  RqrcpWs r;
+  double *Pn, *Gb, *Cr;
+};
+TrqrcpWs carve_trqrcp(void* ws, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p, bool need_omega) {
+  TrqrcpWs w;
+  w.r = carve_rqrcp(ws, m, n, b, p, need_omega, false);
+  Carve c(ws);
+  c.off = w.r.total;
+  w.Pn = c.take<double>(m * b);
+  w.Gb = c.take<double>(b * n);
+  w.Cr = c.take<double>(b * std::max<int64_t>(k, 1));
+  w.r.total = c.off + 256;
+  return w;
+}
+}  // namespace
+
+extern "C" int64_t sqr_trqrcp_workspace(int64_t m, int64_t n, int64_t k, int64_t b, int64_t p) {
+  return carve_trqrcp(nullptr, m, n, k, b, p, true).r.total;
+}
+
+// Truncated RQRCP (randomized.py:250-341): A is only permuted; per block the
+// panel is materialised through the accumulated reflections, and the new
+// W^T / R rows come from the adjusted inner products, so A is read about once
+// per block (one GEMM sweep Y2^T A).
+extern "C" int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+                          uint64_t seed, const double* omegaT, int64_t ldo, double* Yg, int64_t ldy, double* Wg,
+                          int64_t ldw, double* Rg, int64_t ldr, int64_t* perm, double* taus, double* T,
+                          sqr_status* st, void* workspace, int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t ell = b + p;
+  if (m <= 0 || n <= 0 || k < 1 || k > std::min(m, n) || b < 1 || p < 0 || ell >= m || lda < m || ldy < m ||
+      ldw < k || ldr < k) {
+    set_error("sqr_trqrcp: invalid arguments");
+    return SQR_EINVAL;
+  }
+  if (b > 128 || ell > 144) {
+    set_error("sqr_trqrcp: b=%lld / l=%lld exceed the kernel limits (b<=128, b+p<=144)", (long long)b,
+              (long long)ell);
+    return SQR_EINVAL;
+  }
+  TrqrcpWs tw = carve_trqrcp(workspace, m, n, k, b, p, omegaT == nullptr);
+  RqrcpWs& w = tw.r;
+  if (workspace == nullptr || workspace_bytes < w.total) {
+    set_error("sqr_trqrcp: workspace %lld < %lld bytes", (long long)workspace_bytes, (long long)w.total);
+    return SQR_EINVAL;
+  }
+  SQR_CUDA(cudaMemsetAsync(st, 0, sizeof(sqr_status), s));
+  int rc = iota(perm, n, s);
+  if (rc) return rc;
+  if (omegaT == nullptr) {
+    if ((rc = gaussian(w.OmT, m, ell, m, seed, 0, 1, nullptr, s))) return rc;
+    omegaT = w.OmT;
+    ldo = m;
+  }
+  if ((rc = gemm_tn(ell, n, m, 1.0, omegaT, ldo, A, lda, 0.0, nullptr, 0, w.Bcur, ell, w.gemm, kGemmWsBytes, s,
+                    GemmDyn{})))
+    return rc;
+  const int64_t nblk = cdiv(k, b);
+  double* Bc = w.Bcur;
+  double* Bn = w.Bnext;
+  for (int64_t J = 0; J < nblk; ++J) {
+    const int64_t i0 = J * b, bb = std::min(b, k - i0), nt = n - i0, mr = m - i0;
+    double* TJ = T + J * b * b;
+    double* Ypan = Yg + i0 + i0 * ldy;  // Yg[i0:, i0:i0+bb]
+    GemmDyn gate{&st->stop, nullptr, 0};
+    if ((rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
+                          w.sample_bytes, s)))
+      return rc;
+    if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
+    if (i0 > 0) {
+      if ((rc = apply_moves(Wg, ldw, i0, i0, nullptr, w.moves, st, 2 * bb, s))) return rc;
+      if ((rc = apply_moves(Rg, ldr, i0, i0, nullptr, w.moves, st, 2 * bb, s))) return rc;
+    }
+    // panel = A[i0:, sel] - Yg[i0:, :i0] Wg[:i0, sel]   (randomized.py:304-306)
+    if ((rc = gemm_nn(mr, bb, i0, -1.0, Yg + i0, ldy, Wg + i0 * ldw, ldw, 1.0, A + i0 + i0 * lda, lda, tw.Pn, m,
+                      s, gate)))
+      return rc;
+    if ((rc = panel_qr(tw.Pn, m, mr, -1, bb, Ypan, ldy, taus + i0, 1, st, w.panel, w.panel_bytes, s))) return rc;
+    if ((rc = copy_upper(tw.Pn, m, Rg + i0 + i0 * ldr, ldr, bb, &st->stop, s))) return rc;
+    if ((rc = gemm_tn(bb, bb, mr, 1.0, Ypan, ldy, Ypan, ldy, 0.0, nullptr, 0, w.Gm, bb, w.gemm, kGemmWsBytes, s,
+                      gate)))
+      return rc;
+    if ((rc = build_t(w.Gm, bb, taus + i0, bb, TJ, b, &st->stop, s))) return rc;
+    if (nt > 1) {
+      GemmDyn shB{&st->stop, &st->bhat, kShiftB};
+      GemmDyn sh0{&st->stop, &st->bhat, 0};
+      GemmDyn shD{&st->stop, &st->bhat, kShiftD};
+      GemmDyn shBD{&st->stop, &st->bhat, kShiftB | kShiftD};
+      // G = Y2^T A[i0:, tcols]   (randomized.py:322)
+      if ((rc = gemm_tn(bb, nt, mr, 1.0, Ypan, ldy, A + i0 + i0 * lda, lda, 0.0, nullptr, 0, tw.Gb, b, w.gemm,
+                        kGemmWsBytes, s, shB)))
+        return rc;
+      if (i0 > 0) {
+        // G -= (Y2^T Y1) W1^T   (randomized.py:325-326)
+        if ((rc = gemm_tn(bb, i0, mr, 1.0, Ypan, ldy, Yg + i0, ldy, 0.0, nullptr, 0, tw.Cr, b, w.gemm, kGemmWsBytes,
+                          s, gate)))
+          return rc;
+        if ((rc = gemm_nn(bb, nt, i0, -1.0, tw.Cr, b, Wg + i0 * ldw, ldw, 1.0, tw.Gb, b, tw.Gb, b, s, shB)))
+          return rc;
+      }
+      // Wg[i0:i0+bb, tcols] = T2^T G   (randomized.py:327)
+      if ((rc = gemm_tn(bb, nt, bb, 1.0, TJ, b, tw.Gb, b, 0.0, nullptr, 0, Wg + i0 + i0 * ldw, ldw, w.gemm,
+                        kGemmWsBytes, s, shD)))
+        return rc;
+      // R12 = A[i0:i0+bb, tcols] - Yg[i0:i0+bb, :i0+bb] Wg[:i0+bb, tcols]   (randomized.py:329-330)
+      if ((rc = gemm_nn(bb, nt, i0 + bb, -1.0, Yg + i0, ldy, Wg + i0 * ldw, ldw, 1.0, A + i0 + i0 * lda, lda,
+                        Rg + i0 + i0 * ldr, ldr, s, shBD)))
+        return rc;
+      (void)sh0;
+    }
+    if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
+    if (J + 1 < nblk) {
+      if ((rc = sample_update(w.Bf, ell, ell, Rg + i0 + i0 * ldr, ldr, nt - bb, b, Bn, ell, st, s))) return rc;
+      std::swap(Bc, Bn);
+    }
+  }
+  return SQR_OK;
+}
+
+// ------------------------------------------------------------ qr_blocked
+extern "C" int64_t sqr_qr_blocked_workspace(int64_t m, int64_t n, int64_t /*k*/, int64_t b) {
+  Carve c(nullptr);
+  c.take<double>(kGemmWsBytes / 8);
+  c.take<char>(panel_workspace(std::min<int64_t>(b, 128)));
+  c.take<double>(m * b);        // Ypan
+  c.take<double>(b * b);        // G
+  c.take<double>(b * n * 2);    // Wt, W
+  c.take<sqr_status>(1);
+  return c.off + 256;
+}
+
+extern "C" int sqr_qr_blocked(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, double* taus,
+                              double* T, void* workspace, int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (m <= 0 || n <= 0 || k < 1 || k > std::min(m, n) || b < 1 || b > 128 || lda < m) {
+    set_error("sqr_qr_blocked: invalid arguments");
+    return SQR_EINVAL;
+  }
+  if (workspace_bytes < sqr_qr_blocked_workspace(m, n, k, b)) {
+    set_error("sqr_qr_blocked: workspace too small");
+    return SQR_EINVAL;
+  }
+  Carve c(workspace);
+  double* gws = c.take<double>(kGemmWsBytes / 8);
+  const int64_t pb = panel_workspace(std::min<int64_t>(b, 128));
+  void* pws = c.take<char>(pb);
+  double* Ypan = c.take<double>(m * b);
+  double* Gm = c.take<double>(b * b);
+  double* Wt = c.take<double>(b * n);
+  double* W = c.take<double>(b * n);
+  sqr_status* st = c.take<sqr_status>(1);
+  SQR_CUDA(cudaMemsetAsync(st, 0, sizeof(sqr_status), s));
+  int rc;
+  for (int64_t i0 = 0; i0 < k; i0 += b) {
+    const int64_t bb = std::min(b, k - i0), mr = m - i0, nt = n - i0;
+    double* P = A + i0 + i0 * lda;
+    double* TJ = T + (i0 / b) * b * b;
+    if ((rc = panel_qr(P, lda, mr, bb, bb, Ypan, m, taus + i0, 0, st, pws, pb, s))) return rc;
+    if ((rc = gemm_tn(bb, bb, mr, 1.0, Ypan, m, Ypan, m, 0.0, nullptr, 0, Gm, bb, gws, kGemmWsBytes, s,
+                      GemmDyn{})))
+      return rc;
+    if ((rc = build_t(Gm, bb, taus + i0, bb, TJ, b, nullptr, s))) return rc;
+    if ((rc = trailing_update(P, lda, mr, nt, bb, Ypan, m, TJ, b, Wt, W, b, st, gws, s))) return rc;
+  }
+  return SQR_OK;
+}
+
+// ------------------------------------------------------------ WY helpers
+extern "C" int sqr_build_t(const double* Y, int64_t ldy, int64_t m, int64_t j, const double* taus, double* T,
+                           int64_t ldt, double* workspace, int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (j <= 0) return SQR_OK;
+  if (j > 144 || workspace_bytes < (int64_t)(j * j * 8) + kGemmWsBytes) {
+    set_error("sqr_build_t: j > 144 or workspace too small");
+    return SQR_EINVAL;
+  }
+  double* Gm = workspace;
+  double* gws = workspace + rup(j * j, 32);
+  int rc = gemm_tn(j, j, m, 1.0, Y, ldy, Y, ldy, 0.0, nullptr, 0, Gm, j, gws, kGemmWsBytes, s, GemmDyn{});
+  if (rc) return rc;
+  return build_t(Gm, j, taus, j, T, ldt, nullptr, s);
+}
+
+extern "C" int sqr_apply_wy(const double* Y, int64_t ldy, const double* T, int64_t ldt, int64_t m, int64_t j,
+                            double* C, int64_t ldc, int64_t ncols, int transpose, double* workspace,
+                            int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (j <= 0 || ncols <= 0) return SQR_OK;
+  if (j > 144 || workspace_bytes < 2 * j * ncols * 8 + kGemmWsBytes + 1024) {
+    set_error("sqr_apply_wy: j > 144 or workspace too small");
+    return SQR_EINVAL;
+  }
+  double* Wt = workspace;
+  double* W = workspace + rup(j * ncols, 32);
+  double* gws = W + rup(j * ncols, 32);
+  // Wt = Y^T C
+  int rc = gemm_tn(j, ncols, m, 1.0, Y, ldy, C, ldc, 0.0, nullptr, 0, Wt, j, gws, kGemmWsBytes, s, GemmDyn{});
+  if (rc) return rc;
+  if (transpose) {
+    // W = -T^T Wt
+    rc = gemm_tn(j, ncols, j, -1.0, T, ldt, Wt, j, 0.0, nullptr, 0, W, j, gws, kGemmWsBytes, s, GemmDyn{});
+  } else {
+    // W = -T Wt
+    rc = gemm_nn(j, ncols, j, -1.0, T, ldt, Wt, j, 0.0, nullptr, 0, W, j, s, GemmDyn{});
+  }
+  if (rc) return rc;
+  return gemm_nn(m, ncols, j, 1.0, Y, ldy, W, j, 1.0, C, ldc, C, ldc, s, GemmDyn{});
+}
+
+extern "C" int sqr_panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, double* Y, int64_t ldy, double* taus,
+                            double* T, int64_t ldt, int stop_at_zero, sqr_status* st, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t wmax = w < 0 ? 128 : w;
+  const int64_t pb = panel_workspace(wmax);
+  const int64_t total = pb + kGemmWsBytes + wmax * wmax * 8 + 1024;
+  char* ws = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&ws), total, s) != cudaSuccess) {
+    set_error("sqr_panel_qr: cudaMallocAsync failed");
+    return SQR_ECUDA;
+  }
+  cudaMemsetAsync(ws, 0, total, s);
+  int rc = panel_qr(P, ldp, mr, w, wmax, Y, ldy, taus, stop_at_zero, st, ws, pb, s);
+  double* Gm = reinterpret_cast<double*>(ws + rup(pb, 256));
+  double* gws = Gm + rup(wmax * wmax, 32);
+  if (!rc)
+    rc = gemm_tn(wmax, wmax, mr, 1.0, Y, ldy, Y, ldy, 0.0, nullptr, 0, Gm, wmax, gws, kGemmWsBytes, s,
+                 GemmDyn{&st->stop, nullptr, 0});
+  if (!rc && T) rc = build_t(Gm, wmax, taus, wmax, T, ldt, &st->stop, s);
+  cudaFreeAsync(ws, s);
+  return rc;
+}

@@ -1,0 +1,487 @@
+// fp64 tensor-core GEMMs for the RQRCP hot path (sm_100a, mma.sync f64 -> DMMA).
+//
+//  gemm_tn:  D(MxN) = alpha * X^T C + beta * E     (short M <= 144, long K, long N)
+//            the sketch B = Omega A (sketch.py:70-71, X = Omega^T), the trailing
+//            update's first sweep Y^T C (randomized.py:206), TRQRCP's Y2^T A
+//            (randomized.py:322), W = T^T (.) (householder.py:109-110).
+//  gemm_nn:  D(MxN) = alpha * X Y + beta * E        (long M, long N, short K)
+//            the trailing update's second sweep C -= Y W (randomized.py:207),
+//            TRQRCP panel/R-row materialisation (randomized.py:305,330), TUXV A V_k
+//            (randomized.py:384).
+//
+// Both stage operands through a 4-deep cp.async ring in padded shared memory
+// (row pitch = 4 mod 16 doubles => conflict-free f64 fragment gathers) and
+// accumulate with m16n8k4 f64 MMAs.  gemm_tn splits K across CTAs when the
+// N-tiles cannot fill 148 SMs; partials are summed in a FIXED split order by
+// the last-arriving CTA of each tile, so results are bitwise deterministic.
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sqr {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kBK = 16;        // K per pipeline stage
+constexpr int kPitchK = kBK + 4;
+constexpr int kStages = 4;
+
+// ---------------------------------------------------------------- gemm_tn
+// Computed as D^T(N x M) = C^T(N x K) X(K x M): MMA rows = n, MMA cols = i.
+// CTA tile: 128 n x MT i;  8 warps = 4 (n) x 2 (i);  warp tile 32 n x MT/2 i.
+template <int MT, int VEC>
+struct TnCfg {
+  static constexpr int BN = 128;
+  static constexpr int NI = MT / 16;  // n8 fragments per warp along i
+  static constexpr int A_ELEMS = BN * kPitchK;
+  static constexpr int B_ELEMS = MT * kPitchK;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int SMEM = STAGE * kStages * 8;
+  static constexpr int ACC = 2 * NI * 4;
+};
+
+template <int MT, int VEC>
+__device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const double* __restrict__ X,
+                                              int64_t ldx, const double* __restrict__ C, int64_t ldc,
+                                              int M, int N, int n0, int k0, int kend) {
+  using Cfg = TnCfg<MT, VEC>;
+  constexpr int CPR = kBK / VEC;  // chunks per row
+  const int tid = threadIdx.x;
+  // A operand rows: columns n of C, K contiguous.
+  for (int c = tid; c < Cfg::BN * CPR; c += kThreads) {
+    const int r = c / CPR, kc = (c % CPR) * VEC;
+    const int n = n0 + r, k = k0 + kc;
+    const bool ok = (n < N) && (k < kend);
+    const double* src = ok ? C + (int64_t)n * ldc + k : C;
+    double* dst = sA + r * kPitchK + kc;
+    if constexpr (VEC == 2) {
+      const int sz = ok ? ((k + 1 < kend) ? 16 : 8) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                   "r"(sz));
+    } else {
+      cp_async<8>(dst, src, ok);
+    }
+  }
+  // B operand rows: columns i of X, K contiguous.
+  for (int c = tid; c < MT * CPR; c += kThreads) {
+    const int r = c / CPR, kc = (c % CPR) * VEC;
+    const int k = k0 + kc;
+    const bool ok = (r < M) && (k < kend);
+    const double* src = ok ? X + (int64_t)r * ldx + k : X;
+    double* dst = sB + r * kPitchK + kc;
+    if constexpr (VEC == 2) {
+      const int sz = ok ? ((k + 1 < kend) ? 16 : 8) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                   "r"(sz));
+    } else {
+      cp_async<8>(dst, src, ok);
+    }
+  }
+}
+
+template <int MT, int VEC>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
+                   const double* __restrict__ C, int64_t ldc, double beta, const double* E,
+                   int64_t lde, double* D, int64_t ldd, int kchunk, double* part, unsigned* sems,
+                   GemmDyn dyn) {
+  using Cfg = TnCfg<MT, VEC>;
+  extern __shared__ __align__(16) double smem[];
+  if (dyn.stop && *dyn.stop) return;
+  if (dyn.shift) {
+    const int sh = *dyn.shift;
+    N -= sh;
+    if (dyn.flags & kShiftB) C += (int64_t)sh * ldc;
+    if (dyn.flags & kShiftD) {
+      D += (int64_t)sh * ldd;
+      if (E) E += (int64_t)sh * lde;
+    }
+  }
+  if ((int)blockIdx.x * Cfg::BN >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wn = (warp & 3) * 32, wi = (warp >> 2) * (MT / 2);
+  const int n0 = blockIdx.x * Cfg::BN;
+  const int split = blockIdx.y, nsplit = gridDim.y;
+  const int kbeg = split * kchunk;
+  const int kend = min(K, kbeg + kchunk);
+  const int nk = kend > kbeg ? (int)cdiv(kend - kbeg, kBK) : 0;
+
+  double acc[2][Cfg::NI][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < Cfg::NI; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nk) {
+      double* st = smem + s * Cfg::STAGE;
+      tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + s * kBK, kend);
+    }
+    cp_async_commit();
+  }
+
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int ls = kt + kStages - 1;
+      if (ls < nk) {
+        double* st = smem + (ls % kStages) * Cfg::STAGE;
+        tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + ls * kBK,
+                               kend);
+      }
+      cp_async_commit();
+    }
+    const double* sA = smem + (kt % kStages) * Cfg::STAGE;
+    const double* sB = sA + Cfg::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < kBK; kk += 4) {
+      double a[2][2], b[Cfg::NI];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi) {
+        a[mi][0] = sA[(wn + mi * 16 + g) * kPitchK + kk + t];
+        a[mi][1] = sA[(wn + mi * 16 + g + 8) * kPitchK + kk + t];
+      }
+#pragma unroll
+      for (int ni = 0; ni < Cfg::NI; ++ni) b[ni] = sB[(wi + ni * 8 + g) * kPitchK + kk + t];
+#pragma unroll
+      for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+        for (int ni = 0; ni < Cfg::NI; ++ni) dmma16x8x4(acc[mi][ni], a[mi][0], a[mi][1], b[ni]);
+    }
+  }
+  cp_async_wait<0>();
+
+  if (nsplit > 1) {
+    // Publish this split's partial in thread-contiguous layout; the last
+    // arriving CTA of the tile sums all splits in index order (deterministic).
+    const int tiles = gridDim.x;
+    double* mine = part + ((int64_t)blockIdx.x * nsplit + split) * Cfg::ACC * kThreads;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < Cfg::NI; ++b)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) __stcg(mine + ((a * Cfg::NI + b) * 4 + e) * kThreads + tid, acc[a][b][e]);
+    __threadfence();
+    __syncthreads();
+    __shared__ unsigned last;
+    if (tid == 0) {
+      unsigned old = atomicAdd(sems + blockIdx.x, 1u);
+      last = (old == (unsigned)nsplit - 1);
+      if (last) sems[blockIdx.x] = 0u;  // reusable by the next launch
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    (void)tiles;
+#pragma unroll
+    for (int a = 0; a < 2; ++a)
+#pragma unroll
+      for (int b = 0; b < Cfg::NI; ++b)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          double s = 0.0;
+          const double* base = part + (int64_t)blockIdx.x * nsplit * Cfg::ACC * kThreads +
+                               ((a * Cfg::NI + b) * 4 + e) * kThreads + tid;
+          for (int sp = 0; sp < nsplit; ++sp) s += __ldcg(base + (int64_t)sp * Cfg::ACC * kThreads);
+          acc[a][b][e] = s;
+        }
+  }
+
+  // Epilogue: D(i, n) = alpha * acc + beta * E(i, n).
+#pragma unroll
+  for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int n = n0 + wn + mi * 16 + g + h * 8;
+      if (n >= N) continue;
+#pragma unroll
+      for (int ni = 0; ni < Cfg::NI; ++ni)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int i = wi + ni * 8 + 2 * t + e;
+          if (i >= M) continue;
+          double v = alpha * acc[mi][ni][h * 2 + e];
+          if (beta != 0.0) v += beta * E[(int64_t)n * lde + i];
+          D[(int64_t)n * ldd + i] = v;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- gemm_nn
+// CTA tile 128 m x 128 n; 8 warps = 2 (m) x 4 (n); warp tile 64 m x 32 n.
+template <int VEC>
+struct NnCfg {
+  static constexpr int BM = 128, BN = 128;
+  static constexpr int PM = BM + 4;  // pitch of the m-contiguous X tile
+  static constexpr int A_ELEMS = kBK * PM;
+  static constexpr int B_ELEMS = BN * kPitchK;
+  static constexpr int STAGE = A_ELEMS + B_ELEMS;
+  static constexpr int SMEM = STAGE * kStages * 8;
+};
+
+template <int VEC>
+__device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const double* __restrict__ X,
+                                              int64_t ldx, const double* __restrict__ Y, int64_t ldy,
+                                              int M, int N, int K, int m0, int n0, int k0) {
+  using Cfg = NnCfg<VEC>;
+  const int tid = threadIdx.x;
+  constexpr int CPM = Cfg::BM / VEC;  // chunks per k-row of X
+  for (int c = tid; c < kBK * CPM; c += kThreads) {
+    const int kr = c / CPM, mc = (c % CPM) * VEC;
+    const int k = k0 + kr, m = m0 + mc;
+    const bool ok = (k < K) && (m < M);
+    const double* src = ok ? X + (int64_t)k * ldx + m : X;
+    double* dst = sA + kr * Cfg::PM + mc;
+    if constexpr (VEC == 2) {
+      const int sz = ok ? ((m + 1 < M) ? 16 : 8) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                   "r"(sz));
+    } else {
+      cp_async<8>(dst, src, ok);
+    }
+  }
+  constexpr int CPK = kBK / VEC;
+  for (int c = tid; c < Cfg::BN * CPK; c += kThreads) {
+    const int r = c / CPK, kc = (c % CPK) * VEC;
+    const int n = n0 + r, k = k0 + kc;
+    const bool ok = (n < N) && (k < K);
+    const double* src = ok ? Y + (int64_t)n * ldy + k : Y;
+    double* dst = sB + r * kPitchK + kc;
+    if constexpr (VEC == 2) {
+      const int sz = ok ? ((k + 1 < K) ? 16 : 8) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                   "r"(sz));
+    } else {
+      cp_async<8>(dst, src, ok);
+    }
+  }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_nn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
+                   const double* __restrict__ Y, int64_t ldy, double beta, const double* E,
+                   int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
+  using Cfg = NnCfg<VEC>;
+  extern __shared__ __align__(16) double smem[];
+  if (dyn.stop && *dyn.stop) return;
+  if (dyn.shift) {
+    const int sh = *dyn.shift;
+    N -= sh;
+    if (dyn.flags & kShiftB) Y += (int64_t)sh * ldy;
+    if (dyn.flags & kShiftD) {
+      D += (int64_t)sh * ldd;
+      if (E) E += (int64_t)sh * lde;
+    }
+  }
+  if ((int)blockIdx.y * Cfg::BN >= N) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
+  const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  const int nk = (int)cdiv(K, kBK);
+
+  double acc[4][4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < kStages - 1; ++s) {
+    if (s < nk) {
+      double* st = smem + s * Cfg::STAGE;
+      nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
+    }
+    cp_async_commit();
+  }
+  for (int kt = 0; kt < nk; ++kt) {
+    cp_async_wait<kStages - 2>();
+    __syncthreads();
+    {
+      const int ls = kt + kStages - 1;
+      if (ls < nk) {
+        double* st = smem + (ls % kStages) * Cfg::STAGE;
+        nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
+      }
+      cp_async_commit();
+    }
+    const double* sA = smem + (kt % kStages) * Cfg::STAGE;
+    const double* sB = sA + Cfg::A_ELEMS;
+#pragma unroll
+    for (int kk = 0; kk < kBK; kk += 4) {
+      double a[4][2], b[4];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi) {
+        a[mi][0] = sA[(kk + t) * Cfg::PM + wm + mi * 16 + g];
+        a[mi][1] = sA[(kk + t) * Cfg::PM + wm + mi * 16 + g + 8];
+      }
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj) b[nj] = sB[(wn + nj * 8 + g) * kPitchK + kk + t];
+#pragma unroll
+      for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+        for (int nj = 0; nj < 4; ++nj) dmma16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int mi = 0; mi < 4; ++mi)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int m = m0 + wm + mi * 16 + g + h * 8;
+      if (m >= M) continue;
+#pragma unroll
+      for (int nj = 0; nj < 4; ++nj)
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+          const int n = n0 + wn + nj * 8 + 2 * t + e;
+          if (n >= N) continue;
+          double v = alpha * acc[mi][nj][h * 2 + e];
+          if (beta != 0.0) v += beta * E[(int64_t)n * lde + m];
+          D[(int64_t)n * ldd + m] = v;
+        }
+    }
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+template <int MT, int VEC>
+int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* C,
+              int64_t ldc, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
+              double* ws, int64_t ws_bytes, GemmDyn dyn, cudaStream_t s) {
+  using Cfg = TnCfg<MT, VEC>;
+  static bool configured = false;
+  if (!configured) {
+    SQR_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<MT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::SMEM));
+    configured = true;
+  }
+  const int tiles = (int)cdiv(N, Cfg::BN);
+  const int sms = sm_count();
+  // Pick the split count that minimises waves/split (i.e. the padded work),
+  // keeping >= 512 K per split; ties go to fewer splits.
+  int best = 1;
+  double best_cost = 1e30;
+  const int max_split = std::max(1, std::min(sms, K / 512));
+  for (int sp = 1; sp <= max_split; ++sp) {
+    if ((int64_t)tiles * sp > 8LL * sms) break;  // bounded partial workspace
+    const double waves = (double)cdiv((int64_t)tiles * sp, sms);
+    const double cost = waves / sp + 0.02 * (sp > 1);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  int kchunk = (int)rup(cdiv(K, best), kBK);
+  int nsplit = (int)cdiv(K, kchunk);
+  if (nsplit < 1) nsplit = 1;
+  double* part = nullptr;
+  unsigned* sems = nullptr;
+  if (nsplit > 1) {
+    const int64_t need = (int64_t)tiles * nsplit * Cfg::ACC * kThreads * 8 + (int64_t)tiles * 4 + 16;
+    if (ws == nullptr || ws_bytes < need) {
+      nsplit = 1;
+      kchunk = K;
+    } else {
+      sems = reinterpret_cast<unsigned*>(ws);
+      part = ws + cdiv((int64_t)tiles * 4, 8) + 2;
+    }
+  }
+  if (nsplit == 1) kchunk = std::max(K, 1);
+  dim3 grid(tiles, nsplit);
+  gemm_tn_kernel<MT, VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, C, ldc, beta, E,
+                                                           lde, D, ldd, kchunk, part, sems, dyn);
+  SQR_LAUNCH("gemm_tn_kernel");
+  return SQR_OK;
+}
+
+template <int MT>
+int dispatch_tn_vec(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* C,
+                    int64_t ldc, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
+                    double* ws, int64_t ws_bytes, GemmDyn dyn, cudaStream_t s) {
+  const bool v2 = aligned16(X) && aligned16(C) && (ldx % 2 == 0) && (ldc % 2 == 0);
+  if (v2)
+    return launch_tn<MT, 2>(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
+  return launch_tn<MT, 1>(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
+}
+
+template <int VEC>
+int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* Y,
+              int64_t ldy, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
+              GemmDyn dyn, cudaStream_t s) {
+  using Cfg = NnCfg<VEC>;
+  static bool configured = false;
+  if (!configured) {
+    SQR_CUDA(cudaFuncSetAttribute(gemm_nn_kernel<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  Cfg::SMEM));
+    configured = true;
+  }
+  dim3 grid((unsigned)cdiv(M, Cfg::BM), (unsigned)cdiv(N, Cfg::BN));
+  gemm_nn_kernel<VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde,
+                                                       D, ldd, dyn);
+  SQR_LAUNCH("gemm_nn_kernel");
+  return SQR_OK;
+}
+
+}  // namespace
+
+int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+            const double* C, int64_t ldc, double beta, const double* E, int64_t lde, double* D,
+            int64_t ldd, double* ws, int64_t ws_bytes, cudaStream_t s, GemmDyn dyn) {
+  if (M <= 0 || N <= 0) return SQR_OK;
+  if (M > 144 || K < 0) {
+    set_error("gemm_tn: M=%lld must be in [1,144]", (long long)M);
+    return SQR_EINVAL;
+  }
+  if (beta != 0.0 && E == nullptr) E = D;
+  const int m = (int)M, n = (int)N, k = (int)K;
+#define SQR_TN(MT)                                                                                  \
+  if (M <= MT)                                                                                      \
+    return dispatch_tn_vec<MT>(m, n, k, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
+  SQR_TN(16) SQR_TN(32) SQR_TN(48) SQR_TN(64) SQR_TN(80) SQR_TN(96) SQR_TN(112) SQR_TN(128) SQR_TN(144)
+#undef SQR_TN
+  return SQR_EINVAL;
+}
+
+int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+            const double* Y, int64_t ldy, double beta, const double* E, int64_t lde, double* D,
+            int64_t ldd, cudaStream_t s, GemmDyn dyn) {
+  if (M <= 0 || N <= 0) return SQR_OK;
+  if (beta != 0.0 && E == nullptr) E = D;
+  const bool v2 = aligned16(X) && aligned16(Y) && (ldx % 2 == 0) && (ldy % 2 == 0);
+  if (v2) return launch_nn<2>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s);
+  return launch_nn<1>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s);
+}
+
+int64_t gemm_tn_workspace(int64_t N, int64_t /*K*/) {
+  const int64_t tiles = cdiv(N, 128);
+  return tiles * 148 * (2 * 9 * 4) * kThreads * 8 / 8 + tiles * 4 + 64;
+}
+
+}  // namespace sqr
+
+extern "C" int sqr_gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+                           const double* C, int64_t ldc, double beta, const double* E, int64_t lde,
+                           double* D, int64_t ldd, double* workspace, int64_t workspace_bytes,
+                           void* stream) {
+  return sqr::gemm_tn(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, workspace,
+                      workspace_bytes, static_cast<cudaStream_t>(stream), sqr::GemmDyn{});
+}
+
+extern "C" int sqr_gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+                           const double* Y, int64_t ldy, double beta, const double* E, int64_t lde,
+                           double* D, int64_t ldd, void* stream) {
+  return sqr::gemm_nn(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd,
+                      static_cast<cudaStream_t>(stream), sqr::GemmDyn{});
+}

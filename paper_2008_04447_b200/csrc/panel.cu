@@ -1,0 +1,366 @@
+// K4/K5: unpivoted Householder QR of a tall panel (randomized.py:107-130 for
+// the randomized drivers, reference.py:281-291 for qr_blocked) on one
+// persistent cooperative kernel, plus the compact-WY T factor
+// (householder.py:52-61).
+//
+// The mr x w panel is split by rows over G CTAs; each CTA keeps its row slab
+// of the current sub-panel (<= sw columns) in shared memory.  A column step
+// needs ONE grid-wide reduction: every CTA publishes, over its rows below the
+// pivot row, [sum a_r^2, sum a_r P_rc for the remaining sub-panel columns];
+// after the barrier every CTA sums the partials in the same fixed order and
+// rebuilds the identical reflector:
+//     nrm = sqrt(a_t^2 + s_a), beta = -sign(a_t) nrm, y0 = a_t - beta,
+//     y_r = a_r / y0, tau = 2 / (1 + s_a / y0^2),
+//     w_c = tau (P_tc + s_c / y0),   P_rc -= y_r w_c
+// (house_gen, householder.py:44-48, with y^T P expanded so one reduction
+// suffices).  Between sub-panels the finished sub-panel's reflectors are
+// applied to the rest of the panel in compact-WY form with one fixed-order
+// two-phase reduction of [Y_s^T Y_s | Y_s^T P_rest].  An exactly zero column
+// stops the panel (randomized.py:120-121) after the remaining panel columns
+// have received every earlier reflector, as in the reference loop.
+#include <math.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace sqr {
+namespace {
+
+constexpr int kPThreads = 256;
+constexpr int kPWarps = kPThreads / 32;
+
+struct PanelArgs {
+  double* P;
+  int64_t ldp;
+  int mr;      // panel rows
+  int wstat;   // panel width (<0: st->sample_achieved)
+  int wmax;    // columns of Y / taus to define (zero beyond bhat)
+  int sw, h, hp, stop_at_zero;
+  double* Y;
+  int64_t ldy;
+  double* taus;
+  sqr_status* st;
+  unsigned* bar;
+  double* part;   // [2][G][sw+1]   per-step partials
+  double* rowt;   // [2][sw+1]      pivot-row values
+  double* wpart;  // [G][sw*wmax]   WY partials
+  double* wred;   // [sw*wmax]      WY reduced
+};
+
+__global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double vals[136];
+  __shared__ double rowv[136];
+  __shared__ double wv[136];
+  if (a.st->stop) return;
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int w = a.wstat < 0 ? min(a.st->sample_achieved, a.wmax) : a.wstat;
+  const int row0 = g * a.h;
+  const int nrows = max(0, min(a.h, a.mr - row0));
+  GridBarrier gb;
+  gb.init(a.bar);
+  double* slab = sm;                              // sw x hp
+  double* Ts = slab + (size_t)a.sw * a.hp;        // sw x sw
+  double* GS = Ts + (size_t)a.sw * a.sw;          // swe x (swe + rest)
+  int bhat = w;
+  bool stopped = false;
+  int parity = 0;
+  int written = 0;  // Y columns [0, written) defined on my rows
+
+  for (int c0 = 0; c0 < w; c0 += a.sw) {
+    const int c1 = min(w, c0 + a.sw);
+    const int swe = c1 - c0;
+    for (int c = 0; c < swe; ++c)
+      for (int r = tid; r < nrows; r += kPThreads)
+        slab[c * a.hp + r] = a.P[(int64_t)(c0 + c) * a.ldp + row0 + r];
+    __syncthreads();
+
+    for (int t = c0; t < c1; ++t) {
+      const int tl = t - c0;
+      const int L = c1 - t;
+      const int par = parity;
+      parity ^= 1;
+      const int rbeg = max(0, t + 1 - row0);
+      for (int v = warp; v < L; v += kPWarps) {
+        const double* acol = slab + tl * a.hp;
+        const double* pcol = slab + (tl + v) * a.hp;
+        double s = 0.0;
+        for (int r = rbeg + lane; r < nrows; r += 32) s = fma(acol[r], pcol[r], s);
+        s = warp_sum(s);
+        if (lane == 0) a.part[((size_t)par * G + g) * (a.sw + 1) + v] = s;
+      }
+      if (t >= row0 && t < row0 + nrows) {
+        for (int v = tid; v < L; v += kPThreads)
+          a.rowt[par * (a.sw + 1) + v] = slab[(tl + v) * a.hp + (t - row0)];
+      }
+      gb.sync();
+      for (int v = warp; v < L; v += kPWarps) {
+        double s = 0.0;
+        for (int i = lane; i < G; i += 32) s += __ldcg(a.part + ((size_t)par * G + i) * (a.sw + 1) + v);
+        s = warp_sum(s);
+        if (lane == 0) vals[v] = s;
+      }
+      for (int v = tid; v < L; v += kPThreads) rowv[v] = __ldcg(a.rowt + par * (a.sw + 1) + v);
+      __syncthreads();
+      const double at = rowv[0], sa = vals[0];
+      const double nrm = sqrt(fma(at, at, sa));
+      if (nrm == 0.0 && a.stop_at_zero) {
+        bhat = t;
+        stopped = true;
+        break;
+      }
+      double beta = 0.0, tau = 0.0, y0 = 1.0;
+      if (nrm != 0.0) {
+        beta = (at >= 0.0 ? -1.0 : 1.0) * nrm;
+        y0 = at - beta;
+        tau = 2.0 / (1.0 + sa / (y0 * y0));
+      }
+      for (int v = 1 + tid; v < L; v += kPThreads) wv[v] = tau * (rowv[v] + vals[v] / y0);
+      if (g == 0 && tid == 0) a.taus[t] = tau;
+      __syncthreads();
+      for (int r = rbeg + tid; r < nrows; r += kPThreads) {
+        const double yr = nrm != 0.0 ? slab[tl * a.hp + r] / y0 : 0.0;
+        slab[tl * a.hp + r] = yr;
+        for (int v = 1; v < L; ++v) slab[(tl + v) * a.hp + r] = fma(-yr, wv[v], slab[(tl + v) * a.hp + r]);
+      }
+      if (t >= row0 && t < row0 + nrows && tid == 0) {
+        const int rt = t - row0;
+        for (int v = 1; v < L; ++v) slab[(tl + v) * a.hp + rt] -= wv[v];
+        slab[tl * a.hp + rt] = beta;
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    // Write the sub-panel back (packed R / reflector tails) and explicit Y.
+    for (int c = 0; c < swe; ++c) {
+      const int gc = c0 + c;
+      for (int r = tid; r < nrows; r += kPThreads) {
+        const int R = row0 + r;
+        const double v = slab[c * a.hp + r];
+        a.P[(int64_t)gc * a.ldp + R] = v;
+        double y = 0.0;
+        if (gc < bhat) y = R > gc ? v : (R == gc ? 1.0 : 0.0);
+        a.Y[(int64_t)gc * a.ldy + R] = y;
+      }
+    }
+    written = c1;
+    if (c1 >= w) break;
+    // ---- compact-WY update of panel columns [c1, w) with this sub-panel.
+    const int rest = w - c1;
+    const int ncoef = swe * (swe + rest);
+    for (int e = tid; e < ncoef; e += kPThreads) {
+      const int ai = e % swe, cj = e / swe;
+      const int gca = c0 + ai;
+      double s = 0.0;
+      if (gca < bhat) {
+        if (cj < swe) {
+          const int gcb = c0 + cj;
+          if (gcb < bhat) {
+            for (int r = max(0, max(gca, gcb) - row0); r < nrows; ++r) {
+              const int R = row0 + r;
+              const double ya = R > gca ? slab[ai * a.hp + r] : 1.0;
+              const double yb = R > gcb ? slab[cj * a.hp + r] : 1.0;
+              s = fma(ya, yb, s);
+            }
+          }
+        } else {
+          const double* pcol = a.P + (int64_t)(c1 + cj - swe) * a.ldp + row0;
+          for (int r = max(0, gca - row0); r < nrows; ++r) {
+            const int R = row0 + r;
+            const double ya = R > gca ? slab[ai * a.hp + r] : 1.0;
+            s = fma(ya, pcol[r], s);
+          }
+        }
+      }
+      a.wpart[(size_t)g * ncoef + e] = s;
+    }
+    gb.sync();
+    {
+      const int per = (int)cdiv(ncoef, G);
+      for (int e = g * per + tid; e < min(ncoef, (g + 1) * per); e += kPThreads) {
+        double s = 0.0;
+        for (int i = 0; i < G; ++i) s += __ldcg(a.wpart + (size_t)i * ncoef + e);
+        a.wred[e] = s;
+      }
+    }
+    gb.sync();
+    for (int e = tid; e < ncoef; e += kPThreads) GS[e] = __ldcg(a.wred + e);
+    for (int e = tid; e < a.sw * a.sw; e += kPThreads) Ts[e] = 0.0;
+    __syncthreads();
+    // T_s recurrence (householder.py:56-60): T[i,c] = -tau_c sum_{l=i}^{c-1} T[i,l] G[l,c].
+    for (int c = 0; c < swe; ++c) {
+      const double tc = (c0 + c < bhat) ? __ldcg(a.taus + c0 + c) : 0.0;
+      for (int i = warp; i < c; i += kPWarps) {
+        double s = 0.0;
+        for (int l = i + lane; l < c; l += 32) s = fma(Ts[l * a.sw + i], GS[c * swe + l], s);
+        s = warp_sum(s);
+        if (lane == 0) Ts[c * a.sw + i] = -tc * s;
+      }
+      if (tid == 0) Ts[c * a.sw + c] = tc;
+      __syncthreads();
+    }
+    // W = T^T S in place over S, one column at a time.
+    for (int j = 0; j < rest; ++j) {
+      double* Sj = GS + (size_t)(swe + j) * swe;
+      double acc = 0.0;
+      if (tid < swe)
+        for (int l = 0; l <= tid; ++l) acc = fma(Ts[tid * a.sw + l], Sj[l], acc);
+      __syncthreads();
+      if (tid < swe) Sj[tid] = acc;
+    }
+    __syncthreads();
+    // P_rest -= Y_s W on my rows.
+    for (int j = 0; j < rest; ++j) {
+      const double* Wj = GS + (size_t)(swe + j) * swe;
+      double* pcol = a.P + (int64_t)(c1 + j) * a.ldp + row0;
+      for (int r = tid; r < nrows; r += kPThreads) {
+        const int R = row0 + r;
+        if (R < c0) continue;
+        double s = 0.0;
+        const int amax = min(swe, min(bhat - c0, R - c0 + 1));
+        for (int ai = 0; ai < amax; ++ai) {
+          const double ya = (R > c0 + ai) ? slab[ai * a.hp + r] : 1.0;
+          s = fma(ya, Wj[ai], s);
+        }
+        pcol[r] -= s;
+      }
+    }
+    __syncthreads();
+    if (stopped) break;
+  }
+  // Undefined Y columns (never reached, or beyond the dynamic width) are zero.
+  for (int c = written; c < a.wmax; ++c)
+    for (int r = tid; r < nrows; r += kPThreads) a.Y[(int64_t)c * a.ldy + row0 + r] = 0.0;
+  if (g == 0 && tid == 0) {
+    a.st->bhat = bhat;
+    for (int c = bhat; c < a.wmax; ++c) a.taus[c] = 0.0;
+    if (bhat == 0 && a.stop_at_zero) {
+      a.st->stop = 1;
+      a.st->reason = SQR_STOP_PANEL_ZERO;
+    }
+  }
+}
+
+// T from G = Y^T Y and taus (one CTA).  T[c,c] = tau_c,
+// T[:c, c] = -tau_c T[:c,:c] G[:c, c]  (householder.py:52-61).
+constexpr int kTThreads = 512;
+__global__ void __launch_bounds__(kTThreads, 1)
+    build_t_kernel(const double* Gm, int64_t ldg, const double* taus, int j, double* T, int64_t ldt,
+                   const int32_t* gate) {
+  extern __shared__ __align__(16) double Ts[];
+  if (gate && *gate) return;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kTThreads / 32;
+  const int ld = j | 1;
+  for (int e = tid; e < ld * j; e += kTThreads) Ts[e] = 0.0;
+  __syncthreads();
+  for (int c = 0; c < j; ++c) {
+    const double tc = taus[c];
+    for (int i = warp; i < c; i += nw) {
+      double s = 0.0;
+      for (int l = i + lane; l < c; l += 32) s = fma(Ts[l * ld + i], Gm[(int64_t)c * ldg + l], s);
+      s = warp_sum(s);
+      if (lane == 0) Ts[c * ld + i] = -tc * s;
+    }
+    if (tid == 0) Ts[c * ld + c] = tc;
+    __syncthreads();
+  }
+  for (int e = tid; e < j * j; e += kTThreads) {
+    const int r = e % j, c = e / j;
+    T[(int64_t)c * ldt + r] = Ts[c * ld + r];
+  }
+}
+
+}  // namespace
+
+int64_t panel_workspace(int64_t w) {
+  const int64_t G = 148, sw = 128;
+  return 64 + 2 * G * (sw + 1) * 8 + 2 * (sw + 1) * 8 + G * sw * std::max<int64_t>(w, 1) * 8 +
+         sw * std::max<int64_t>(w, 1) * 8 + 4096;
+}
+
+// Rows per CTA >= 64 and at most one CTA per SM; the largest sub-panel width
+// whose slab + WY scratch fits in shared memory.
+int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
+             double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes,
+             cudaStream_t s) {
+  if (mr <= 0 || wmax <= 0) return SQR_OK;
+  if (wmax > 128) {
+    set_error("panel_qr: width %lld > 128", (long long)wmax);
+    return SQR_EINVAL;
+  }
+  if (ws_bytes < panel_workspace(wmax)) {
+    set_error("panel_qr: workspace too small");
+    return SQR_EINVAL;
+  }
+  const int sms = sm_count();
+  int G = (int)std::min<int64_t>(sms, std::max<int64_t>(1, cdiv(mr, 64)));
+  const int h = (int)cdiv(mr, G);
+  G = (int)cdiv(mr, h);
+  const int hp = h | 1;
+  const int64_t budget = std::min<int64_t>(max_smem_optin(), 224 * 1024) - 256;
+  int sw = 0;
+  for (int cand : {128, 64, 32, 16, 8, 4, 2, 1}) {
+    const int64_t swc = std::min<int64_t>(cand, wmax);
+    const int64_t need = (swc * hp + swc * swc + swc * wmax) * 8;
+    if (need <= budget) {
+      sw = (int)swc;
+      break;
+    }
+  }
+  if (sw == 0) {
+    set_error("panel_qr: panel of %lld rows does not fit shared memory", (long long)mr);
+    return SQR_EINVAL;
+  }
+  const int64_t smem = ((int64_t)sw * hp + (int64_t)sw * sw + (int64_t)sw * wmax) * 8;
+  PanelArgs a;
+  a.P = P;
+  a.ldp = ldp;
+  a.mr = (int)mr;
+  a.wstat = (int)w;
+  a.wmax = (int)wmax;
+  a.sw = sw;
+  a.h = h;
+  a.hp = hp;
+  a.stop_at_zero = stop_at_zero;
+  a.Y = Y;
+  a.ldy = ldy;
+  a.taus = taus;
+  a.st = st;
+  char* p = static_cast<char*>(ws);
+  a.bar = reinterpret_cast<unsigned*>(p);
+  p += 64;
+  a.part = reinterpret_cast<double*>(p);
+  p += 2 * 148 * (128 + 1) * 8;
+  a.rowt = reinterpret_cast<double*>(p);
+  p += 2 * (128 + 1) * 8;
+  a.wpart = reinterpret_cast<double*>(p);
+  p += (int64_t)148 * 128 * wmax * 8;
+  a.wred = reinterpret_cast<double*>(p);
+  static int configured = 0;
+  if (smem > configured) {
+    SQR_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = (int)smem;
+  }
+  void* args[] = {&a};
+  SQR_CUDA(cudaLaunchCooperativeKernel((const void*)panel_kernel, dim3(G), dim3(kPThreads), args,
+                                       (size_t)smem, s));
+  return SQR_OK;
+}
+
+int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
+            const int32_t* gate, cudaStream_t s) {
+  if (j <= 0) return SQR_OK;
+  const int64_t smem = (int64_t)(j | 1) * j * 8;
+  static int configured = 0;
+  if (smem > configured) {
+    SQR_CUDA(cudaFuncSetAttribute(build_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    configured = (int)smem;
+  }
+  build_t_kernel<<<1, kTThreads, smem, s>>>(Gm, ldg, taus, (int)j, T, ldt, gate);
+  SQR_LAUNCH("build_t_kernel");
+  return SQR_OK;
+}
+
+}  // namespace sqr
