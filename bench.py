@@ -1,0 +1,307 @@
+#!/usr/bin/env python
+"""Benchmark: RQRCP fp64 GFLOP/s at n = 32768 on B200 (BASELINE.json configs[4]).
+
+One "step" = one full rank-revealing factorisation rqrcp(A, k=32768, b=128,
+p=8, seed=0) of a 32768 x 32768 fp64 giid matrix through the package's public
+API with A already resident in HBM (the call copies A, as the reference
+does, so every step factors the same input).  GFLOP/s uses the LAPACK
+DGEQP3/DGEQRF convention 2mn^2 - 2n^3/3 (46,912.5 GFLOP at C5); the
+algorithmic count of SURVEY.md §8(d) is reported alongside.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port of sketchqr, oracle/port.py, NumPy/OpenBLAS on all host cores) on
+a bounded sample of the same workload (full RQRCP of a 4096 x 4096 giid
+matrix, b=128, p=8), same metric and unit.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RQRCP/TRQRCP fp64 GFLOP/s (n=32768) at 1/2/4/8 B200; TUXV time-to-rank-k"
+PEAK_FP64_TFLOPS = 37.0   # builder-measured DMMA microbenchmark, profiles/fp64_peak_r01.log
+PEAK_SOURCE = ("builder-measured fp64 DMMA peak (mma.sync f64 microbenchmark, profiles/fp64_peak_r01.log; "
+               "cuBLAS DGEMM 8192^3 = 35.4 TF); MEASURED_PEAKS.json has no fp64 entry")
+
+
+def lapack_gflop(m, n):
+    """2mn^2 - 2n^3/3 for m >= n (DGEQRF / DGEQP3 convention)."""
+    return (2.0 * m * n * n - 2.0 * n ** 3 / 3.0) / 1e9
+
+
+def rqrcp_flops_by_kernel(m, n, k, b, p):
+    """Algorithmic flops per step of the GEMM kernel classes."""
+    ell = b + p
+    tn = 2.0 * ell * m * n  # sketch
+    nn = 0.0
+    total = 2.0 * ell * m * n
+    for i0 in range(0, k, b):
+        bb = min(b, k - i0)
+        mr, nt_ = m - i0, n - i0
+        ntr = nt_ - bb
+        tn += 2.0 * bb * bb * mr            # G = Y^T Y for T
+        total += sum(4.0 * (ell - t) * (nt_ - t) for t in range(bb))   # sample QRCP
+        total += sum(4.0 * (mr - t) * (bb - t - 1) + 3.0 * (mr - t) for t in range(bb))  # panel
+        total += mr * bb * bb               # T
+        if ntr > 0:
+            tn += 2.0 * bb * mr * ntr + 2.0 * bb * bb * ntr   # Y^T C, T^T W
+            nn += 2.0 * bb * mr * ntr                          # C -= Y W
+            total += 4.0 * bb * mr * ntr + 2.0 * bb * bb * ntr + 3.0 * bb * bb * ntr
+    return {"gemm_tn": tn, "gemm_nn": nn, "algorithmic_total": total}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out = self.proc.communicate(timeout=5)[0]
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out = ""
+            self.lines = [ln for ln in out.strip().splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            try:
+                sm.append(float(f[0]))
+                smax = max(smax, float(f[1]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------- CPU baselines
+def cpu_sample(n_sample, b, p, reps=1):
+    """Oracle port (NumPy -> OpenBLAS, all host threads) on a bounded sample."""
+    from oracle import port as O
+    A = O.gauss_matrix(n_sample, n_sample, 5)
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        O.rqrcp(A, n_sample, b=b, p=p, seed=0)
+        times.append(time.perf_counter() - t0)
+    return lapack_gflop(n_sample, n_sample), times
+
+
+def host_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        th = [i.get("num_threads") for i in threadpool_info() if i.get("internal_api") == "openblas"]
+        if th:
+            return int(th[0])
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    n_s = args.cpu_sample_n
+    gflop, _ = cpu_sample(max(256, n_s // 8), args.b, args.p)  # import / first-touch warm-up
+    times = []
+    for i in range(args.warmup + args.steps):
+        g, t = cpu_sample(n_s, args.b, args.p)
+        if i >= args.warmup:
+            times.append(t[0])
+    t = float(np.mean(times))
+    value = g / t
+    sample = f"full rqrcp of giid({n_s},{n_s},seed=5), b={args.b}, p={args.p}, oracle port (NumPy/OpenBLAS)"
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": f"rqrcp n={n_s} (bounded CPU sample of C5 n=32768)", "b": args.b, "p": args.p,
+                   "flop_convention": "LAPACK 2mn^2-2n^3/3"},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": host_cores(), "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        from paper_2008_04447_b200 import distributed
+        return distributed.bench_main(args, METRIC, PEAK_FP64_TFLOPS, PEAK_SOURCE)
+    torch.cuda.set_device(local)
+    import paper_2008_04447_b200 as G
+    from paper_2008_04447_b200 import _lib
+    L = _lib.lib()
+    dev = torch.device("cuda", local)
+    m = n = args.n
+    k, b, p = n, args.b, args.p
+    A = G.device_giid(m, n, seed=5, device=dev)  # (m, n) column-major view
+    torch.cuda.synchronize()
+
+    def step(Ain):
+        return G.rqrcp(Ain, k, b=b, p=p, seed=0)
+
+    for _ in range(args.warmup):
+        pf = step(A)
+        del pf
+    torch.cuda.synchronize()
+    launches0 = L.sqr_launch_count()
+    L.sqr_profile_enable(20000 * max(1, args.steps))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(args.steps):
+            pf = step(A)
+            ach = pf.achieved_rank
+            del pf
+        e1.record()
+        torch.cuda.synchronize()
+    launches = L.sqr_launch_count() - launches0
+    prof = _lib.profile_collect()
+    L.sqr_profile_enable(0)
+    ms = e0.elapsed_time(e1) / args.steps
+    gflop = lapack_gflop(m, n)
+    value = gflop / (ms / 1e3)
+
+    fl = rqrcp_flops_by_kernel(m, n, k, b, p)
+    dom = max(("gemm_tn", "gemm_nn"), key=lambda t: prof[t][0])
+    dom_ms = prof[dom][0] / args.steps
+    achieved_tf = fl[dom] / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf, "peak": PEAK_FP64_TFLOPS,
+                "unit": "TFLOP/s", "frac": (achieved_tf / PEAK_FP64_TFLOPS) if achieved_tf else None,
+                "traffic": traffic, "peak_source": PEAK_SOURCE,
+                "launches_per_step": prof[dom][1] / args.steps,
+                "flops_per_step": fl[dom]}
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if args.e2e_steps > 0:
+        A_host = torch.empty((n, m), dtype=torch.float64, pin_memory=True)  # column-major A
+        A_host.copy_(A.T)  # A is an (m, n) transposed view of (n, m) storage
+        R_host = torch.empty((n, n), dtype=torch.float64, pin_memory=True)
+        P_host = torch.empty(n, dtype=torch.int64, pin_memory=True)
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            Ad = A_host.to(dev, non_blocking=True).T     # H2D of the step's input
+            pf = G.rqrcp(Ad, k, b=b, p=p, seed=0)
+            R_host[: pf.achieved_rank].copy_(pf.R_device(), non_blocking=True)  # D2H of R
+            P_host.copy_(pf.perm_device(), non_blocking=True)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+            del pf, Ad
+        t_e2e = float(np.median(ts))
+        e2e = {"value": gflop / t_e2e, "unit": "GFLOP/s", "h2d_bytes_per_step": int(m * n * 8),
+               "d2h_bytes_per_step": int(ach * n * 8 + n * 8), "ms_per_step": t_e2e * 1e3,
+               "steps": args.e2e_steps}
+        del A_host, R_host
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        g_s, t_s = cpu_sample(args.cpu_sample_n, b, p)
+        cpu = {"value": g_s / t_s[0], "unit": "GFLOP/s", "cores": host_cores(), "kind": "port",
+               "sample": f"oracle port rqrcp on giid({args.cpu_sample_n},{args.cpu_sample_n},seed=5), b={b}, "
+                         f"p={p} (full rank), {t_s[0]:.1f} s"}
+
+    phases = {t: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+              for t, v in prof.items() if v[1]}
+    line = {
+        "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "C5: rqrcp(A, k=32768, b=128, p=8, seed=0), A = giid(32768, 32768, seed=5) "
+                               "from the reference stream generated on device",
+                   "m": m, "n": n, "k": k, "b": b, "p": p, "parallelism": "single GPU",
+                   "flop_convention": "LAPACK 2mn^2-2n^3/3 = %.1f GFLOP" % gflop,
+                   "algorithmic_gflop": fl["algorithmic_total"] / 1e9,
+                   "l2": "inputs (8.6 GB) larger than L2 (126 MB); no flush needed",
+                   "achieved_rank": ach},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "phases": phases,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--b", type=int, default=128)
+    ap.add_argument("--p", type=int, default=8)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample-n", type=int, default=4096)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -61,6 +61,14 @@ const char* sqr_version(void);
 const char* sqr_last_error(void);
 int sqr_device_sm_count(void);
 
+/* Kernels launched by this library since load (bench.py's gpu_launches). */
+int64_t sqr_launch_count(void);
+/* Per-kernel-class CUDA-event timing of the next <= max_launches launches
+ * (0 disables).  Classes: 0 gemm_tn, 1 gemm_nn, 2 sample_qrcp, 3 panel,
+ * 4 build_t, 5 apply_moves, 6 sample_update, 7 gaussian, 8 misc. */
+int sqr_profile_enable(int64_t max_launches);
+int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, int ntags);
+
 /* ------------------------------------------------------------ RNG (L0)
  * Omega[i, t] = normal(seed, offset + i + t*rows) for a rows x cols matrix
  * filled column-major (rng.py:49-70, NormalStream.matrix rng.py:90-93).

@@ -26,6 +26,9 @@ SIGNATURES = {
     "sqr_version": (ctypes.c_char_p, []),
     "sqr_last_error": (ctypes.c_char_p, []),
     "sqr_device_sm_count": (c_int, []),
+    "sqr_launch_count": (c_i64, []),
+    "sqr_profile_enable": (c_int, [c_i64]),
+    "sqr_profile_collect": (c_int, [c_ptr, c_ptr, c_int]),
     "sqr_gaussian": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_u64, c_u64, c_int, c_ptr]),
     "sqr_gemm_tn": (c_int, [c_i64, c_i64, c_i64, c_dbl, c_ptr, c_i64, c_ptr, c_i64, c_dbl, c_ptr, c_i64,
                             c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
@@ -95,3 +98,15 @@ def check(rc: int, what: str = "libsqr") -> None:
         if rc == 1:
             raise ValueError(f"{what}: {msg}")
         raise RuntimeError(f"{what} failed (rc={rc}): {msg}")
+
+
+PROFILE_TAGS = ["gemm_tn", "gemm_nn", "sample_qrcp", "panel", "build_t", "apply_moves", "sample_update",
+                "gaussian", "misc"]
+
+
+def profile_collect():
+    """{class: (ms, launches)} since sqr_profile_enable."""
+    ms = (ctypes.c_double * 16)()
+    cnt = (ctypes.c_int64 * 16)()
+    lib().sqr_profile_collect(ms, cnt, 16)
+    return {t: (ms[i], cnt[i]) for i, t in enumerate(PROFILE_TAGS)}

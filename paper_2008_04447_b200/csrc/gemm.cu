@@ -216,14 +216,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ---------------------------------------------------------------- gemm_nn
 // CTA tile 128 m x 128 n; 8 warps = 2 (m) x 4 (n); warp tile 64 m x 32 n.
+// The E tile (the trailing matrix C in C -= Y W) is streamed into shared
+// memory in 1/nk slices riding along with the k-stages, so its HBM read
+// overlaps the MMAs instead of being exposed in the epilogue.
+constexpr int kStagesNN = 2;
 template <int VEC>
 struct NnCfg {
   static constexpr int BM = 128, BN = 128;
-  static constexpr int PM = BM + 4;  // pitch of the m-contiguous X tile
+  static constexpr int PM = BM + 4;   // pitch of the m-contiguous X tile (4 mod 16)
+  static constexpr int PC = BM + 2;   // pitch of the E tile (2 mod 16: conflict-free epilogue)
   static constexpr int A_ELEMS = kBK * PM;
   static constexpr int B_ELEMS = BN * kPitchK;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int SMEM = STAGE * kStages * 8;
+  static constexpr int C_ELEMS = BN * PC;
+  static constexpr int SMEM = (STAGE * kStagesNN + C_ELEMS) * 8;
 };
 
 template <int VEC>
@@ -264,6 +270,29 @@ __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const doub
   }
 }
 
+// Columns [c0, c1) of the E tile into shared memory.
+template <int VEC>
+__device__ __forceinline__ void nn_load_e(double* sC, const double* __restrict__ E, int64_t lde, int M, int N,
+                                          int m0, int n0, int c0, int c1) {
+  using Cfg = NnCfg<VEC>;
+  constexpr int CPM = Cfg::BM / VEC;
+  const int tid = threadIdx.x;
+  for (int c = tid; c < (c1 - c0) * CPM; c += kThreads) {
+    const int cn = c0 + c / CPM, mc = (c % CPM) * VEC;
+    const int n = n0 + cn, m = m0 + mc;
+    const bool ok = (n < N) && (m < M);
+    const double* src = ok ? E + (int64_t)n * lde + m : E;
+    double* dst = sC + cn * Cfg::PC + mc;
+    if constexpr (VEC == 2) {
+      const int sz = ok ? ((m + 1 < M) ? 16 : 8) : 0;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
+                   "r"(sz));
+    } else {
+      cp_async<8>(dst, src, ok);
+    }
+  }
+}
+
 template <int VEC>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_nn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
@@ -287,6 +316,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
   const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
   const int nk = (int)cdiv(K, kBK);
+  double* sC = smem + kStagesNN * Cfg::STAGE;
+  const bool use_e = beta != 0.0;
+  const int cps = nk > 0 ? (int)cdiv(Cfg::BN, nk) : Cfg::BN;  // E columns per k-stage
 
   double acc[4][4][4];
 #pragma unroll
@@ -296,26 +328,30 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
 
+  if (nk == 0 && use_e) nn_load_e<VEC>(sC, E, lde, M, N, m0, n0, 0, Cfg::BN);
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < kStagesNN - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * Cfg::STAGE;
       nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
+      if (use_e) nn_load_e<VEC>(sC, E, lde, M, N, m0, n0, min(Cfg::BN, s * cps), min(Cfg::BN, (s + 1) * cps));
     }
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<kStages - 2>();
+    cp_async_wait<kStagesNN - 2>();
     __syncthreads();
     {
-      const int ls = kt + kStages - 1;
+      const int ls = kt + kStagesNN - 1;
       if (ls < nk) {
-        double* st = smem + (ls % kStages) * Cfg::STAGE;
+        double* st = smem + (ls % kStagesNN) * Cfg::STAGE;
         nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
+        if (use_e)
+          nn_load_e<VEC>(sC, E, lde, M, N, m0, n0, min(Cfg::BN, ls * cps), min(Cfg::BN, (ls + 1) * cps));
       }
       cp_async_commit();
     }
-    const double* sA = smem + (kt % kStages) * Cfg::STAGE;
+    const double* sA = smem + (kt % kStagesNN) * Cfg::STAGE;
     const double* sB = sA + Cfg::A_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) {
@@ -332,23 +368,28 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int nj = 0; nj < 4; ++nj) dmma16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
     }
+    // The next iteration refills this stage: everyone must be done reading it.
+    if (kStagesNN == 2) __syncthreads();
   }
   cp_async_wait<0>();
+  __syncthreads();
 
 #pragma unroll
   for (int mi = 0; mi < 4; ++mi)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int m = m0 + wm + mi * 16 + g + h * 8;
+      const int ml = wm + mi * 16 + g + h * 8;
+      const int m = m0 + ml;
       if (m >= M) continue;
 #pragma unroll
       for (int nj = 0; nj < 4; ++nj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int n = n0 + wn + nj * 8 + 2 * t + e;
+          const int nl = wn + nj * 8 + 2 * t + e;
+          const int n = n0 + nl;
           if (n >= N) continue;
           double v = alpha * acc[mi][nj][h * 2 + e];
-          if (beta != 0.0) v += beta * E[(int64_t)n * lde + m];
+          if (use_e) v = fma(beta, sC[nl * Cfg::PC + ml], v);
           D[(int64_t)n * ldd + m] = v;
         }
     }
@@ -400,6 +441,7 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
   }
   if (nsplit == 1) kchunk = std::max(K, 1);
   dim3 grid(tiles, nsplit);
+  ProfScope ps(kTagGemmTn, s);
   gemm_tn_kernel<MT, VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, C, ldc, beta, E,
                                                            lde, D, ldd, kchunk, part, sems, dyn);
   SQR_LAUNCH("gemm_tn_kernel");
@@ -428,6 +470,7 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
     configured = true;
   }
   dim3 grid((unsigned)cdiv(M, Cfg::BM), (unsigned)cdiv(N, Cfg::BN));
+  ProfScope ps(kTagGemmNn, s);
   gemm_nn_kernel<VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde,
                                                        D, ldd, dyn);
   SQR_LAUNCH("gemm_nn_kernel");
@@ -459,7 +502,8 @@ int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int6
             int64_t ldd, cudaStream_t s, GemmDyn dyn) {
   if (M <= 0 || N <= 0) return SQR_OK;
   if (beta != 0.0 && E == nullptr) E = D;
-  const bool v2 = aligned16(X) && aligned16(Y) && (ldx % 2 == 0) && (ldy % 2 == 0);
+  const bool v2 = aligned16(X) && aligned16(Y) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
+                  (beta == 0.0 || (aligned16(E) && lde % 2 == 0));
   if (v2) return launch_nn<2>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s);
   return launch_nn<1>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s);
 }

@@ -9,7 +9,9 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "common.cuh"
 
@@ -27,6 +29,36 @@ void set_error(const char* fmt, ...) {
 int check_cuda(cudaError_t e, const char* what) {
   set_error("%s: %s", what, cudaGetErrorString(e));
   return SQR_ECUDA;
+}
+
+// ------------------------------------------------------------ accounting
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+namespace {
+struct Profiler {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> tags;
+  size_t used = 0;
+  cudaEvent_t pending[kNumTags] = {};
+};
+Profiler g_prof;
+}  // namespace
+
+void prof_begin(int tag, cudaStream_t s) {
+  if (!g_prof.on || g_prof.used + 2 > g_prof.ev.size()) return;
+  cudaEvent_t e = g_prof.ev[g_prof.used];
+  cudaEventRecord(e, s);
+  g_prof.pending[tag] = e;
+}
+void prof_end(int tag, cudaStream_t s) {
+  if (!g_prof.on || g_prof.pending[tag] == nullptr || g_prof.used + 2 > g_prof.ev.size()) return;
+  cudaEvent_t e = g_prof.ev[g_prof.used + 1];
+  cudaEventRecord(e, s);
+  g_prof.tags.push_back(tag);
+  g_prof.used += 2;
+  g_prof.pending[tag] = nullptr;
 }
 
 int sm_count() {
@@ -235,6 +267,7 @@ int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
   const int64_t total = rows * cols;
   if (total <= 0) return SQR_OK;
   const int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sm_count() * 16);
+  ProfScope ps(kTagGaussian, s);
   gaussian_kernel<<<blocks, 256, 0, s>>>(out, ld, rows, cols, seed, offset, transpose, gate);
   SQR_LAUNCH("gaussian_kernel");
   return SQR_OK;
@@ -250,6 +283,7 @@ int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm
     configured = smem;
   }
   const int blocks = (int)std::max<int64_t>(1, cdiv(rows, kMoveRows));
+  ProfScope ps(kTagMoves, s);
   apply_moves_kernel<<<blocks, 256, smem, s>>>(X, ld, rows, col0, perm, moves, st);
   SQR_LAUNCH("apply_moves_kernel");
   return SQR_OK;
@@ -265,6 +299,7 @@ int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, 
                                   (int)smem));
     configured = smem;
   }
+  ProfScope ps(kTagSampleUpd, s);
   sample_update_kernel<<<(unsigned)cdiv(nt, kSuCols), kSuThreads, smem, s>>>(Bf, ldbf, (int)ell, R, ldr,
                                                                            (int)nt, Bn, ldbn, st);
   SQR_LAUNCH("sample_update_kernel");
@@ -272,6 +307,7 @@ int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, 
 }
 
 int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s) {
+  ProfScope ps(kTagMisc, s);
   finish_block_kernel<<<1, 1, 0, s>>>(st, widths, i0, bb, k, n);
   SQR_LAUNCH("finish_block_kernel");
   return SQR_OK;
@@ -280,6 +316,7 @@ int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, 
 int copy_upper(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, const int32_t* gate,
                cudaStream_t s) {
   if (n <= 0) return SQR_OK;
+  ProfScope ps(kTagMisc, s);
   copy_upper_kernel<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 256), 256, 0, s>>>(src, lds, dst, ldd, (int)n,
                                                                                      gate);
   SQR_LAUNCH("copy_upper_kernel");
@@ -288,6 +325,7 @@ int copy_upper(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t
 
 int iota(int64_t* p, int64_t n, cudaStream_t s) {
   if (n <= 0) return SQR_OK;
+  ProfScope ps(kTagMisc, s);
   iota_kernel<<<(unsigned)std::min<int64_t>(cdiv(n, 256), 1024), 256, 0, s>>>(p, n);
   SQR_LAUNCH("iota_kernel");
   return SQR_OK;
@@ -313,4 +351,44 @@ extern "C" int sqr_apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0
 extern "C" int sqr_sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr,
                                  int64_t nt, double* Bnext, int64_t ldbn, sqr_status* st, void* stream) {
   return sqr::sample_update(Bf, ldbf, ell, R, ldr, nt, ell, Bnext, ldbn, st, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t sqr_launch_count(void) { return sqr::g_launches.load(); }
+
+extern "C" int sqr_profile_enable(int64_t max_launches) {
+  using sqr::g_prof;
+  for (auto e : g_prof.ev) cudaEventDestroy(e);
+  g_prof.ev.clear();
+  g_prof.tags.clear();
+  g_prof.used = 0;
+  for (auto& p : g_prof.pending) p = nullptr;
+  g_prof.on = max_launches > 0;
+  if (!g_prof.on) return SQR_OK;
+  g_prof.ev.resize(2 * max_launches);
+  for (auto& e : g_prof.ev)
+    if (cudaEventCreate(&e) != cudaSuccess) return sqr::check_cuda(cudaGetLastError(), "cudaEventCreate");
+  return SQR_OK;
+}
+
+// Sum of device time (ms) and launch count per kernel class since
+// sqr_profile_enable; synchronises on the recorded events, then resets.
+extern "C" int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, int ntags) {
+  using sqr::g_prof;
+  for (int t = 0; t < ntags; ++t) {
+    ms_per_tag[t] = 0.0;
+    count_per_tag[t] = 0;
+  }
+  for (size_t i = 0; i < g_prof.tags.size(); ++i) {
+    float ms = 0.f;
+    cudaEventSynchronize(g_prof.ev[2 * i + 1]);
+    if (cudaEventElapsedTime(&ms, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]) != cudaSuccess) continue;
+    const int t = g_prof.tags[i];
+    if (t < ntags) {
+      ms_per_tag[t] += ms;
+      count_per_tag[t] += 1;
+    }
+  }
+  g_prof.tags.clear();
+  g_prof.used = 0;
+  return SQR_OK;
 }

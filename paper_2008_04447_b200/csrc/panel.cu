@@ -29,6 +29,7 @@ namespace {
 
 constexpr int kPThreads = 256;
 constexpr int kPWarps = kPThreads / 32;
+constexpr int kMaxG = 152;  // >= SM count, multiple of 8
 
 struct PanelArgs {
   double* P;
@@ -42,7 +43,7 @@ struct PanelArgs {
   double* taus;
   sqr_status* st;
   unsigned* bar;
-  double* part;   // [2][G][sw+1]   per-step partials
+  double* part;   // [2][sw+1][G]   per-step partials (value-major)
   double* rowt;   // [2][sw+1]      pivot-row values
   double* wpart;  // [G][sw*wmax]   WY partials
   double* wred;   // [sw*wmax]      WY reduced
@@ -89,18 +90,31 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
         double s = 0.0;
         for (int r = rbeg + lane; r < nrows; r += 32) s = fma(acol[r], pcol[r], s);
         s = warp_sum(s);
-        if (lane == 0) a.part[((size_t)par * G + g) * (a.sw + 1) + v] = s;
+        if (lane == 0) a.part[((size_t)par * (a.sw + 1) + v) * G + g] = s;
       }
       if (t >= row0 && t < row0 + nrows) {
         for (int v = tid; v < L; v += kPThreads)
           a.rowt[par * (a.sw + 1) + v] = slab[(tl + v) * a.hp + (t - row0)];
       }
       gb.sync();
-      for (int v = warp; v < L; v += kPWarps) {
+      // Fixed-order reduction of the G partials of every value: 8 lanes per
+      // value, each summing G/8 partials whose loads are all in flight at once.
+      for (int v0 = 0; v0 < L; v0 += kPThreads / 8) {
+        const int v = v0 + (tid >> 3), q = tid & 7;
+        double x[kMaxG / 8];
+        const double* src = a.part + ((size_t)par * (a.sw + 1) + v) * G;
+#pragma unroll
+        for (int i = 0; i < kMaxG / 8; ++i) {
+          const int gi = q + 8 * i;
+          x[i] = (v < L && gi < G) ? __ldcg(src + gi) : 0.0;
+        }
         double s = 0.0;
-        for (int i = lane; i < G; i += 32) s += __ldcg(a.part + ((size_t)par * G + i) * (a.sw + 1) + v);
-        s = warp_sum(s);
-        if (lane == 0) vals[v] = s;
+#pragma unroll
+        for (int i = 0; i < kMaxG / 8; ++i) s += x[i];
+        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);
+        if (v < L && q == 0) vals[v] = s;
       }
       for (int v = tid; v < L; v += kPThreads) rowv[v] = __ldcg(a.rowt + par * (a.sw + 1) + v);
       __syncthreads();
@@ -181,7 +195,15 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
       const int per = (int)cdiv(ncoef, G);
       for (int e = g * per + tid; e < min(ncoef, (g + 1) * per); e += kPThreads) {
         double s = 0.0;
-        for (int i = 0; i < G; ++i) s += __ldcg(a.wpart + (size_t)i * ncoef + e);
+        int i = 0;
+        for (; i + 8 <= G; i += 8) {  // 8 loads in flight, summed in index order
+          double x[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) x[q] = __ldcg(a.wpart + (size_t)(i + q) * ncoef + e);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) s += x[q];
+        }
+        for (; i < G; ++i) s += __ldcg(a.wpart + (size_t)i * ncoef + e);
         a.wred[e] = s;
       }
     }
@@ -295,7 +317,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
     return SQR_EINVAL;
   }
   const int sms = sm_count();
-  int G = (int)std::min<int64_t>(sms, std::max<int64_t>(1, cdiv(mr, 64)));
+  int G = (int)std::min<int64_t>(std::min(sms, kMaxG), std::max<int64_t>(1, cdiv(mr, 64)));
   const int h = (int)cdiv(mr, G);
   G = (int)cdiv(mr, h);
   const int hp = h | 1;
@@ -344,6 +366,9 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
     configured = (int)smem;
   }
   void* args[] = {&a};
+  SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+  ProfScope ps(kTagPanel, s);
+  count_launch();
   SQR_CUDA(cudaLaunchCooperativeKernel((const void*)panel_kernel, dim3(G), dim3(kPThreads), args,
                                        (size_t)smem, s));
   return SQR_OK;
@@ -358,6 +383,7 @@ int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double
     SQR_CUDA(cudaFuncSetAttribute(build_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = (int)smem;
   }
+  ProfScope ps(kTagBuildT, s);
   build_t_kernel<<<1, kTThreads, smem, s>>>(Gm, ldg, taus, (int)j, T, ldt, gate);
   SQR_LAUNCH("build_t_kernel");
   return SQR_OK;

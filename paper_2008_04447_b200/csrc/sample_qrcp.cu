@@ -23,6 +23,7 @@ namespace sqr {
 namespace {
 
 constexpr int kSqThreads = 256;
+constexpr int kMaxRowsPerLane = 5;  // spill path: ell <= 160
 constexpr double kNormGuard = 0x1p-40;   // reference.py:40
 constexpr double kRankFloor = 0x1p-52;   // reference.py:44
 constexpr double kSampleFloor = 0x1p-48; // sketch.py:38
@@ -79,7 +80,7 @@ __device__ Cand block_argmax(Cand c, Cand* red) {
 struct SampleArgs {
   const double* B;
   int64_t ldb;
-  int ell, nt, bb, w, cap, ldS, first;
+  int ell, nt, bb, w, cap, ldS, first, warp_spill;
   double* Bf;
   int64_t ldbf;
   int64_t* lperm;
@@ -105,6 +106,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
   GridBarrier gb;
   gb.init(a.bar);
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
   const int ell = a.ell;
   const int col0 = g * a.w;
   const int ncols = max(0, min(a.w, a.nt - col0));
@@ -228,7 +230,9 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
     if (g == 0 && tid == 0) a.taus[j] = tau;
     __syncthreads();
     // Apply H_j to my active columns, downdate norms (reference.py:131-149).
-    for (int lc = tid; lc < ncols; lc += kSqThreads) {
+    // Shared-memory columns: one thread per column.
+    const int nsm = a.warp_spill ? min(ncols, a.cap) : ncols;
+    for (int lc = tid; lc < nsm; lc += kSqThreads) {
       const int p = pos[lc];
       if (p < 0) continue;
       double* d = colp(lc);
@@ -268,6 +272,66 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       } else {
         nsq[lc] = fmax(ns, 0.0);
       }
+    }
+    // Spilled (L2-resident) columns: one warp per column, coalesced rows.
+    for (int lc = a.cap + warp; a.warp_spill && lc < ncols; lc += kSqThreads / 32) {
+      const int p = pos[lc];
+      if (p < 0) continue;
+      double* d = a.spill + (size_t)(col0 + lc) * ell;
+      if (p == pc) {
+        for (int r = lane; r < ell; r += 32)
+          a.Bf[(int64_t)j * a.ldbf + r] = r < j ? __ldcg(d + r) : (r == j ? beta : yv[r - j]);
+        if (lane == 0) {
+          a.lperm[j] = col0 + lc;
+          if (col0 + lc != j) {
+            const int slot = atomicAdd(&a.st->nmoves, 1);
+            a.moves[2 * slot] = j;
+            a.moves[2 * slot + 1] = col0 + lc;
+          }
+          pos[lc] = -1;
+        }
+        __syncwarp();
+        continue;
+      }
+      __syncwarp();
+      if (p == j && lane == 0) pos[lc] = pc;
+      double x[kMaxRowsPerLane];
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = j + lane + 32 * i;
+        x[i] = r < ell ? __ldcg(d + r) : 0.0;
+      }
+      double part = 0.0;
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = j + lane + 32 * i;
+        if (r < ell) part = fma(yv[r - j], x[i], part);
+      }
+      const double wv = tau * warp_sum(part);
+      double ex = 0.0;
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = j + lane + 32 * i;
+        if (r < ell) {
+          x[i] = fma(-yv[r - j], wv, x[i]);
+          d[r] = x[i];
+          if (r > j) ex = fma(x[i], x[i], ex);
+        }
+      }
+      const double rj = __shfl_sync(0xffffffffu, x[0], 0);
+      const double ns = nsq[lc] - rj * rj;
+      const bool recompute = ns < kNormGuard * rsq[lc];
+      ex = warp_sum(ex);
+      __syncwarp();
+      if (lane == 0) {
+        if (recompute) {
+          nsq[lc] = ex;
+          rsq[lc] = ex;
+        } else {
+          nsq[lc] = fmax(ns, 0.0);
+        }
+      }
+      __syncwarp();
     }
     achieved = j + 1;
     __syncthreads();
@@ -319,11 +383,17 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     return SQR_EINVAL;
   }
   const int sms = sm_count();
-  // Enough columns per CTA to amortise the per-step barrier; at most one CTA per SM.
-  int G = (int)std::min<int64_t>(sms, std::max<int64_t>(1, cdiv(nt, 32)));
-  const int w = (int)cdiv(std::max<int64_t>(nt, 1), G);
-  G = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(nt, 1), w));
+  // At least 32 columns per CTA (amortise the per-step barrier), enough CTAs
+  // to keep every column in shared memory when possible, one CTA per SM.
   const int ldS = (int)(ell | 1);
+  const int64_t fixed_per_col = 16 + 4;
+  const int64_t smem_avail = std::min<int64_t>(max_smem_optin(), 220 * 1024) - (ell + 2) * 8 - 64;
+  const int64_t fit = std::max<int64_t>(1, smem_avail / ((int64_t)ldS * 8 + fixed_per_col));
+  const int64_t ntc = std::max<int64_t>(nt, 1);
+  int G = (int)std::min<int64_t>(sms, std::max<int64_t>(cdiv(ntc, 32), cdiv(ntc, fit)));
+  G = std::max(G, 1);
+  const int w = (int)cdiv(ntc, G);
+  G = (int)cdiv(ntc, w);
   const int64_t fixed = (int64_t)w * 16 + (ell + 2) * 8 + (int64_t)w * 4 + 64;
   const int64_t budget = std::min<int64_t>(max_smem_optin(), 220 * 1024) - fixed;
   int cap = (int)std::max<int64_t>(0, std::min<int64_t>(w, budget / ((int64_t)ldS * 8)));
@@ -340,6 +410,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   a.cap = cap;
   a.ldS = ldS;
   a.first = first;
+  a.warp_spill = ell <= 32 * kMaxRowsPerLane;
   a.Bf = Bf;
   a.ldbf = ldbf;
   a.lperm = lperm;
@@ -367,6 +438,9 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     configured_smem = (int)smem;
   }
   void* args[] = {&a};
+  SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+  ProfScope ps(kTagSample, s);
+  count_launch();
   SQR_CUDA(cudaLaunchCooperativeKernel((const void*)sample_qrcp_kernel, dim3(G), dim3(kSqThreads), args,
                                        (size_t)smem, s));
   return SQR_OK;
