@@ -68,6 +68,8 @@ int64_t sqr_launch_count(void);
  * 4 build_t, 5 apply_moves, 6 sample_update, 7 gaussian, 8 misc. */
 int sqr_profile_enable(int64_t max_launches);
 int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, int ntags);
+/* Debug: %globaltimer phase stamps of the cooperative kernels (NULL = off). */
+int sqr_debug_trace(void* device_buffer);
 
 /* ------------------------------------------------------------ RNG (L0)
  * Omega[i, t] = normal(seed, offset + i + t*rows) for a rows x cols matrix

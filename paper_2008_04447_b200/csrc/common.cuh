@@ -120,6 +120,19 @@ struct GridBarrier {
   }
 };
 
+// Debug phase trace (sqr_debug_trace): CTA 0 / thread 0 of the cooperative
+// kernels stamps %globaltimer at phase boundaries when a buffer is set.
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SQR_TRACE(buf, idx)                                                      \
+  do {                                                                           \
+    if ((buf) != nullptr && blockIdx.x == 0 && threadIdx.x == 0) (buf)[idx] = gtimer(); \
+  } while (0)
+extern unsigned long long* g_trace_host_ptr;
+
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

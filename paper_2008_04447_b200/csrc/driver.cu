@@ -245,7 +245,6 @@ extern "C" int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t 
     if ((rc = build_t(w.Gm, bb, taus + i0, bb, TJ, b, &st->stop, s))) return rc;
     if (nt > 1) {
       GemmDyn shB{&st->stop, &st->bhat, kShiftB};
-      GemmDyn sh0{&st->stop, &st->bhat, 0};
       GemmDyn shD{&st->stop, &st->bhat, kShiftD};
       GemmDyn shBD{&st->stop, &st->bhat, kShiftB | kShiftD};
       // G = Y2^T A[i0:, tcols]   (randomized.py:322)
@@ -268,7 +267,6 @@ extern "C" int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t 
       if ((rc = gemm_nn(bb, nt, i0 + bb, -1.0, Yg + i0, ldy, Wg + i0 * ldw, ldw, 1.0, A + i0 + i0 * lda, lda,
                         Rg + i0 + i0 * ldr, ldr, s, shBD)))
         return rc;
-      (void)sh0;
     }
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
     if (J + 1 < nblk) {

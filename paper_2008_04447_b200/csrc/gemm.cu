@@ -22,17 +22,20 @@ namespace sqr {
 
 namespace {
 
-constexpr int kThreads = 256;
+// 4 warps per CTA and two CTAs per SM: a CTA waiting at __syncthreads or on
+// its epilogue leaves the DMMA pipe to the other one (ptxas spaces a warp's
+// DMMA.8x8x4 16 cycles apart, so the pipe needs >= 2 issuing warps per SMSP).
+constexpr int kThreads = 128;
 constexpr int kBK = 16;        // K per pipeline stage
 constexpr int kPitchK = kBK + 4;
-constexpr int kStages = 4;
+constexpr int kStages = 3;
 
 // ---------------------------------------------------------------- gemm_tn
 // Computed as D^T(N x M) = C^T(N x K) X(K x M): MMA rows = n, MMA cols = i.
-// CTA tile: 128 n x MT i;  8 warps = 4 (n) x 2 (i);  warp tile 32 n x MT/2 i.
+// CTA tile: 64 n x MT i;  4 warps = 2 (n) x 2 (i);  warp tile 32 n x MT/2 i.
 template <int MT, int VEC>
 struct TnCfg {
-  static constexpr int BN = 128;
+  static constexpr int BN = 64;
   static constexpr int NI = MT / 16;  // n8 fragments per warp along i
   static constexpr int A_ELEMS = BN * kPitchK;
   static constexpr int B_ELEMS = MT * kPitchK;
@@ -48,7 +51,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
   using Cfg = TnCfg<MT, VEC>;
   constexpr int CPR = kBK / VEC;  // chunks per row
   const int tid = threadIdx.x;
-  // A operand rows: columns n of C, K contiguous.
+#pragma unroll 4
   for (int c = tid; c < Cfg::BN * CPR; c += kThreads) {
     const int r = c / CPR, kc = (c % CPR) * VEC;
     const int n = n0 + r, k = k0 + kc;
@@ -63,7 +66,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
       cp_async<8>(dst, src, ok);
     }
   }
-  // B operand rows: columns i of X, K contiguous.
+#pragma unroll 4
   for (int c = tid; c < MT * CPR; c += kThreads) {
     const int r = c / CPR, kc = (c % CPR) * VEC;
     const int k = k0 + kc;
@@ -81,7 +84,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
 }
 
 template <int MT, int VEC>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_tn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
                    const double* __restrict__ C, int64_t ldc, double beta, const double* E,
                    int64_t lde, double* D, int64_t ldd, int kchunk, double* part, unsigned* sems,
@@ -101,7 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if ((int)blockIdx.x * Cfg::BN >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wn = (warp & 3) * 32, wi = (warp >> 2) * (MT / 2);
+  const int wn = (warp & 1) * 32, wi = (warp >> 1) * (MT / 2);
   const int n0 = blockIdx.x * Cfg::BN;
   const int split = blockIdx.y, nsplit = gridDim.y;
   const int kbeg = split * kchunk;
@@ -160,7 +163,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (nsplit > 1) {
     // Publish this split's partial in thread-contiguous layout; the last
     // arriving CTA of the tile sums all splits in index order (deterministic).
-    const int tiles = gridDim.x;
     double* mine = part + ((int64_t)blockIdx.x * nsplit + split) * Cfg::ACC * kThreads;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
@@ -179,7 +181,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (!last) return;
     __threadfence();
-    (void)tiles;
 #pragma unroll
     for (int a = 0; a < 2; ++a)
 #pragma unroll
@@ -202,34 +203,31 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int n = n0 + wn + mi * 16 + g + h * 8;
       if (n >= N) continue;
 #pragma unroll
-      for (int ni = 0; ni < Cfg::NI; ++ni)
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int i = wi + ni * 8 + 2 * t + e;
-          if (i >= M) continue;
-          double v = alpha * acc[mi][ni][h * 2 + e];
-          if (beta != 0.0) v += beta * E[(int64_t)n * lde + i];
-          D[(int64_t)n * ldd + i] = v;
+      for (int ni = 0; ni < Cfg::NI; ++ni) {
+        const int i = wi + ni * 8 + 2 * t;
+        double v0 = alpha * acc[mi][ni][h * 2], v1 = alpha * acc[mi][ni][h * 2 + 1];
+        if (beta != 0.0) {
+          if (i < M) v0 += beta * E[(int64_t)n * lde + i];
+          if (i + 1 < M) v1 += beta * E[(int64_t)n * lde + i + 1];
         }
+        if (i < M) D[(int64_t)n * ldd + i] = v0;
+        if (i + 1 < M) D[(int64_t)n * ldd + i + 1] = v1;
+      }
     }
 }
 
 // ---------------------------------------------------------------- gemm_nn
-// CTA tile 128 m x 128 n; 8 warps = 2 (m) x 4 (n); warp tile 64 m x 32 n.
-// The E tile (the trailing matrix C in C -= Y W) is streamed into shared
-// memory in 1/nk slices riding along with the k-stages, so its HBM read
-// overlaps the MMAs instead of being exposed in the epilogue.
-constexpr int kStagesNN = 2;
+// CTA tile 64 m x 128 n; 4 warps = 2 (m) x 2 (n); warp tile 32 m x 64 n.
+// beta * E is read in the epilogue in two halves (32 values per thread in
+// flight each), its latency covered by the SM's other CTA.
 template <int VEC>
 struct NnCfg {
-  static constexpr int BM = 128, BN = 128;
+  static constexpr int BM = 64, BN = 128;
   static constexpr int PM = BM + 4;   // pitch of the m-contiguous X tile (4 mod 16)
-  static constexpr int PC = BM + 2;   // pitch of the E tile (2 mod 16: conflict-free epilogue)
   static constexpr int A_ELEMS = kBK * PM;
   static constexpr int B_ELEMS = BN * kPitchK;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int C_ELEMS = BN * PC;
-  static constexpr int SMEM = (STAGE * kStagesNN + C_ELEMS) * 8;
+  static constexpr int SMEM = STAGE * kStages * 8;
 };
 
 template <int VEC>
@@ -239,6 +237,7 @@ __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const doub
   using Cfg = NnCfg<VEC>;
   const int tid = threadIdx.x;
   constexpr int CPM = Cfg::BM / VEC;  // chunks per k-row of X
+#pragma unroll 4
   for (int c = tid; c < kBK * CPM; c += kThreads) {
     const int kr = c / CPM, mc = (c % CPM) * VEC;
     const int k = k0 + kr, m = m0 + mc;
@@ -254,6 +253,7 @@ __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const doub
     }
   }
   constexpr int CPK = kBK / VEC;
+#pragma unroll 4
   for (int c = tid; c < Cfg::BN * CPK; c += kThreads) {
     const int r = c / CPK, kc = (c % CPK) * VEC;
     const int n = n0 + r, k = k0 + kc;
@@ -270,31 +270,8 @@ __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const doub
   }
 }
 
-// Columns [c0, c1) of the E tile into shared memory.
 template <int VEC>
-__device__ __forceinline__ void nn_load_e(double* sC, const double* __restrict__ E, int64_t lde, int M, int N,
-                                          int m0, int n0, int c0, int c1) {
-  using Cfg = NnCfg<VEC>;
-  constexpr int CPM = Cfg::BM / VEC;
-  const int tid = threadIdx.x;
-  for (int c = tid; c < (c1 - c0) * CPM; c += kThreads) {
-    const int cn = c0 + c / CPM, mc = (c % CPM) * VEC;
-    const int n = n0 + cn, m = m0 + mc;
-    const bool ok = (n < N) && (m < M);
-    const double* src = ok ? E + (int64_t)n * lde + m : E;
-    double* dst = sC + cn * Cfg::PC + mc;
-    if constexpr (VEC == 2) {
-      const int sz = ok ? ((m + 1 < M) ? 16 : 8) : 0;
-      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
-                   "r"(sz));
-    } else {
-      cp_async<8>(dst, src, ok);
-    }
-  }
-}
-
-template <int VEC>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     gemm_nn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
                    const double* __restrict__ Y, int64_t ldy, double beta, const double* E,
                    int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
@@ -310,89 +287,87 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (E) E += (int64_t)sh * lde;
     }
   }
-  if ((int)blockIdx.y * Cfg::BN >= N) return;
+  const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  if (n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 1) * 64, wn = (warp >> 1) * 32;
-  const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 64;
   const int nk = (int)cdiv(K, kBK);
-  double* sC = smem + kStagesNN * Cfg::STAGE;
-  const bool use_e = beta != 0.0;
-  const int cps = nk > 0 ? (int)cdiv(Cfg::BN, nk) : Cfg::BN;  // E columns per k-stage
 
-  double acc[4][4][4];
+  double acc[2][8][4];
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+  for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b)
+    for (int b = 0; b < 8; ++b)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
 
-  if (nk == 0 && use_e) nn_load_e<VEC>(sC, E, lde, M, N, m0, n0, 0, Cfg::BN);
 #pragma unroll
-  for (int s = 0; s < kStagesNN - 1; ++s) {
+  for (int s = 0; s < kStages - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * Cfg::STAGE;
       nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
-      if (use_e) nn_load_e<VEC>(sC, E, lde, M, N, m0, n0, min(Cfg::BN, s * cps), min(Cfg::BN, (s + 1) * cps));
     }
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<kStagesNN - 2>();
+    cp_async_wait<kStages - 2>();
     __syncthreads();
     {
-      const int ls = kt + kStagesNN - 1;
+      const int ls = kt + kStages - 1;
       if (ls < nk) {
-        double* st = smem + (ls % kStagesNN) * Cfg::STAGE;
+        double* st = smem + (ls % kStages) * Cfg::STAGE;
         nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
-        if (use_e)
-          nn_load_e<VEC>(sC, E, lde, M, N, m0, n0, min(Cfg::BN, ls * cps), min(Cfg::BN, (ls + 1) * cps));
       }
       cp_async_commit();
     }
-    const double* sA = smem + (kt % kStagesNN) * Cfg::STAGE;
+    const double* sA = smem + (kt % kStages) * Cfg::STAGE;
     const double* sB = sA + Cfg::A_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) {
-      double a[4][2], b[4];
+      double a[2][2], b[8];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi) {
+      for (int mi = 0; mi < 2; ++mi) {
         a[mi][0] = sA[(kk + t) * Cfg::PM + wm + mi * 16 + g];
         a[mi][1] = sA[(kk + t) * Cfg::PM + wm + mi * 16 + g + 8];
       }
 #pragma unroll
-      for (int nj = 0; nj < 4; ++nj) b[nj] = sB[(wn + nj * 8 + g) * kPitchK + kk + t];
+      for (int nj = 0; nj < 8; ++nj) b[nj] = sB[(wn + nj * 8 + g) * kPitchK + kk + t];
 #pragma unroll
-      for (int mi = 0; mi < 4; ++mi)
+      for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < 4; ++nj) dmma16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+        for (int nj = 0; nj < 8; ++nj) dmma16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
     }
-    // The next iteration refills this stage: everyone must be done reading it.
-    if (kStagesNN == 2) __syncthreads();
   }
   cp_async_wait<0>();
-  __syncthreads();
 
 #pragma unroll
-  for (int mi = 0; mi < 4; ++mi)
+  for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      const int ml = wm + mi * 16 + g + h * 8;
-      const int m = m0 + ml;
+      const int m = m0 + wm + mi * 16 + g + h * 8;
+      double ev[8][2];
+      if (beta != 0.0) {
+#pragma unroll
+        for (int nj = 0; nj < 8; ++nj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = n0 + wn + nj * 8 + 2 * t + e;
+            ev[nj][e] = (m < M && n < N) ? E[(int64_t)n * lde + m] : 0.0;
+          }
+      }
       if (m >= M) continue;
 #pragma unroll
-      for (int nj = 0; nj < 4; ++nj)
+      for (int nj = 0; nj < 8; ++nj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-          const int nl = wn + nj * 8 + 2 * t + e;
-          const int n = n0 + nl;
+          const int n = n0 + wn + nj * 8 + 2 * t + e;
           if (n >= N) continue;
           double v = alpha * acc[mi][nj][h * 2 + e];
-          if (use_e) v = fma(beta, sC[nl * Cfg::PC + ml], v);
+          if (beta != 0.0) v = fma(beta, ev[nj][e], v);
           D[(int64_t)n * ldd + m] = v;
         }
-    }
+  }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -409,7 +384,7 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
     configured = true;
   }
   const int tiles = (int)cdiv(N, Cfg::BN);
-  const int sms = sm_count();
+  const int sms = 2 * sm_count();  // resident CTAs (2 per SM)
   // Pick the split count that minimises waves/split (i.e. the padded work),
   // keeping >= 512 K per split; ties go to fewer splits.
   int best = 1;

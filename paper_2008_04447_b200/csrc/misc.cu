@@ -31,6 +31,8 @@ int check_cuda(cudaError_t e, const char* what) {
   return SQR_ECUDA;
 }
 
+unsigned long long* g_trace_host_ptr = nullptr;
+
 // ------------------------------------------------------------ accounting
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -390,5 +392,12 @@ extern "C" int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, i
   }
   g_prof.tags.clear();
   g_prof.used = 0;
+  return SQR_OK;
+}
+
+// Debug: device buffer (>= 8 * steps u64) receiving %globaltimer stamps of
+// the next cooperative kernels' phases (CTA 0); NULL disables.
+extern "C" int sqr_debug_trace(void* device_buffer) {
+  sqr::g_trace_host_ptr = static_cast<unsigned long long*>(device_buffer);
   return SQR_OK;
 }

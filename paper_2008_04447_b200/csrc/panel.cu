@@ -47,6 +47,7 @@ struct PanelArgs {
   double* rowt;   // [2][sw+1]      pivot-row values
   double* wpart;  // [G][sw*wmax]   WY partials
   double* wred;   // [sw*wmax]      WY reduced
+  unsigned long long* trace;
 };
 
 __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
       const int par = parity;
       parity ^= 1;
       const int rbeg = max(0, t + 1 - row0);
+      SQR_TRACE(a.trace, 8 * t + 0);
       for (int v = warp; v < L; v += kPWarps) {
         const double* acol = slab + tl * a.hp;
         const double* pcol = slab + (tl + v) * a.hp;
@@ -96,28 +98,31 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
         for (int v = tid; v < L; v += kPThreads)
           a.rowt[par * (a.sw + 1) + v] = slab[(tl + v) * a.hp + (t - row0)];
       }
+      SQR_TRACE(a.trace, 8 * t + 1);
       gb.sync();
-      // Fixed-order reduction of the G partials of every value: 8 lanes per
-      // value, each summing G/8 partials whose loads are all in flight at once.
-      for (int v0 = 0; v0 < L; v0 += kPThreads / 8) {
-        const int v = v0 + (tid >> 3), q = tid & 7;
-        double x[kMaxG / 8];
+      SQR_TRACE(a.trace, 8 * t + 2);
+      // Fixed-order reduction of the G partials of every value: 4 lanes per
+      // value, each summing G/4 partials whose loads are all in flight at
+      // once; the pivot-row values are fetched in the same round.
+      for (int v = tid; v < L; v += kPThreads) rowv[v] = __ldcg(a.rowt + par * (a.sw + 1) + v);
+      for (int v0 = 0; v0 < L; v0 += kPThreads / 4) {
+        const int v = v0 + (tid >> 2), q = tid & 3;
+        double x[kMaxG / 4];
         const double* src = a.part + ((size_t)par * (a.sw + 1) + v) * G;
 #pragma unroll
-        for (int i = 0; i < kMaxG / 8; ++i) {
-          const int gi = q + 8 * i;
+        for (int i = 0; i < kMaxG / 4; ++i) {
+          const int gi = q + 4 * i;
           x[i] = (v < L && gi < G) ? __ldcg(src + gi) : 0.0;
         }
         double s = 0.0;
 #pragma unroll
-        for (int i = 0; i < kMaxG / 8; ++i) s += x[i];
-        s += __shfl_xor_sync(0xffffffffu, s, 4);
+        for (int i = 0; i < kMaxG / 4; ++i) s += x[i];
         s += __shfl_xor_sync(0xffffffffu, s, 2);
         s += __shfl_xor_sync(0xffffffffu, s, 1);
         if (v < L && q == 0) vals[v] = s;
       }
-      for (int v = tid; v < L; v += kPThreads) rowv[v] = __ldcg(a.rowt + par * (a.sw + 1) + v);
       __syncthreads();
+      SQR_TRACE(a.trace, 8 * t + 3);
       const double at = rowv[0], sa = vals[0];
       const double nrm = sqrt(fma(at, at, sa));
       if (nrm == 0.0 && a.stop_at_zero) {
@@ -134,17 +139,26 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
       for (int v = 1 + tid; v < L; v += kPThreads) wv[v] = tau * (rowv[v] + vals[v] / y0);
       if (g == 0 && tid == 0) a.taus[t] = tau;
       __syncthreads();
+      SQR_TRACE(a.trace, 8 * t + 4);
       for (int r = rbeg + tid; r < nrows; r += kPThreads) {
         const double yr = nrm != 0.0 ? slab[tl * a.hp + r] / y0 : 0.0;
         slab[tl * a.hp + r] = yr;
-        for (int v = 1; v < L; ++v) slab[(tl + v) * a.hp + r] = fma(-yr, wv[v], slab[(tl + v) * a.hp + r]);
+        double* pr = slab + (tl + 1) * a.hp + r;
+        int v = 1;
+        for (; v + 2 <= L; v += 2, pr += 2 * a.hp) {
+          const double p0 = pr[0], p1 = pr[a.hp];
+          pr[0] = fma(-yr, wv[v], p0);
+          pr[a.hp] = fma(-yr, wv[v + 1], p1);
+        }
+        if (v < L) pr[0] = fma(-yr, wv[v], pr[0]);
       }
-      if (t >= row0 && t < row0 + nrows && tid == 0) {
+      if (t >= row0 && t < row0 + nrows) {
         const int rt = t - row0;
-        for (int v = 1; v < L; ++v) slab[(tl + v) * a.hp + rt] -= wv[v];
-        slab[tl * a.hp + rt] = beta;
+        for (int v = 1 + tid; v < L; v += kPThreads) slab[(tl + v) * a.hp + rt] -= wv[v];
+        if (tid == 0) slab[tl * a.hp + rt] = beta;
       }
       __syncthreads();
+      SQR_TRACE(a.trace, 8 * t + 5);
     }
     __syncthreads();
     // Write the sub-panel back (packed R / reflector tails) and explicit Y.
@@ -321,11 +335,12 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   const int h = (int)cdiv(mr, G);
   G = (int)cdiv(mr, h);
   const int hp = h | 1;
-  const int64_t budget = std::min<int64_t>(max_smem_optin(), 224 * 1024) - 256;
+  const int64_t budget = (int64_t)max_smem_optin() - 4 * 1024;  // static smem of the kernel
   int sw = 0;
   for (int cand : {128, 64, 32, 16, 8, 4, 2, 1}) {
     const int64_t swc = std::min<int64_t>(cand, wmax);
-    const int64_t need = (swc * hp + swc * swc + swc * wmax) * 8;
+    // One sub-panel covering the whole width needs no compact-WY scratch.
+    const int64_t need = swc == wmax ? swc * hp * 8 : (swc * hp + swc * swc + swc * wmax) * 8;
     if (need <= budget) {
       sw = (int)swc;
       break;
@@ -335,7 +350,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
     set_error("panel_qr: panel of %lld rows does not fit shared memory", (long long)mr);
     return SQR_EINVAL;
   }
-  const int64_t smem = ((int64_t)sw * hp + (int64_t)sw * sw + (int64_t)sw * wmax) * 8;
+  const int64_t smem = sw == wmax ? (int64_t)sw * hp * 8 : ((int64_t)sw * hp + (int64_t)sw * sw + (int64_t)sw * wmax) * 8;
   PanelArgs a;
   a.P = P;
   a.ldp = ldp;
@@ -360,6 +375,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   a.wpart = reinterpret_cast<double*>(p);
   p += (int64_t)148 * 128 * wmax * 8;
   a.wred = reinterpret_cast<double*>(p);
+  a.trace = g_trace_host_ptr;
   static int configured = 0;
   if (smem > configured) {
     SQR_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -23,7 +23,8 @@ namespace sqr {
 namespace {
 
 constexpr int kSqThreads = 256;
-constexpr int kMaxRowsPerLane = 5;  // spill path: ell <= 160
+constexpr int kMaxRowsPerLane = 5;  // warp paths: ell <= 160
+constexpr int kSpillPerWarp = 5;    // register-resident spill columns per warp
 constexpr double kNormGuard = 0x1p-40;   // reference.py:40
 constexpr double kRankFloor = 0x1p-52;   // reference.py:44
 constexpr double kSampleFloor = 0x1p-48; // sketch.py:38
@@ -38,49 +39,10 @@ __device__ __forceinline__ bool better(double v1, int p1, double v2, int p2) {
   return v1 > v2 || (v1 == v2 && p1 < p2);
 }
 
-// Block-wide argmax of (val, pos) with ties to the lowest pos.  Result in out[0].
-__device__ Cand block_argmax(Cand c, Cand* red) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    double v = __shfl_xor_sync(0xffffffffu, c.val, o);
-    int p = __shfl_xor_sync(0xffffffffu, c.pos, o);
-    int l = __shfl_xor_sync(0xffffffffu, c.lc, o);
-    if (better(v, p, c.val, c.pos)) {
-      c.val = v;
-      c.pos = p;
-      c.lc = l;
-    }
-  }
-  __syncthreads();
-  if (lane == 0) red[wid] = c;
-  __syncthreads();
-  if (wid == 0) {
-    const int nw = blockDim.x >> 5;
-    Cand d = lane < nw ? red[lane] : Cand{-1.0, INT_MAX, -1};
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      double v = __shfl_xor_sync(0xffffffffu, d.val, o);
-      int p = __shfl_xor_sync(0xffffffffu, d.pos, o);
-      int l = __shfl_xor_sync(0xffffffffu, d.lc, o);
-      if (better(v, p, d.val, d.pos)) {
-        d.val = v;
-        d.pos = p;
-        d.lc = l;
-      }
-    }
-    if (lane == 0) red[0] = d;
-  }
-  __syncthreads();
-  Cand r = red[0];
-  __syncthreads();
-  return r;
-}
-
 struct SampleArgs {
   const double* B;
   int64_t ldb;
-  int ell, nt, bb, w, cap, ldS, first, warp_spill;
+  int ell, nt, bb, w, cap, ldS, first, warp_spill, reg_spill;
   double* Bf;
   int64_t ldbf;
   int64_t* lperm;
@@ -94,13 +56,39 @@ struct SampleArgs {
   double* psum;    // [G]
   double* pmax;    // [G]
   double* spill;   // [nt][ell] for columns beyond cap
+  unsigned long long* trace;
 };
 
+__device__ __forceinline__ void warp_argmax(double& v, int& p, int& l) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int p2 = __shfl_xor_sync(0xffffffffu, p, o);
+    const int l2 = __shfl_xor_sync(0xffffffffu, l, o);
+    if (better(v2, p2, v, p)) {
+      v = v2;
+      p = p2;
+      l = l2;
+    }
+  }
+}
+
+// One pivot step costs one grid barrier and one __syncthreads: after the
+// barrier every WARP independently (and identically) picks the global winner
+// from the published candidates, loads the winner column, and rebuilds the
+// reflector in registers, writing y to its own shared-memory slice; threads
+// then update their own columns and fold the next step's local candidate
+// into the same pass.
 __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ Cand red[32];
+  __shared__ double wv_s[kSqThreads / 32];
+  __shared__ int wp_s[kSqThreads / 32], wl_s[kSqThreads / 32];
   __shared__ double sred[32];
-  __shared__ int s_stop;
+  struct Bcast {
+    int go, pc;
+    double beta, tau;
+  };
+  __shared__ Bcast bc_s;
   if (a.st->stop) return;  // uniform: no CTA enters the barrier
 
   GridBarrier gb;
@@ -113,38 +101,83 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
   double* cols = sm;                                   // cap x ldS
   double* nsq = sm + (size_t)a.cap * a.ldS;            // w
   double* rsq = nsq + a.w;                             // w
-  double* yv = rsq + a.w;                              // ell (+pad)
-  int* pos = reinterpret_cast<int*>(yv + ell + 2);     // w
+  double* ysh = rsq + a.w;                             // ell (+2): the current reflector
+  int* pos = reinterpret_cast<int*>(ysh + ell + 2);    // w
 
   auto colp = [&](int lc) -> double* {
     return lc < a.cap ? cols + (size_t)lc * a.ldS : a.spill + (size_t)(col0 + lc) * ell;
   };
 
   if (g == 0 && tid == 0) a.st->nmoves = 0;
-  // Load my columns (coalesced along rows).
-  for (int64_t e = tid; e < (int64_t)ncols * ell; e += kSqThreads) {
+  const int nld = a.reg_spill ? min(ncols, a.cap) : ncols;
+  for (int64_t e = tid; e < (int64_t)nld * ell; e += kSqThreads) {
     const int lc = (int)(e / ell), r = (int)(e % ell);
     colp(lc)[r] = a.B[(int64_t)(col0 + lc) * a.ldb + r];
   }
+  double xs[kSpillPerWarp][kMaxRowsPerLane];  // this warp's spill columns (reg mode)
+#pragma unroll
+  for (int i = 0; i < kSpillPerWarp; ++i) {
+    const int lc = a.cap + warp + 8 * i;
+#pragma unroll
+    for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+      const int r = lane + 32 * qq;
+      xs[i][qq] = (a.reg_spill && lc < ncols && r < ell) ? a.B[(int64_t)(col0 + lc) * a.ldb + r] : 0.0;
+    }
+  }
   __syncthreads();
   double my_sum = 0.0, my_max = 0.0;
-  for (int lc = tid; lc < ncols; lc += kSqThreads) {
+  double cbv = -1.0;
+  int cbp = INT_MAX, cbl = -1;
+  for (int lc = tid; lc < nld; lc += kSqThreads) {
     const double* d = colp(lc);
-    double s = 0.0;
-    for (int r = 0; r < ell; ++r) s = fma(d[r], d[r], s);
+    double s0 = 0.0, s1 = 0.0;
+    int r = 0;
+    for (; r + 2 <= ell; r += 2) {
+      s0 = fma(d[r], d[r], s0);
+      s1 = fma(d[r + 1], d[r + 1], s1);
+    }
+    if (r < ell) s0 = fma(d[r], d[r], s0);
+    const double s = s0 + s1;
     nsq[lc] = s;
     rsq[lc] = s;
     pos[lc] = col0 + lc;
     my_sum += s;
     my_max = fmax(my_max, s);
+    if (better(s, col0 + lc, cbv, cbp)) {
+      cbv = s;
+      cbp = col0 + lc;
+      cbl = lc;
+    }
   }
-  // Deterministic CTA partials of sum / max of column norms^2.
+  if (a.reg_spill) {
+#pragma unroll
+    for (int i = 0; i < kSpillPerWarp; ++i) {
+      const int lc = a.cap + warp + 8 * i;
+      if (lc >= ncols) continue;
+      double s = 0.0;
+#pragma unroll
+      for (int qq = 0; qq < kMaxRowsPerLane; ++qq) s = fma(xs[i][qq], xs[i][qq], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        nsq[lc] = s;
+        rsq[lc] = s;
+        pos[lc] = col0 + lc;
+        my_sum += s;
+        my_max = fmax(my_max, s);
+        if (better(s, col0 + lc, cbv, cbp)) {
+          cbv = s;
+          cbp = col0 + lc;
+          cbl = lc;
+        }
+      }
+    }
+  }
   {
-    double s = block_sum(my_sum, sred);
+    const double s = block_sum(my_sum, sred);
     double mx = my_max;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    if ((tid & 31) == 0) sred[tid >> 5] = mx;
+    if (lane == 0) sred[warp] = mx;
     __syncthreads();
     if (tid == 0) {
       for (int i = 1; i < (kSqThreads >> 5); ++i) mx = fmax(mx, sred[i]);
@@ -152,7 +185,6 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       a.psum[g] = s;
       a.pmax[g] = mx;
     }
-    __syncthreads();
   }
   gb.sync();
   double total = 0.0, gmax = 0.0;
@@ -162,85 +194,143 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
   }
   const double fro = sqrt(total);
   const double rank_floor_sq = (kRankFloor * fro) * (kRankFloor * fro);
-  double sample_floor;
-  if (a.first) {
-    sample_floor = kSampleFloor * kSampleFloor * gmax;
-  } else {
-    sample_floor = __ldcg(&a.st->floor_sq);
-  }
-  // Everyone must have read floor_sq before CTA 0 overwrites it.
-  gb.sync();
-  if (g == 0 && tid == 0 && a.first) a.st->floor_sq = sample_floor;
+  const double sample_floor = a.first ? kSampleFloor * kSampleFloor * gmax : __ldcg(&a.st->floor_sq);
   if (a.nt == 0 || gmax <= sample_floor) {
     if (g == 0 && tid == 0) {
+      if (a.first) a.st->floor_sq = sample_floor;
       a.st->stop = 1;
       a.st->reason = SQR_STOP_SAMPLE_FLOOR;
       a.st->sample_achieved = 0;
     }
     return;
   }
+  if (g == 0 && tid == 0 && a.first) a.st->floor_sq = sample_floor;
 
   int achieved = 0;
   for (int j = 0; j < a.bb; ++j) {
     const int par = j & 1;
-    // Local candidate among active columns.
-    Cand c{-1.0, INT_MAX, -1};
-    for (int lc = tid; lc < ncols; lc += kSqThreads) {
-      const int p = pos[lc];
-      if (p >= 0 && better(nsq[lc], p, c.val, c.pos)) c = Cand{nsq[lc], p, lc};
+    SQR_TRACE(a.trace, 8 * j + 0);
+    // ---- CTA candidate (folded into the previous pass) -> publish.
+    warp_argmax(cbv, cbp, cbl);
+    if (lane == 0) {
+      wv_s[warp] = cbv;
+      wp_s[warp] = cbp;
+      wl_s[warp] = cbl;
     }
-    c = block_argmax(c, red);
-    if (tid == 0) {
-      a.cval[par * G + g] = c.val;
-      a.cpos[par * G + g] = c.pos;
-    }
-    if (c.lc >= 0) {
-      const double* d = colp(c.lc);
-      for (int r = j + tid; r < ell; r += kSqThreads) a.ccol[((size_t)par * G + g) * ell + r] = d[r];
-    }
-    gb.sync();
-    // Global winner (identical on every CTA).
-    Cand wbest{-1.0, INT_MAX, -1};
-    for (int i = tid; i < G; i += kSqThreads) {
-      const double v = __ldcg(a.cval + par * G + i);
-      const int p = __ldcg(a.cpos + par * G + i);
-      if (better(v, p, wbest.val, wbest.pos)) wbest = Cand{v, p, i};
-    }
-    wbest = block_argmax(wbest, red);
-    if (wbest.val <= rank_floor_sq) break;  // reference.py:123-124
-    const int pc = wbest.pos, gw = wbest.lc;
-    const int len = ell - j;
-    // Reflector from the published winner column (rows j..ell-1).
-    const double* u = a.ccol + ((size_t)par * G + gw) * ell + j;
-    double part = 0.0;
-    for (int r = 1 + tid; r < len; r += kSqThreads) {
-      const double x = __ldcg(u + r);
-      part = fma(x, x, part);
-    }
-    const double s1 = block_sum(part, sred);
-    const double u0 = __ldcg(u);
-    const double nrm = sqrt(fma(u0, u0, s1));
-    double beta = 0.0, tau = 0.0, y0 = 1.0;
-    if (nrm != 0.0) {
-      beta = (u0 >= 0.0 ? -1.0 : 1.0) * nrm;
-      y0 = u0 - beta;
-      tau = 2.0 / (1.0 + s1 / (y0 * y0));
-    }
-    for (int r = tid; r < len; r += kSqThreads) yv[r] = (r == 0) ? 1.0 : (nrm != 0.0 ? __ldcg(u + r) / y0 : 0.0);
-    if (g == 0 && tid == 0) a.taus[j] = tau;
     __syncthreads();
-    // Apply H_j to my active columns, downdate norms (reference.py:131-149).
-    // Shared-memory columns: one thread per column.
+    {
+      double v = lane < (kSqThreads >> 5) ? wv_s[lane] : -1.0;
+      int p = lane < (kSqThreads >> 5) ? wp_s[lane] : INT_MAX;
+      int l = lane < (kSqThreads >> 5) ? wl_s[lane] : -1;
+      warp_argmax(v, p, l);
+      if (warp == 0 && lane == 0) {
+        a.cval[par * G + g] = v;
+        a.cpos[par * G + g] = p;
+      }
+      double* dst = a.ccol + ((size_t)par * G + g) * ell;
+      if (l >= 0 && (!a.reg_spill || l < a.cap)) {
+        if (warp == 0) {
+          const double* d = colp(l);
+          for (int r = j + lane; r < ell; r += 32) dst[r] = d[r];
+        }
+      } else if (l >= 0 && warp == (l - a.cap) % 8) {
+        const int iw = (l - a.cap) / 8;
+#pragma unroll
+        for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+          // select chain, not xs[iw][qq]: keeps xs in registers
+          double v = xs[0][qq];
+#pragma unroll
+          for (int i = 1; i < kSpillPerWarp; ++i) {
+            const double c = xs[i][qq];
+            asm("{ .reg .pred p; setp.eq.s32 p, %2, %3; selp.f64 %0, %1, %0, p; }" : "+d"(v) : "d"(c), "r"(iw), "r"(i));
+          }
+          const int r = lane + 32 * qq;
+          if (r >= j && r < ell) dst[r] = v;
+        }
+      }
+    }
+    SQR_TRACE(a.trace, 8 * j + 1);
+    gb.sync();
+    SQR_TRACE(a.trace, 8 * j + 2);
+    // ---- global winner + reflector: warp 0 alone reads the published
+    // candidates and the winner column (one reader per CTA keeps the L2
+    // hot lines cool) and broadcasts y / tau / beta through shared memory.
+    if (warp == 0) {
+      double bv = -1.0;
+      int bp = INT_MAX, bl = -1;
+      for (int i = lane; i < G; i += 32) {
+        const double v = __ldcg(a.cval + par * G + i);
+        const int p = __ldcg(a.cpos + par * G + i);
+        if (better(v, p, bv, bp)) {
+          bv = v;
+          bp = p;
+          bl = i;
+        }
+      }
+      warp_argmax(bv, bp, bl);
+      const int len = ell - j;
+      double x[kMaxRowsPerLane];
+      double s1 = 0.0, nrm = 0.0, beta = 0.0, tau = 0.0, y0 = 1.0;
+      const bool go = bv > rank_floor_sq;
+      if (go) {
+        const double* u = a.ccol + ((size_t)par * G + bl) * ell + j;
+#pragma unroll
+        for (int i = 0; i < kMaxRowsPerLane; ++i) {
+          const int r = lane + 32 * i;
+          x[i] = r < len ? __ldcg(u + r) : 0.0;
+        }
+        for (int r = lane + 32 * kMaxRowsPerLane; r < len; r += 32) {  // tall samples only
+          const double v = __ldcg(u + r);
+          s1 = fma(v, v, s1);
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxRowsPerLane; ++i)
+          if (lane + 32 * i >= 1) s1 = fma(x[i], x[i], s1);
+        s1 = warp_sum(s1);
+        const double u0 = __shfl_sync(0xffffffffu, x[0], 0);
+        nrm = sqrt(fma(u0, u0, s1));
+        if (nrm != 0.0) {
+          beta = (u0 >= 0.0 ? -1.0 : 1.0) * nrm;
+          y0 = u0 - beta;
+          tau = 2.0 / (1.0 + s1 / (y0 * y0));
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxRowsPerLane; ++i) {
+          const int r = lane + 32 * i;
+          if (r < len) ysh[r] = (r == 0) ? 1.0 : (nrm != 0.0 ? x[i] / y0 : 0.0);
+        }
+        for (int r = lane + 32 * kMaxRowsPerLane; r < len; r += 32) ysh[r] = nrm != 0.0 ? __ldcg(u + r) / y0 : 0.0;
+      }
+      if (lane == 0) {
+        bc_s.go = go;
+        bc_s.pc = bp;
+        bc_s.beta = beta;
+        bc_s.tau = tau;
+      }
+    }
+    __syncthreads();
+    if (!bc_s.go) break;  // reference.py:123-124 (uniform across the grid)
+    const int pc = bc_s.pc;
+    const double beta = bc_s.beta, tau = bc_s.tau;
+    const int len = ell - j;
+    const double* yw = ysh;
+    if (g == 0 && tid == 0) a.taus[j] = tau;
+    SQR_TRACE(a.trace, 8 * j + 3);
+
+    // ---- apply H_j to my columns, downdate norms (reference.py:131-149),
+    // and track the next step's local candidate.
+    cbv = -1.0;
+    cbp = INT_MAX;
+    cbl = -1;
     const int nsm = a.warp_spill ? min(ncols, a.cap) : ncols;
     for (int lc = tid; lc < nsm; lc += kSqThreads) {
       const int p = pos[lc];
       if (p < 0) continue;
-      double* d = colp(lc);
+      double* d = a.warp_spill ? cols + (size_t)lc * a.ldS : colp(lc);
       if (p == pc) {
-        // The winner: final column j of the factored sample.
         for (int r = 0; r < j; ++r) a.Bf[(int64_t)j * a.ldbf + r] = d[r];
         a.Bf[(int64_t)j * a.ldbf + j] = beta;
-        for (int r = 1; r < len; ++r) a.Bf[(int64_t)j * a.ldbf + j + r] = yv[r];
+        for (int r = 1; r < len; ++r) a.Bf[(int64_t)j * a.ldbf + j + r] = yw[r];
         a.lperm[j] = col0 + lc;
         if (col0 + lc != j) {
           const int slot = atomicAdd(&a.st->nmoves, 1);
@@ -250,37 +340,123 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
         pos[lc] = -1;
         continue;
       }
-      if (p == j) pos[lc] = pc;  // the column that sat at position j moves to pc
-      double dot = 0.0;
+      const int pn = (p == j) ? pc : p;  // the column that sat at position j moves to pc
+      pos[lc] = pn;
+      double* dj = d + j;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       int r = 0;
       for (; r + 4 <= len; r += 4) {
-        dot = fma(yv[r], d[j + r], dot);
-        dot = fma(yv[r + 1], d[j + r + 1], dot);
-        dot = fma(yv[r + 2], d[j + r + 2], dot);
-        dot = fma(yv[r + 3], d[j + r + 3], dot);
+        d0 = fma(yw[r], dj[r], d0);
+        d1 = fma(yw[r + 1], dj[r + 1], d1);
+        d2 = fma(yw[r + 2], dj[r + 2], d2);
+        d3 = fma(yw[r + 3], dj[r + 3], d3);
       }
-      for (; r < len; ++r) dot = fma(yv[r], d[j + r], dot);
-      const double wv = tau * dot;
-      for (r = 0; r < len; ++r) d[j + r] = fma(-yv[r], wv, d[j + r]);
-      const double rj = d[j];
+      for (; r < len; ++r) d0 = fma(yw[r], dj[r], d0);
+      const double wvv = tau * ((d0 + d1) + (d2 + d3));
+      for (r = 0; r < len; ++r) dj[r] = fma(-yw[r], wvv, dj[r]);
+      const double rj = dj[0];
       double ns = nsq[lc] - rj * rj;
       if (ns < kNormGuard * rsq[lc]) {
-        double ex = 0.0;
-        for (int q = j + 1; q < ell; ++q) ex = fma(d[q], d[q], ex);
-        nsq[lc] = ex;
-        rsq[lc] = ex;
+        double e0 = 0.0, e1 = 0.0;
+        int q = j + 1;
+        for (; q + 2 <= ell; q += 2) {
+          e0 = fma(d[q], d[q], e0);
+          e1 = fma(d[q + 1], d[q + 1], e1);
+        }
+        if (q < ell) e0 = fma(d[q], d[q], e0);
+        ns = e0 + e1;
+        rsq[lc] = ns;
       } else {
-        nsq[lc] = fmax(ns, 0.0);
+        ns = fmax(ns, 0.0);
+      }
+      nsq[lc] = ns;
+      if (better(ns, pn, cbv, cbp)) {
+        cbv = ns;
+        cbp = pn;
+        cbl = lc;
       }
     }
+    SQR_TRACE(a.trace, 8 * j + 4);
+    // Register-resident spill columns: one warp per column.  Written as an
+    // explicitly instantiated lambda per column so xs stays in registers.
+    if (a.reg_spill) {
+      auto spill_col = [&](double(&xc)[kMaxRowsPerLane], const int i) {
+        const int lc = a.cap + warp + 8 * i;
+        if (lc >= ncols) return;
+        const int p = pos[lc];
+        if (p < 0) return;
+        if (p == pc) {
+#pragma unroll
+          for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+            const int r = lane + 32 * qq;
+            if (r < ell) a.Bf[(int64_t)j * a.ldbf + r] = r < j ? xc[qq] : (r == j ? beta : yw[r - j]);
+          }
+          __syncwarp();
+          if (lane == 0) {
+            a.lperm[j] = col0 + lc;
+            if (col0 + lc != j) {
+              const int slot = atomicAdd(&a.st->nmoves, 1);
+              a.moves[2 * slot] = j;
+              a.moves[2 * slot + 1] = col0 + lc;
+            }
+            pos[lc] = -1;
+          }
+          __syncwarp();
+          return;
+        }
+        const int pn = (p == j) ? pc : p;
+        double part = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+          const int r = lane + 32 * qq;
+          if (r >= j && r < ell) part = fma(yw[r - j], xc[qq], part);
+        }
+        const double wvv = tau * warp_sum(part);
+        double ex = 0.0, rjv = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+          const int r = lane + 32 * qq;
+          if (r >= j && r < ell) {
+            xc[qq] = fma(-yw[r - j], wvv, xc[qq]);
+            if (r > j) ex = fma(xc[qq], xc[qq], ex);
+          }
+          // select, not xc[j >> 5]: a dynamic index would demote xs to local memory
+          asm("{ .reg .pred p; setp.eq.s32 p, %2, %3; selp.f64 %0, %1, %0, p; }" : "+d"(rjv) : "d"(xc[qq]), "r"(j >> 5), "r"(qq));
+        }
+        const double rj = __shfl_sync(0xffffffffu, rjv, j & 31);
+        double ns = nsq[lc] - rj * rj;
+        const bool recompute = ns < kNormGuard * rsq[lc];
+        ex = warp_sum(ex);
+        ns = recompute ? ex : fmax(ns, 0.0);
+        __syncwarp();
+        if (lane == 0) {
+          if (recompute) rsq[lc] = ex;
+          nsq[lc] = ns;
+          pos[lc] = pn;
+          if (better(ns, pn, cbv, cbp)) {
+            cbv = ns;
+            cbp = pn;
+            cbl = lc;
+          }
+        }
+        __syncwarp();
+      };
+      static_assert(kSpillPerWarp == 5, "unrolled below");
+      spill_col(xs[0], 0);
+      spill_col(xs[1], 1);
+      spill_col(xs[2], 2);
+      spill_col(xs[3], 3);
+      spill_col(xs[4], 4);
+    }
     // Spilled (L2-resident) columns: one warp per column, coalesced rows.
-    for (int lc = a.cap + warp; a.warp_spill && lc < ncols; lc += kSqThreads / 32) {
+    for (int lc = a.cap + warp; a.warp_spill && !a.reg_spill && lc < ncols; lc += kSqThreads / 32) {
       const int p = pos[lc];
       if (p < 0) continue;
       double* d = a.spill + (size_t)(col0 + lc) * ell;
       if (p == pc) {
         for (int r = lane; r < ell; r += 32)
-          a.Bf[(int64_t)j * a.ldbf + r] = r < j ? __ldcg(d + r) : (r == j ? beta : yv[r - j]);
+          a.Bf[(int64_t)j * a.ldbf + r] = r < j ? __ldcg(d + r) : (r == j ? beta : yw[r - j]);
+        __syncwarp();
         if (lane == 0) {
           a.lperm[j] = col0 + lc;
           if (col0 + lc != j) {
@@ -293,51 +469,76 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
         __syncwarp();
         continue;
       }
-      __syncwarp();
-      if (p == j && lane == 0) pos[lc] = pc;
-      double x[kMaxRowsPerLane];
+      const int pn = (p == j) ? pc : p;
+      double xs[kMaxRowsPerLane];
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = j + lane + 32 * i;
-        x[i] = r < ell ? __ldcg(d + r) : 0.0;
+        xs[i] = r < ell ? __ldcg(d + r) : 0.0;
       }
       double part = 0.0;
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = j + lane + 32 * i;
-        if (r < ell) part = fma(yv[r - j], x[i], part);
+        if (r < ell) part = fma(yw[r - j], xs[i], part);
       }
-      const double wv = tau * warp_sum(part);
+      const double wvv = tau * warp_sum(part);
       double ex = 0.0;
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = j + lane + 32 * i;
         if (r < ell) {
-          x[i] = fma(-yv[r - j], wv, x[i]);
-          d[r] = x[i];
-          if (r > j) ex = fma(x[i], x[i], ex);
+          xs[i] = fma(-yw[r - j], wvv, xs[i]);
+          d[r] = xs[i];
+          if (r > j) ex = fma(xs[i], xs[i], ex);
         }
       }
-      const double rj = __shfl_sync(0xffffffffu, x[0], 0);
-      const double ns = nsq[lc] - rj * rj;
+      const double rj = __shfl_sync(0xffffffffu, xs[0], 0);
+      double ns = nsq[lc] - rj * rj;
       const bool recompute = ns < kNormGuard * rsq[lc];
       ex = warp_sum(ex);
+      ns = recompute ? ex : fmax(ns, 0.0);
       __syncwarp();
       if (lane == 0) {
-        if (recompute) {
-          nsq[lc] = ex;
-          rsq[lc] = ex;
-        } else {
-          nsq[lc] = fmax(ns, 0.0);
-        }
+        if (recompute) rsq[lc] = ex;
+        nsq[lc] = ns;
+        pos[lc] = pn;
       }
       __syncwarp();
+      if (lane == 0 && better(ns, pn, cbv, cbp)) {
+        cbv = ns;
+        cbp = pn;
+        cbl = lc;
+      }
     }
+    SQR_TRACE(a.trace, 8 * j + 5);
     achieved = j + 1;
-    __syncthreads();
+  }
+  __syncthreads();
+  if (a.reg_spill) {
+#pragma unroll
+    for (int i = 0; i < kSpillPerWarp; ++i) {
+      const int lc = a.cap + warp + 8 * i;
+      if (lc >= ncols) continue;
+      const int p = pos[lc];
+      if (p < 0) continue;
+#pragma unroll
+      for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+        const int r = lane + 32 * qq;
+        if (r < ell) a.Bf[(int64_t)p * a.ldbf + r] = xs[i][qq];
+      }
+      if (lane == 0) {
+        a.lperm[p] = col0 + lc;
+        if (p != col0 + lc) {
+          const int slot = atomicAdd(&a.st->nmoves, 1);
+          a.moves[2 * slot] = p;
+          a.moves[2 * slot + 1] = col0 + lc;
+        }
+      }
+    }
   }
   // Remaining (trailing) columns go to their final positions.
-  for (int lc = tid; lc < ncols; lc += kSqThreads) {
+  for (int lc = tid; lc < (a.reg_spill ? min(ncols, a.cap) : ncols); lc += kSqThreads) {
     const int p = pos[lc];
     if (p < 0) continue;
     const double* d = colp(lc);
@@ -356,7 +557,6 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       a.st->reason = SQR_STOP_SAMPLE_RANK;
     }
   }
-  (void)s_stop;
 }
 
 }  // namespace
@@ -387,7 +587,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   // to keep every column in shared memory when possible, one CTA per SM.
   const int ldS = (int)(ell | 1);
   const int64_t fixed_per_col = 16 + 4;
-  const int64_t smem_avail = std::min<int64_t>(max_smem_optin(), 220 * 1024) - (ell + 2) * 8 - 64;
+  const int64_t smem_avail = (int64_t)max_smem_optin() - 2048 - (ell + 2) * 8 - 64;
   const int64_t fit = std::max<int64_t>(1, smem_avail / ((int64_t)ldS * 8 + fixed_per_col));
   const int64_t ntc = std::max<int64_t>(nt, 1);
   int G = (int)std::min<int64_t>(sms, std::max<int64_t>(cdiv(ntc, 32), cdiv(ntc, fit)));
@@ -395,7 +595,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   const int w = (int)cdiv(ntc, G);
   G = (int)cdiv(ntc, w);
   const int64_t fixed = (int64_t)w * 16 + (ell + 2) * 8 + (int64_t)w * 4 + 64;
-  const int64_t budget = std::min<int64_t>(max_smem_optin(), 220 * 1024) - fixed;
+  const int64_t budget = (int64_t)max_smem_optin() - 2048 - fixed;
   int cap = (int)std::max<int64_t>(0, std::min<int64_t>(w, budget / ((int64_t)ldS * 8)));
   const int64_t smem = (int64_t)cap * ldS * 8 + fixed;
 
@@ -411,6 +611,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   a.ldS = ldS;
   a.first = first;
   a.warp_spill = ell <= 32 * kMaxRowsPerLane;
+  a.reg_spill = a.warp_spill && (w - cap) <= 8 * kSpillPerWarp;
   a.Bf = Bf;
   a.ldbf = ldbf;
   a.lperm = lperm;
@@ -430,6 +631,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   a.pmax = reinterpret_cast<double*>(p);
   p += 148 * 8;
   a.spill = reinterpret_cast<double*>(p);
+  a.trace = g_trace_host_ptr;
 
   static int configured_smem = 0;
   if (smem > configured_smem) {

@@ -1,0 +1,100 @@
+"""Time the four hot kernels of one C5 block in isolation (builder tool; also the
+ncu target: `ncu --set full -k regex:... python tools/kernel_probe.py`)."""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2008_04447_b200 import _lib  # noqa: E402
+from paper_2008_04447_b200._dev import ColMajor, status_new, stream_handle  # noqa: E402
+
+L = _lib.lib()
+dev = torch.device("cuda", 0)
+only = sys.argv[1] if len(sys.argv) > 1 else "all"
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+m = n = 32768
+b, ell = 128, 136
+
+
+def timed(name, fn, flops=None, nbytes=None):
+    if only not in ("all", name):
+        return
+    fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 1e30
+    for _ in range(reps):
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    extra = ""
+    if flops:
+        extra += f"  {flops / best / 1e9:.2f} TFLOP/s"
+    if nbytes:
+        extra += f"  {nbytes / best / 1e6:.1f} GB/s"
+    print(f"{name:12s} {best * 1e3:10.1f} us{extra}", flush=True)
+
+
+g = torch.Generator(device=dev).manual_seed(0)
+ws = torch.zeros(400 << 20, dtype=torch.uint8, device=dev)
+A = ColMajor(torch.randn((n, m), dtype=torch.float64, device=dev, generator=g), m, n, m)
+Y = ColMajor(torch.randn((b, m), dtype=torch.float64, device=dev, generator=g), m, b, m)
+W = ColMajor(torch.randn((n, b), dtype=torch.float64, device=dev, generator=g), b, n, b)
+Wt = ColMajor.empty(b, n, dev)
+nt = n - b
+s = stream_handle()
+timed("gemm_nn", lambda: _lib.check(L.sqr_gemm_nn(m, nt, b, 1.0, Y.ptr, Y.ld, W.ptr, W.ld, 1.0, A.col_ptr(0, b), A.ld,
+                                                 A.col_ptr(0, b), A.ld, s)), flops=2.0 * m * nt * b)
+timed("gemm_tn", lambda: _lib.check(L.sqr_gemm_tn(b, nt, m, 1.0, Y.ptr, Y.ld, A.col_ptr(0, b), A.ld, 0.0, None, 0,
+                                                 Wt.ptr, Wt.ld, ws.data_ptr(), ws.numel(), s)), flops=2.0 * m * nt * b)
+Om = ColMajor(torch.randn((ell, m), dtype=torch.float64, device=dev, generator=g), m, ell, m)
+Bs = ColMajor.empty(ell, n, dev)
+timed("sketch", lambda: _lib.check(L.sqr_gemm_tn(ell, n, m, 1.0, Om.ptr, Om.ld, A.ptr, A.ld, 0.0, None, 0, Bs.ptr, Bs.ld,
+                                                ws.data_ptr(), ws.numel(), s)), flops=2.0 * m * n * ell)
+B = ColMajor(torch.randn((n, ell), dtype=torch.float64, device=dev, generator=g), ell, n, ell)
+Bf = ColMajor.empty(ell, n, dev)
+lperm = torch.empty(n, dtype=torch.int64, device=dev)
+moves = torch.empty(1024, dtype=torch.int32, device=dev)
+taus = torch.zeros(b, dtype=torch.float64, device=dev)
+st = status_new(dev)
+
+
+def sample():
+    st.zero_()
+    _lib.check(L.sqr_sample_qrcp(B.ptr, B.ld, ell, n, b, Bf.ptr, Bf.ld, lperm.data_ptr(), moves.data_ptr(),
+                                 taus.data_ptr(), 1, st.data_ptr(), s))
+
+
+timed("sample_qrcp", sample)
+P0 = torch.randn((b, m), dtype=torch.float64, device=dev, generator=g)
+P = ColMajor(P0.clone(), m, b, m)
+T = ColMajor.empty(b, b, dev)
+
+
+def panel():
+    P.t.copy_(P0)
+    st.zero_()
+    _lib.check(L.sqr_panel_qr(P.ptr, P.ld, m, b, Y.ptr, Y.ld, taus.data_ptr(), T.ptr, T.ld, 1, st.data_ptr(), s))
+
+
+timed("panel", panel)
+
+if os.environ.get("SQR_TRACE"):
+    import numpy as np
+    tr = torch.zeros(8 * 256, dtype=torch.int64, device=dev)
+    for name, fn in (("sample_qrcp", sample), ("panel", panel)):
+        tr.zero_()
+        L.sqr_debug_trace(tr.data_ptr())
+        fn()
+        torch.cuda.synchronize()
+        L.sqr_debug_trace(None)
+        t = tr.cpu().numpy().reshape(256, 8)[:128].astype(np.float64)
+        ok = t[:, 0] > 0
+        t = t[ok]
+        base = t[:, 0:1]
+        d = np.diff(np.concatenate([t[:, :6], t[1:, :1].tolist() + [[t[-1, 5]]]], axis=1), axis=1) / 1e3
+        print(name, "per-step phase us (mean over steps):", np.round(d.mean(axis=0), 2), "steps", len(t))
+        print("   step0", np.round(d[0], 2), "step64", np.round(d[min(64, len(d) - 1)], 2))
