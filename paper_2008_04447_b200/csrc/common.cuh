@@ -106,6 +106,22 @@ struct GridBarrier {
     target = 0;
     nblocks = gridDim.x * gridDim.y * gridDim.z;
   }
+  // Split phases: arrive() publishes this CTA's prior writes; wait() (any
+  // one warp may call it, the caller's thread 0 polls) returns once every
+  // CTA has arrived.  sync() = arrive + wait.
+  __device__ void arrive() {
+    __syncthreads();
+    target += nblocks;
+    if (threadIdx.x == 0) {
+      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
+    }
+  }
+  __device__ void wait_lane0() {  // call from lane 0 of one warp
+    while ((int)(ld_relaxed_u32(ctr) - target) < 0) {
+    }
+    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+  }
   __device__ void sync() {
     __syncthreads();
     target += nblocks;
@@ -169,6 +185,12 @@ struct GemmDyn {
   const int32_t* stop = nullptr;
   const int32_t* shift = nullptr;
   int flags = 0;
+  // gemm_tn only: the first npre columns of the C operand come from pre
+  // (ld ldpre) and are never shifted -- lets the trailing-update sweep
+  // Y^T [Y | C] produce the Gram matrix Y^T Y for T in the same launch.
+  const double* pre = nullptr;
+  int64_t ldpre = 0;
+  int npre = 0;
 };
 
 __host__ __device__ constexpr int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

@@ -53,24 +53,33 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.stau = c.take<double>(b);
   w.Ypan = c.take<double>(m * b);
   w.Gm = c.take<double>(b * b);
-  w.Wt = c.take<double>(b * n);
+  w.Wt = c.take<double>(b * (n + b));
   w.W = c.take<double>(b * n);
   w.OmT = (need_omega || resample) ? c.take<double>(m * ell) : nullptr;
   w.total = c.off + 256;
   return w;
 }
 
-// One compact-WY block reflection of the trailing matrix (randomized.py:203-210):
-// Wt = Y^T C;  W = -T^T Wt;  C += Y W, with C starting bhat columns right of P.
+// One compact-WY block reflection of the trailing matrix (randomized.py:203-210)
+// plus the block's T (householder.py:52-61):
+//   [G | Wt] = Y^T [Y | C]     one sweep; G = Y^T Y is free next to Y^T C
+//   T        = build_t(G, tau)
+//   W        = -T^T Wt;   C += Y W,
+// with C starting bhat columns right of P (device-side shift).
 int trailing_update(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, const double* Y,
-                    int64_t ldy, const double* T, int64_t ldt, double* Wt, double* W, int64_t ldw,
-                    sqr_status* st, double* gws, cudaStream_t s) {
-  if (nt <= 1) return SQR_OK;
+                    int64_t ldy, const double* taus, double* T, int64_t ldt, double* GWt, double* W,
+                    int64_t ldw, sqr_status* st, double* gws, cudaStream_t s) {
   GemmDyn d1{&st->stop, &st->bhat, kShiftB};
+  d1.pre = Y;
+  d1.ldpre = ldy;
+  d1.npre = (int)bb;
   GemmDyn d2{&st->stop, &st->bhat, 0};
   GemmDyn d3{&st->stop, &st->bhat, kShiftD};
-  int rc = gemm_tn(bb, nt, mr, 1.0, Y, ldy, P, lda, 0.0, nullptr, 0, Wt, ldw, gws, kGemmWsBytes, s, d1);
+  int rc = gemm_tn(bb, bb + nt, mr, 1.0, Y, ldy, P, lda, 0.0, nullptr, 0, GWt, ldw, gws, kGemmWsBytes, s, d1);
   if (rc) return rc;
+  if ((rc = build_t(GWt, ldw, taus, bb, T, ldt, &st->stop, s))) return rc;
+  if (nt <= 1) return SQR_OK;
+  const double* Wt = GWt + bb * ldw;
   rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, Wt, ldw, 0.0, nullptr, 0, W, ldw, gws, kGemmWsBytes, s, d2);
   if (rc) return rc;
   return gemm_nn(mr, nt, bb, 1.0, Y, ldy, W, ldw, 1.0, P, lda, P, lda, s, d3);
@@ -133,11 +142,8 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
       return rc;
     if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
     if ((rc = panel_qr(P, lda, mr, -1, bb, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, s))) return rc;
-    if ((rc = gemm_tn(bb, bb, mr, 1.0, w.Ypan, m, w.Ypan, m, 0.0, nullptr, 0, w.Gm, bb, w.gemm, kGemmWsBytes,
-                      s, GemmDyn{&st->stop, nullptr, 0})))
+    if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s)))
       return rc;
-    if ((rc = build_t(w.Gm, bb, taus + i0, bb, TJ, b, &st->stop, s))) return rc;
-    if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, TJ, b, w.Wt, w.W, b, st, w.gemm, s))) return rc;
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
     if (J + 1 < nblk) {
       const int64_t a1 = i0 + bb;  // achieved if the block completed
@@ -169,7 +175,7 @@ TrqrcpWs carve_trqrcp(void* ws, int64_t m, int64_t n, int64_t k, int64_t b, int6
   Carve c(ws);
   c.off = w.r.total;
   w.Pn = c.take<double>(m * b);
-  w.Gb = c.take<double>(b * n);
+  w.Gb = c.take<double>(b * (n + b));
   w.Cr = c.take<double>(b * std::max<int64_t>(k, 1));
   w.r.total = c.off + 256;
   return w;
@@ -239,28 +245,30 @@ extern "C" int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t 
       return rc;
     if ((rc = panel_qr(tw.Pn, m, mr, -1, bb, Ypan, ldy, taus + i0, 1, st, w.panel, w.panel_bytes, s))) return rc;
     if ((rc = copy_upper(tw.Pn, m, Rg + i0 + i0 * ldr, ldr, bb, &st->stop, s))) return rc;
-    if ((rc = gemm_tn(bb, bb, mr, 1.0, Ypan, ldy, Ypan, ldy, 0.0, nullptr, 0, w.Gm, bb, w.gemm, kGemmWsBytes, s,
-                      gate)))
+    // [Y2^T Y2 | G] = Y2^T [Y2 | A[i0:, tcols]]   (randomized.py:311,322) in one sweep
+    GemmDyn shP{&st->stop, &st->bhat, kShiftB};
+    shP.pre = Ypan;
+    shP.ldpre = ldy;
+    shP.npre = (int)bb;
+    if ((rc = gemm_tn(bb, bb + nt, mr, 1.0, Ypan, ldy, A + i0 + i0 * lda, lda, 0.0, nullptr, 0, tw.Gb, b, w.gemm,
+                      kGemmWsBytes, s, shP)))
       return rc;
-    if ((rc = build_t(w.Gm, bb, taus + i0, bb, TJ, b, &st->stop, s))) return rc;
+    if ((rc = build_t(tw.Gb, b, taus + i0, bb, TJ, b, &st->stop, s))) return rc;
     if (nt > 1) {
       GemmDyn shB{&st->stop, &st->bhat, kShiftB};
       GemmDyn shD{&st->stop, &st->bhat, kShiftD};
       GemmDyn shBD{&st->stop, &st->bhat, kShiftB | kShiftD};
-      // G = Y2^T A[i0:, tcols]   (randomized.py:322)
-      if ((rc = gemm_tn(bb, nt, mr, 1.0, Ypan, ldy, A + i0 + i0 * lda, lda, 0.0, nullptr, 0, tw.Gb, b, w.gemm,
-                        kGemmWsBytes, s, shB)))
-        return rc;
+      double* Gbt = tw.Gb + bb * b;  // G = Y2^T A[i0:, tcols]
       if (i0 > 0) {
         // G -= (Y2^T Y1) W1^T   (randomized.py:325-326)
         if ((rc = gemm_tn(bb, i0, mr, 1.0, Ypan, ldy, Yg + i0, ldy, 0.0, nullptr, 0, tw.Cr, b, w.gemm, kGemmWsBytes,
                           s, gate)))
           return rc;
-        if ((rc = gemm_nn(bb, nt, i0, -1.0, tw.Cr, b, Wg + i0 * ldw, ldw, 1.0, tw.Gb, b, tw.Gb, b, s, shB)))
+        if ((rc = gemm_nn(bb, nt, i0, -1.0, tw.Cr, b, Wg + i0 * ldw, ldw, 1.0, Gbt, b, Gbt, b, s, shB)))
           return rc;
       }
       // Wg[i0:i0+bb, tcols] = T2^T G   (randomized.py:327)
-      if ((rc = gemm_tn(bb, nt, bb, 1.0, TJ, b, tw.Gb, b, 0.0, nullptr, 0, Wg + i0 + i0 * ldw, ldw, w.gemm,
+      if ((rc = gemm_tn(bb, nt, bb, 1.0, TJ, b, Gbt, b, 0.0, nullptr, 0, Wg + i0 + i0 * ldw, ldw, w.gemm,
                         kGemmWsBytes, s, shD)))
         return rc;
       // R12 = A[i0:i0+bb, tcols] - Yg[i0:i0+bb, :i0+bb] Wg[:i0+bb, tcols]   (randomized.py:329-330)
@@ -284,7 +292,8 @@ extern "C" int64_t sqr_qr_blocked_workspace(int64_t m, int64_t n, int64_t /*k*/,
   c.take<char>(panel_workspace(std::min<int64_t>(b, 128)));
   c.take<double>(m * b);        // Ypan
   c.take<double>(b * b);        // G
-  c.take<double>(b * n * 2);    // Wt, W
+  c.take<double>(b * (n + b));  // [G | Wt]
+  c.take<double>(b * n);        // W
   c.take<sqr_status>(1);
   return c.off + 256;
 }
@@ -306,9 +315,10 @@ extern "C" int sqr_qr_blocked(double* A, int64_t lda, int64_t m, int64_t n, int6
   void* pws = c.take<char>(pb);
   double* Ypan = c.take<double>(m * b);
   double* Gm = c.take<double>(b * b);
-  double* Wt = c.take<double>(b * n);
+  double* Wt = c.take<double>(b * (n + b));
   double* W = c.take<double>(b * n);
   sqr_status* st = c.take<sqr_status>(1);
+  (void)Gm;
   SQR_CUDA(cudaMemsetAsync(st, 0, sizeof(sqr_status), s));
   int rc;
   for (int64_t i0 = 0; i0 < k; i0 += b) {
@@ -316,11 +326,7 @@ extern "C" int sqr_qr_blocked(double* A, int64_t lda, int64_t m, int64_t n, int6
     double* P = A + i0 + i0 * lda;
     double* TJ = T + (i0 / b) * b * b;
     if ((rc = panel_qr(P, lda, mr, bb, bb, Ypan, m, taus + i0, 0, st, pws, pb, s))) return rc;
-    if ((rc = gemm_tn(bb, bb, mr, 1.0, Ypan, m, Ypan, m, 0.0, nullptr, 0, Gm, bb, gws, kGemmWsBytes, s,
-                      GemmDyn{})))
-      return rc;
-    if ((rc = build_t(Gm, bb, taus + i0, bb, TJ, b, nullptr, s))) return rc;
-    if ((rc = trailing_update(P, lda, mr, nt, bb, Ypan, m, TJ, b, Wt, W, b, st, gws, s))) return rc;
+    if ((rc = trailing_update(P, lda, mr, nt, bb, Ypan, m, taus + i0, TJ, b, Wt, W, b, st, gws, s))) return rc;
   }
   return SQR_OK;
 }

@@ -47,7 +47,7 @@ struct TnCfg {
 template <int MT, int VEC>
 __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const double* __restrict__ X,
                                               int64_t ldx, const double* __restrict__ C, int64_t ldc,
-                                              int M, int N, int n0, int k0, int kend) {
+                                              int M, int N, int n0, int k0, int kend, const GemmDyn& dyn) {
   using Cfg = TnCfg<MT, VEC>;
   constexpr int CPR = kBK / VEC;  // chunks per row
   const int tid = threadIdx.x;
@@ -56,7 +56,9 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
     const int r = c / CPR, kc = (c % CPR) * VEC;
     const int n = n0 + r, k = k0 + kc;
     const bool ok = (n < N) && (k < kend);
-    const double* src = ok ? C + (int64_t)n * ldc + k : C;
+    const double* src = !ok ? C
+                            : (n < dyn.npre ? dyn.pre + (int64_t)n * dyn.ldpre + k
+                                            : C + (int64_t)(n - dyn.npre) * ldc + k);
     double* dst = sA + r * kPitchK + kc;
     if constexpr (VEC == 2) {
       const int sz = ok ? ((k + 1 < kend) ? 16 : 8) : 0;
@@ -123,7 +125,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   for (int s = 0; s < kStages - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * Cfg::STAGE;
-      tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + s * kBK, kend);
+      tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + s * kBK, kend, dyn);
     }
     cp_async_commit();
   }
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (ls < nk) {
         double* st = smem + (ls % kStages) * Cfg::STAGE;
         tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + ls * kBK,
-                               kend);
+                               kend, dyn);
       }
       cp_async_commit();
     }
@@ -161,38 +163,23 @@ __global__ void __launch_bounds__(kThreads, 2)
   cp_async_wait<0>();
 
   if (nsplit > 1) {
-    // Publish this split's partial in thread-contiguous layout; the last
-    // arriving CTA of the tile sums all splits in index order (deterministic).
-    double* mine = part + ((int64_t)blockIdx.x * nsplit + split) * Cfg::ACC * kThreads;
+    // Split-K: store the raw partial as part[split][n][i] (ld MT); the
+    // separate splitk_reduce kernel sums the splits in index order.
+    double* mine = part + (int64_t)split * N * MT;
 #pragma unroll
-    for (int a = 0; a < 2; ++a)
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-      for (int b = 0; b < Cfg::NI; ++b)
+      for (int h = 0; h < 2; ++h) {
+        const int n = n0 + wn + mi * 16 + g + h * 8;
+        if (n >= N) continue;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) __stcg(mine + ((a * Cfg::NI + b) * 4 + e) * kThreads + tid, acc[a][b][e]);
-    __threadfence();
-    __syncthreads();
-    __shared__ unsigned last;
-    if (tid == 0) {
-      unsigned old = atomicAdd(sems + blockIdx.x, 1u);
-      last = (old == (unsigned)nsplit - 1);
-      if (last) sems[blockIdx.x] = 0u;  // reusable by the next launch
-    }
-    __syncthreads();
-    if (!last) return;
-    __threadfence();
-#pragma unroll
-    for (int a = 0; a < 2; ++a)
-#pragma unroll
-      for (int b = 0; b < Cfg::NI; ++b)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          double s = 0.0;
-          const double* base = part + (int64_t)blockIdx.x * nsplit * Cfg::ACC * kThreads +
-                               ((a * Cfg::NI + b) * 4 + e) * kThreads + tid;
-          for (int sp = 0; sp < nsplit; ++sp) s += __ldcg(base + (int64_t)sp * Cfg::ACC * kThreads);
-          acc[a][b][e] = s;
+        for (int ni = 0; ni < Cfg::NI; ++ni) {
+          const int i = wi + ni * 8 + 2 * t;
+          __stcg(reinterpret_cast<double2*>(mine + (int64_t)n * MT + i),
+                 make_double2(acc[mi][ni][h * 2], acc[mi][ni][h * 2 + 1]));
         }
+      }
+    return;
   }
 
   // Epilogue: D(i, n) = alpha * acc + beta * E(i, n).
@@ -214,6 +201,41 @@ __global__ void __launch_bounds__(kThreads, 2)
         if (i + 1 < M) D[(int64_t)n * ldd + i + 1] = v1;
       }
     }
+}
+
+// Deterministic split-K reduction: D(i, n) = alpha * sum_s part[s][n][i] +
+// beta * E(i, n), splits summed in index order, all SMs participating.
+__global__ void __launch_bounds__(256)
+    splitk_reduce_kernel(int M, int N, int MT, int nsplit, double alpha, const double* __restrict__ part,
+                         double beta, const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
+  if (dyn.stop && *dyn.stop) return;
+  if (dyn.shift) {
+    const int sh = *dyn.shift;
+    N -= sh;
+    if (dyn.flags & kShiftD) {
+      D += (int64_t)sh * ldd;
+      if (E) E += (int64_t)sh * lde;
+    }
+  }
+  const int64_t total = (int64_t)M * N;
+  const int64_t stride = (int64_t)N * MT;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % M), n = (int)(e / M);
+    const double* src = part + (int64_t)n * MT + i;
+    double s = 0.0;
+    int sp = 0;
+    for (; sp + 8 <= nsplit; sp += 8) {
+      double x[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) x[q] = __ldcg(src + (sp + q) * stride);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) s += x[q];
+    }
+    for (; sp < nsplit; ++sp) s += __ldcg(src + sp * stride);
+    double v = alpha * s;
+    if (beta != 0.0) v += beta * E[(int64_t)n * lde + i];
+    D[(int64_t)n * ldd + i] = v;
+  }
 }
 
 // ---------------------------------------------------------------- gemm_nn
@@ -403,23 +425,27 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
   int nsplit = (int)cdiv(K, kchunk);
   if (nsplit < 1) nsplit = 1;
   double* part = nullptr;
-  unsigned* sems = nullptr;
   if (nsplit > 1) {
-    const int64_t need = (int64_t)tiles * nsplit * Cfg::ACC * kThreads * 8 + (int64_t)tiles * 4 + 16;
+    const int64_t need = (int64_t)nsplit * N * MT * 8;
     if (ws == nullptr || ws_bytes < need) {
       nsplit = 1;
       kchunk = K;
     } else {
-      sems = reinterpret_cast<unsigned*>(ws);
-      part = ws + cdiv((int64_t)tiles * 4, 8) + 2;
+      part = ws;
     }
   }
   if (nsplit == 1) kchunk = std::max(K, 1);
   dim3 grid(tiles, nsplit);
   ProfScope ps(kTagGemmTn, s);
   gemm_tn_kernel<MT, VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, C, ldc, beta, E,
-                                                           lde, D, ldd, kchunk, part, sems, dyn);
+                                                           lde, D, ldd, kchunk, part, nullptr, dyn);
   SQR_LAUNCH("gemm_tn_kernel");
+  if (nsplit > 1) {
+    const int64_t total = (int64_t)M * N;
+    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sm_count() * 8);
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn);
+    SQR_LAUNCH("splitk_reduce_kernel");
+  }
   return SQR_OK;
 }
 
@@ -427,7 +453,8 @@ template <int MT>
 int dispatch_tn_vec(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* C,
                     int64_t ldc, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
                     double* ws, int64_t ws_bytes, GemmDyn dyn, cudaStream_t s) {
-  const bool v2 = aligned16(X) && aligned16(C) && (ldx % 2 == 0) && (ldc % 2 == 0);
+  const bool v2 = aligned16(X) && aligned16(C) && (ldx % 2 == 0) && (ldc % 2 == 0) &&
+                  (dyn.npre == 0 || (aligned16(dyn.pre) && dyn.ldpre % 2 == 0));
   if (v2)
     return launch_tn<MT, 2>(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
   return launch_tn<MT, 1>(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);

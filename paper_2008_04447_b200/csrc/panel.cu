@@ -30,6 +30,8 @@ namespace {
 constexpr int kPThreads = 256;
 constexpr int kPWarps = kPThreads / 32;
 constexpr int kMaxG = 152;  // >= SM count, multiple of 8
+constexpr int kRowsPerLane = 8;             // row chunk = 256 rows
+constexpr int kColsPerWarp = 128 / kPWarps;  // sub-panel width <= 128
 
 struct PanelArgs {
   double* P;
@@ -68,7 +70,6 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
   double* GS = Ts + (size_t)a.sw * a.sw;          // swe x (swe + rest)
   int bhat = w;
   bool stopped = false;
-  int parity = 0;
   int written = 0;  // Y columns [0, written) defined on my rows
 
   for (int c0 = 0; c0 < w; c0 += a.sw) {
@@ -79,25 +80,77 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
         slab[c * a.hp + r] = a.P[(int64_t)(c0 + c) * a.ldp + row0 + r];
     __syncthreads();
 
+    // Partial sums of step tcur over my rows > tcur, for the columns
+    // tcur..c1-1 (value v <-> column tcur + v; v = 0 gives |a|^2), fused with
+    // the rank-1 update of the previous step (y in slab column tcur-1, w in
+    // wv[1 + v]) when upd.  Lanes own rows (stride-1 shared-memory access for
+    // any pitch); warp q owns columns v = q, q+8, ...; each warp reduces its
+    // columns with shuffles, so no cross-warp pass is needed.
+    auto fused = [&](int tcur, bool upd) {
+      const int tl = tcur - c0;
+      const int Lc = c1 - tcur;
+      const int par = (tcur - c0) & 1;
+      const double* yprev = slab + (tl - 1) * a.hp;
+      const double* acol = slab + tl * a.hp;
+      const double wa = upd ? wv[1] : 0.0;
+      const int rsum = tcur + 1 - row0;   // summed rows: local index >= rsum
+      const int rupd = tcur - row0;       // updated rows: local index >= rupd
+      double acc[kColsPerWarp];
+#pragma unroll
+      for (int k = 0; k < kColsPerWarp; ++k) acc[k] = 0.0;
+      for (int rc = 0; rc < nrows; rc += 32 * kRowsPerLane) {
+        double yv[kRowsPerLane], av[kRowsPerLane];
+#pragma unroll
+        for (int i = 0; i < kRowsPerLane; ++i) {
+          const int r = rc + lane + 32 * i;
+          const bool in = r < nrows;
+          const double yr = (upd && in && r >= rupd) ? yprev[r] : 0.0;
+          yv[i] = yr;
+          av[i] = (in && r >= rsum) ? fma(-yr, wa, acol[r]) : 0.0;  // 0 => excluded from sums
+        }
+#pragma unroll
+        for (int k = 0; k < kColsPerWarp; ++k) {
+          const int v = warp + kPWarps * k;
+          if (v < Lc) {
+            double* pc = slab + (tl + v) * a.hp;
+            const double wc = upd ? wv[1 + v] : 0.0;
+#pragma unroll
+            for (int i = 0; i < kRowsPerLane; ++i) {
+              const int r = rc + lane + 32 * i;
+              if (r < nrows) {
+                double pv = pc[r];
+                if (upd && r >= rupd) {
+                  pv = fma(-yv[i], wc, pv);
+                  pc[r] = pv;
+                }
+                acc[k] = fma(av[i], pv, acc[k]);
+              }
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kColsPerWarp; ++k) acc[k] = warp_sum(acc[k]);
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < kColsPerWarp; ++k) {
+          const int v = warp + kPWarps * k;
+          if (v < Lc) a.part[((size_t)par * (a.sw + 1) + v) * G + g] = acc[k];
+        }
+      }
+      __syncthreads();
+      // the owner of row tcur publishes it (already updated above)
+      if (tcur >= row0 && tcur < row0 + nrows) {
+        for (int v = tid; v < Lc; v += kPThreads)
+          a.rowt[par * (a.sw + 1) + v] = slab[(tl + v) * a.hp + (tcur - row0)];
+      }
+    };
+
+    fused(c0, false);
     for (int t = c0; t < c1; ++t) {
       const int tl = t - c0;
       const int L = c1 - t;
-      const int par = parity;
-      parity ^= 1;
-      const int rbeg = max(0, t + 1 - row0);
-      SQR_TRACE(a.trace, 8 * t + 0);
-      for (int v = warp; v < L; v += kPWarps) {
-        const double* acol = slab + tl * a.hp;
-        const double* pcol = slab + (tl + v) * a.hp;
-        double s = 0.0;
-        for (int r = rbeg + lane; r < nrows; r += 32) s = fma(acol[r], pcol[r], s);
-        s = warp_sum(s);
-        if (lane == 0) a.part[((size_t)par * (a.sw + 1) + v) * G + g] = s;
-      }
-      if (t >= row0 && t < row0 + nrows) {
-        for (int v = tid; v < L; v += kPThreads)
-          a.rowt[par * (a.sw + 1) + v] = slab[(tl + v) * a.hp + (t - row0)];
-      }
+      const int par = (t - c0) & 1;
       SQR_TRACE(a.trace, 8 * t + 1);
       gb.sync();
       SQR_TRACE(a.trace, 8 * t + 2);
@@ -114,12 +167,12 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
           const int gi = q + 4 * i;
           x[i] = (v < L && gi < G) ? __ldcg(src + gi) : 0.0;
         }
-        double s = 0.0;
+        double sacc = 0.0;
 #pragma unroll
-        for (int i = 0; i < kMaxG / 4; ++i) s += x[i];
-        s += __shfl_xor_sync(0xffffffffu, s, 2);
-        s += __shfl_xor_sync(0xffffffffu, s, 1);
-        if (v < L && q == 0) vals[v] = s;
+        for (int i = 0; i < kMaxG / 4; ++i) sacc += x[i];
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, 2);
+        sacc += __shfl_xor_sync(0xffffffffu, sacc, 1);
+        if (v < L && q == 0) vals[v] = sacc;
       }
       __syncthreads();
       SQR_TRACE(a.trace, 8 * t + 3);
@@ -138,24 +191,24 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
       }
       for (int v = 1 + tid; v < L; v += kPThreads) wv[v] = tau * (rowv[v] + vals[v] / y0);
       if (g == 0 && tid == 0) a.taus[t] = tau;
-      __syncthreads();
-      SQR_TRACE(a.trace, 8 * t + 4);
+      // y for my rows below t; row t keeps beta and its R entries.
+      const int rbeg = max(0, t + 1 - row0);
       for (int r = rbeg + tid; r < nrows; r += kPThreads) {
         const double yr = nrm != 0.0 ? slab[tl * a.hp + r] / y0 : 0.0;
         slab[tl * a.hp + r] = yr;
-        double* pr = slab + (tl + 1) * a.hp + r;
-        int v = 1;
-        for (; v + 2 <= L; v += 2, pr += 2 * a.hp) {
-          const double p0 = pr[0], p1 = pr[a.hp];
-          pr[0] = fma(-yr, wv[v], p0);
-          pr[a.hp] = fma(-yr, wv[v + 1], p1);
-        }
-        if (v < L) pr[0] = fma(-yr, wv[v], pr[0]);
       }
+      __syncthreads();
       if (t >= row0 && t < row0 + nrows) {
         const int rt = t - row0;
         for (int v = 1 + tid; v < L; v += kPThreads) slab[(tl + v) * a.hp + rt] -= wv[v];
         if (tid == 0) slab[tl * a.hp + rt] = beta;
+      }
+      SQR_TRACE(a.trace, 8 * t + 4);
+      if (t + 1 < c1) {
+        fused(t + 1, true);
+      } else if (c1 < w) {
+        // last step of a sub-panel that is followed by others: nothing left
+        // to update inside the sub-panel.
       }
       __syncthreads();
       SQR_TRACE(a.trace, 8 * t + 5);
@@ -279,32 +332,91 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
   }
 }
 
-// T from G = Y^T Y and taus (one CTA).  T[c,c] = tau_c,
-// T[:c, c] = -tau_c T[:c,:c] G[:c, c]  (householder.py:52-61).
-constexpr int kTThreads = 512;
+// T from G = Y^T Y and taus (one CTA), householder.py:52-61.
+//  1. 32 x 32 diagonal blocks, one warp each, by the reference recurrence
+//     T[:c, c] = -tau_c T[:c, :c] G[:c, c] (lane i keeps row i of its block
+//     in registers);
+//  2. blocks merged left to right with the composition rule of
+//     wy_compose (householder.py:94-104): T_AB = -T_AA G_AB T_BB.
+// tau = 0 (identity / padded reflectors) gives zero rows and columns, as in
+// the recurrence.
+constexpr int kTThreads = 256;
+constexpr int kTB = 32;
 __global__ void __launch_bounds__(kTThreads, 1)
     build_t_kernel(const double* Gm, int64_t ldg, const double* taus, int j, double* T, int64_t ldt,
                    const int32_t* gate) {
-  extern __shared__ __align__(16) double Ts[];
+  extern __shared__ __align__(16) double smt[];
   if (gate && *gate) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kTThreads / 32;
-  const int ld = j | 1;
-  for (int e = tid; e < ld * j; e += kTThreads) Ts[e] = 0.0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int P = j | 1;
+  // One j x j array: T in the upper triangle, the symmetric G in the strict
+  // lower one (G(r, c), r < c, stored at M(c, r)).  M(r, c) = M[c * P + r].
+  double* M = smt;
+  double* Xs = M + (size_t)j * P;  // j x kTB scratch
+  for (int e = tid; e < j * j; e += kTThreads) {  // coalesced read of G(r, c)
+    const int r = e % j, c = e / j;
+    const double gv = Gm[(int64_t)c * ldg + r];
+    if (r < c) M[r * P + c] = gv;   // strict lower half of M holds G
+    if (r <= c) M[c * P + r] = 0.0; // upper half (T) starts at zero
+  }
   __syncthreads();
-  for (int c = 0; c < j; ++c) {
-    const double tc = taus[c];
-    for (int i = warp; i < c; i += nw) {
-      double s = 0.0;
-      for (int l = i + lane; l < c; l += 32) s = fma(Ts[l * ld + i], Gm[(int64_t)c * ldg + l], s);
-      s = warp_sum(s);
-      if (lane == 0) Ts[c * ld + i] = -tc * s;
+  const int nb = (j + kTB - 1) / kTB;
+  if (warp < nb) {
+    const int o = warp * kTB, bs = min(kTB, j - o);
+    double trow[kTB];
+#pragma unroll
+    for (int l = 0; l < kTB; ++l) trow[l] = 0.0;
+    for (int c = 0; c < bs; ++c) {
+      const double tc = taus[o + c];
+      double s = 0.0, s2 = 0.0;
+#pragma unroll
+      for (int l = 0; l < kTB; l += 2) {
+        if (l >= lane && l < c) s = fma(trow[l], M[(o + l) * P + o + c], s);  // G(o+l, o+c)
+        if (l + 1 >= lane && l + 1 < c) s2 = fma(trow[l + 1], M[(o + l + 1) * P + o + c], s2);
+      }
+      s += s2;
+      const double v = (lane < c) ? -tc * s : (lane == c ? tc : 0.0);
+#pragma unroll
+      for (int l = 0; l < kTB; ++l)
+        if (l == c) trow[l] = v;
     }
-    if (tid == 0) Ts[c * ld + c] = tc;
+    __syncwarp();
+    if (lane < bs) {
+#pragma unroll
+      for (int l = 0; l < kTB; ++l)
+        if (l >= lane && l < bs) M[(o + l) * P + o + lane] = trow[l];  // T(o+lane, o+l)
+    }
+  }
+  __syncthreads();
+  for (int a = kTB; a < j; a += kTB) {
+    const int bsz = min(kTB, j - a);
+    // X = G[0:a, a:a+bsz] T[a:a+bsz, a:a+bsz]   (T_BB upper triangular)
+    for (int e = tid; e < a * bsz; e += kTThreads) {
+      const int i = e % a, c = e / a;
+      double s = 0.0;
+      for (int l = 0; l <= c; ++l) s = fma(M[i * P + a + l], M[(a + c) * P + a + l], s);
+      Xs[c * P + i] = s;
+    }
+    __syncthreads();
+    // T[0:a, a:a+bsz] = -T[0:a, 0:a] X           (T_AA upper triangular)
+    for (int e = tid; e < a * bsz; e += kTThreads) {
+      const int i = e % a, c = e / a;
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains for ILP
+      int l = i;
+      for (; l + 4 <= a; l += 4) {
+        s0 = fma(M[l * P + i], Xs[c * P + l], s0);
+        s1 = fma(M[(l + 1) * P + i], Xs[c * P + l + 1], s1);
+        s2 = fma(M[(l + 2) * P + i], Xs[c * P + l + 2], s2);
+        s3 = fma(M[(l + 3) * P + i], Xs[c * P + l + 3], s3);
+      }
+      for (; l < a; ++l) s0 = fma(M[l * P + i], Xs[c * P + l], s0);
+      M[(a + c) * P + i] = -((s0 + s1) + (s2 + s3));
+    }
     __syncthreads();
   }
   for (int e = tid; e < j * j; e += kTThreads) {
     const int r = e % j, c = e / j;
-    T[(int64_t)c * ldt + r] = Ts[c * ld + r];
+    T[(int64_t)c * ldt + r] = r <= c ? M[c * P + r] : 0.0;
   }
 }
 
@@ -331,11 +443,15 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
     return SQR_EINVAL;
   }
   const int sms = sm_count();
-  int G = (int)std::min<int64_t>(std::min(sms, kMaxG), std::max<int64_t>(1, cdiv(mr, 64)));
+  const int64_t budget0 = (int64_t)max_smem_optin() - 4 * 1024;  // static smem of the kernel
+  // Fewest CTAs whose row slabs still hold the whole panel in shared memory
+  // (less cross-CTA reduction traffic per step), at least 64 rows each.
+  const int64_t rows_fit = std::max<int64_t>(64, budget0 / (std::max<int64_t>(wmax, 1) * 8));
+  int G = (int)std::min<int64_t>(std::min(sms, kMaxG), std::max<int64_t>(1, cdiv(mr, rows_fit)));
   const int h = (int)cdiv(mr, G);
   G = (int)cdiv(mr, h);
-  const int hp = h | 1;
-  const int64_t budget = (int64_t)max_smem_optin() - 4 * 1024;  // static smem of the kernel
+  const int hp = h;  // lanes walk rows: stride-1, no padding needed
+  const int64_t budget = budget0;
   int sw = 0;
   for (int cand : {128, 64, 32, 16, 8, 4, 2, 1}) {
     const int64_t swc = std::min<int64_t>(cand, wmax);
@@ -393,7 +509,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
 int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
             const int32_t* gate, cudaStream_t s) {
   if (j <= 0) return SQR_OK;
-  const int64_t smem = (int64_t)(j | 1) * j * 8;
+  const int64_t smem = ((int64_t)(j | 1) * j + (int64_t)(j | 1) * kTB) * 8;
   static int configured = 0;
   if (smem > configured) {
     SQR_CUDA(cudaFuncSetAttribute(build_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

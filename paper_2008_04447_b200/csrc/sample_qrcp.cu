@@ -73,12 +73,17 @@ __device__ __forceinline__ void warp_argmax(double& v, int& p, int& l) {
   }
 }
 
-// One pivot step costs one grid barrier and one __syncthreads: after the
-// barrier every WARP independently (and identically) picks the global winner
-// from the published candidates, loads the winner column, and rebuilds the
-// reflector in registers, writing y to its own shared-memory slice; threads
-// then update their own columns and fold the next step's local candidate
-// into the same pass.
+// Pivot step j (one grid barrier):
+//   pass 1  every column: w_c = tau (y . d_c), new row-j entry d_c[j] - w_c,
+//           norm downdate (+ exact recompute under the 2^-40 guard), local
+//           candidate for step j+1; the winner column is written out.
+//   publish the CTA candidate for step j+1 (value, position, updated column)
+//           and ARRIVE at the grid barrier;
+//   overlap warps 1..7: pass 2, d_c[j:] -= w_c y  (the rank-1 update)
+//           warp 0:     wait for the barrier, pick the global winner, load
+//                       its column, build reflector j+1 (y, tau, beta)
+//   __syncthreads.
+// so the rank-1 update hides the barrier and the two L2 round trips.
 __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double wv_s[kSqThreads / 32];
@@ -101,8 +106,9 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
   double* cols = sm;                                   // cap x ldS
   double* nsq = sm + (size_t)a.cap * a.ldS;            // w
   double* rsq = nsq + a.w;                             // w
-  double* ysh = rsq + a.w;                             // ell (+2): the current reflector
-  int* pos = reinterpret_cast<int*>(ysh + ell + 2);    // w
+  double* wcol = rsq + a.w;                            // w: tau * (y . d_c) of the current step
+  double* ybuf = wcol + a.w;                           // [2][ell + 2]: reflectors by step parity
+  int* pos = reinterpret_cast<int*>(ybuf + 2 * (ell + 2));  // w
 
   auto colp = [&](int lc) -> double* {
     return lc < a.cap ? cols + (size_t)lc * a.ldS : a.spill + (size_t)(col0 + lc) * ell;
@@ -140,6 +146,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
     const double s = s0 + s1;
     nsq[lc] = s;
     rsq[lc] = s;
+    wcol[lc] = 0.0;
     pos[lc] = col0 + lc;
     my_sum += s;
     my_max = fmax(my_max, s);
@@ -161,6 +168,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       if (lane == 0) {
         nsq[lc] = s;
         rsq[lc] = s;
+        wcol[lc] = 0.0;
         pos[lc] = col0 + lc;
         my_sum += s;
         my_max = fmax(my_max, s);
@@ -206,11 +214,9 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
   }
   if (g == 0 && tid == 0 && a.first) a.st->floor_sq = sample_floor;
 
-  int achieved = 0;
-  for (int j = 0; j < a.bb; ++j) {
-    const int par = j & 1;
-    SQR_TRACE(a.trace, 8 * j + 0);
-    // ---- CTA candidate (folded into the previous pass) -> publish.
+  // CTA candidate -> publish (value, position, column rows jn.. updated by
+  // reflector jn-1 with coefficient wcol / y of parity (jn-1)&1).
+  auto publish = [&](int jn) {
     warp_argmax(cbv, cbp, cbl);
     if (lane == 0) {
       wv_s[warp] = cbv;
@@ -218,107 +224,137 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       wl_s[warp] = cbl;
     }
     __syncthreads();
-    {
-      double v = lane < (kSqThreads >> 5) ? wv_s[lane] : -1.0;
-      int p = lane < (kSqThreads >> 5) ? wp_s[lane] : INT_MAX;
-      int l = lane < (kSqThreads >> 5) ? wl_s[lane] : -1;
-      warp_argmax(v, p, l);
-      if (warp == 0 && lane == 0) {
-        a.cval[par * G + g] = v;
-        a.cpos[par * G + g] = p;
+    double v = lane < (kSqThreads >> 5) ? wv_s[lane] : -1.0;
+    int p = lane < (kSqThreads >> 5) ? wp_s[lane] : INT_MAX;
+    int l = lane < (kSqThreads >> 5) ? wl_s[lane] : -1;
+    warp_argmax(v, p, l);
+    const int par = jn & 1;
+    if (warp == 0 && lane == 0) {
+      a.cval[par * G + g] = v;
+      a.cpos[par * G + g] = p;
+    }
+    double* dst = a.ccol + ((size_t)par * G + g) * ell;
+    if (l >= 0 && (!a.reg_spill || l < a.cap)) {
+      if (warp == 0) {
+        const double* d = colp(l);
+        const bool lazy = !a.warp_spill || l < a.cap;  // columns updated by pass 2
+        if (jn == 0 || !lazy) {
+          for (int r = jn + lane; r < ell; r += 32) dst[r] = d[r];
+        } else {  // pass 2 of step jn-1 has not run yet: apply it on the fly
+          const double* yp = ybuf + ((jn - 1) & 1) * (ell + 2);
+          const double wl = wcol[l];
+          for (int r = jn + lane; r < ell; r += 32) dst[r] = fma(-yp[r - (jn - 1)], wl, d[r]);
+        }
       }
-      double* dst = a.ccol + ((size_t)par * G + g) * ell;
-      if (l >= 0 && (!a.reg_spill || l < a.cap)) {
-        if (warp == 0) {
-          const double* d = colp(l);
-          for (int r = j + lane; r < ell; r += 32) dst[r] = d[r];
-        }
-      } else if (l >= 0 && warp == (l - a.cap) % 8) {
-        const int iw = (l - a.cap) / 8;
+    } else if (l >= 0 && warp == (l - a.cap) % 8) {
+      const int iw = (l - a.cap) / 8;
 #pragma unroll
-        for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
-          // select chain, not xs[iw][qq]: keeps xs in registers
-          double v = xs[0][qq];
+      for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+        double vv = xs[0][qq];
 #pragma unroll
-          for (int i = 1; i < kSpillPerWarp; ++i) {
-            const double c = xs[i][qq];
-            asm("{ .reg .pred p; setp.eq.s32 p, %2, %3; selp.f64 %0, %1, %0, p; }" : "+d"(v) : "d"(c), "r"(iw), "r"(i));
-          }
-          const int r = lane + 32 * qq;
-          if (r >= j && r < ell) dst[r] = v;
+        for (int i = 1; i < kSpillPerWarp; ++i) {
+          const double c = xs[i][qq];
+          asm("{ .reg .pred p; setp.eq.s32 p, %2, %3; selp.f64 %0, %1, %0, p; }" : "+d"(vv) : "d"(c), "r"(iw), "r"(i));
         }
+        const int r = lane + 32 * qq;
+        if (r >= jn && r < ell) dst[r] = vv;
       }
     }
-    SQR_TRACE(a.trace, 8 * j + 1);
-    gb.sync();
-    SQR_TRACE(a.trace, 8 * j + 2);
-    // ---- global winner + reflector: warp 0 alone reads the published
-    // candidates and the winner column (one reader per CTA keeps the L2
-    // hot lines cool) and broadcasts y / tau / beta through shared memory.
-    if (warp == 0) {
-      double bv = -1.0;
-      int bp = INT_MAX, bl = -1;
-      for (int i = lane; i < G; i += 32) {
-        const double v = __ldcg(a.cval + par * G + i);
-        const int p = __ldcg(a.cpos + par * G + i);
-        if (better(v, p, bv, bp)) {
-          bv = v;
-          bp = p;
-          bl = i;
-        }
-      }
-      warp_argmax(bv, bp, bl);
-      const int len = ell - j;
-      double x[kMaxRowsPerLane];
-      double s1 = 0.0, nrm = 0.0, beta = 0.0, tau = 0.0, y0 = 1.0;
-      const bool go = bv > rank_floor_sq;
-      if (go) {
-        const double* u = a.ccol + ((size_t)par * G + bl) * ell + j;
-#pragma unroll
-        for (int i = 0; i < kMaxRowsPerLane; ++i) {
-          const int r = lane + 32 * i;
-          x[i] = r < len ? __ldcg(u + r) : 0.0;
-        }
-        for (int r = lane + 32 * kMaxRowsPerLane; r < len; r += 32) {  // tall samples only
-          const double v = __ldcg(u + r);
-          s1 = fma(v, v, s1);
-        }
-#pragma unroll
-        for (int i = 0; i < kMaxRowsPerLane; ++i)
-          if (lane + 32 * i >= 1) s1 = fma(x[i], x[i], s1);
-        s1 = warp_sum(s1);
-        const double u0 = __shfl_sync(0xffffffffu, x[0], 0);
-        nrm = sqrt(fma(u0, u0, s1));
-        if (nrm != 0.0) {
-          beta = (u0 >= 0.0 ? -1.0 : 1.0) * nrm;
-          y0 = u0 - beta;
-          tau = 2.0 / (1.0 + s1 / (y0 * y0));
-        }
-#pragma unroll
-        for (int i = 0; i < kMaxRowsPerLane; ++i) {
-          const int r = lane + 32 * i;
-          if (r < len) ysh[r] = (r == 0) ? 1.0 : (nrm != 0.0 ? x[i] / y0 : 0.0);
-        }
-        for (int r = lane + 32 * kMaxRowsPerLane; r < len; r += 32) ysh[r] = nrm != 0.0 ? __ldcg(u + r) / y0 : 0.0;
-      }
-      if (lane == 0) {
-        bc_s.go = go;
-        bc_s.pc = bp;
-        bc_s.beta = beta;
-        bc_s.tau = tau;
+  };
+
+  // Global winner of step jn + reflector, by ONE warp (lane 0 waited).
+  auto winner = [&](int jn) {
+    const int par = jn & 1;
+    double bv = -1.0;
+    int bp = INT_MAX, bl = -1;
+    for (int i = lane; i < G; i += 32) {
+      const double v = __ldcg(a.cval + par * G + i);
+      const int p = __ldcg(a.cpos + par * G + i);
+      if (better(v, p, bv, bp)) {
+        bv = v;
+        bp = p;
+        bl = i;
       }
     }
-    __syncthreads();
-    if (!bc_s.go) break;  // reference.py:123-124 (uniform across the grid)
+    warp_argmax(bv, bp, bl);
+    const int len = ell - jn;
+    double* ysh = ybuf + par * (ell + 2);
+    double x[kMaxRowsPerLane];
+    double s1 = 0.0, nrm = 0.0, beta = 0.0, tau = 0.0, y0 = 1.0;
+    const bool go = bv > rank_floor_sq;  // reference.py:123-124
+    if (go) {
+      const double* u = a.ccol + ((size_t)par * G + bl) * ell + jn;
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = lane + 32 * i;
+        x[i] = r < len ? __ldcg(u + r) : 0.0;
+      }
+      for (int r = lane + 32 * kMaxRowsPerLane; r < len; r += 32) {  // tall samples only
+        const double v = __ldcg(u + r);
+        s1 = fma(v, v, s1);
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i)
+        if (lane + 32 * i >= 1) s1 = fma(x[i], x[i], s1);
+      s1 = warp_sum(s1);
+      const double u0 = __shfl_sync(0xffffffffu, x[0], 0);
+      nrm = sqrt(fma(u0, u0, s1));
+      if (nrm != 0.0) {
+        beta = (u0 >= 0.0 ? -1.0 : 1.0) * nrm;
+        y0 = u0 - beta;
+        tau = 2.0 / (1.0 + s1 / (y0 * y0));
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = lane + 32 * i;
+        if (r < len) ysh[r] = (r == 0) ? 1.0 : (nrm != 0.0 ? x[i] / y0 : 0.0);
+      }
+      for (int r = lane + 32 * kMaxRowsPerLane; r < len; r += 32) ysh[r] = nrm != 0.0 ? __ldcg(u + r) / y0 : 0.0;
+    }
+    if (lane == 0) {
+      bc_s.go = go;
+      bc_s.pc = bp;
+      bc_s.beta = beta;
+      bc_s.tau = tau;
+    }
+  };
+
+  // Pass 2 of step j: d[j:] -= w y on shared-memory columns; threads
+  // [t0, kSqThreads) cooperate, one column per thread.
+  auto pass2 = [&](int j, int t0) {
+    const double* yw = ybuf + (j & 1) * (ell + 2);
+    const int nsm = a.warp_spill ? min(ncols, a.cap) : ncols;
+    const int len = ell - j;
+    for (int lc = tid - t0; lc < nsm; lc += kSqThreads - t0) {
+      if (pos[lc] < 0) continue;
+      const double wvv = wcol[lc];
+      double* dj = (a.warp_spill ? cols + (size_t)lc * a.ldS : colp(lc)) + j;
+      int r = 0;
+      for (; r + 2 <= len; r += 2) {
+        const double p0 = dj[r], p1 = dj[r + 1];
+        dj[r] = fma(-yw[r], wvv, p0);
+        dj[r + 1] = fma(-yw[r + 1], wvv, p1);
+      }
+      if (r < len) dj[r] = fma(-yw[r], wvv, dj[r]);
+    }
+  };
+
+  publish(0);
+  gb.sync();
+  if (warp == 0) winner(0);
+  __syncthreads();
+
+  int achieved = 0;
+  for (int j = 0; j < a.bb; ++j) {
+    SQR_TRACE(a.trace, 8 * j + 0);
+    if (!bc_s.go) break;  // uniform across the grid
     const int pc = bc_s.pc;
     const double beta = bc_s.beta, tau = bc_s.tau;
     const int len = ell - j;
-    const double* yw = ysh;
+    const double* yw = ybuf + (j & 1) * (ell + 2);
     if (g == 0 && tid == 0) a.taus[j] = tau;
-    SQR_TRACE(a.trace, 8 * j + 3);
 
-    // ---- apply H_j to my columns, downdate norms (reference.py:131-149),
-    // and track the next step's local candidate.
+    // ---- pass 1: dots, downdates, next candidate; winner column written out.
     cbv = -1.0;
     cbp = INT_MAX;
     cbl = -1;
@@ -342,7 +378,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       }
       const int pn = (p == j) ? pc : p;  // the column that sat at position j moves to pc
       pos[lc] = pn;
-      double* dj = d + j;
+      const double* dj = d + j;
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       int r = 0;
       for (; r + 4 <= len; r += 4) {
@@ -353,17 +389,15 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       }
       for (; r < len; ++r) d0 = fma(yw[r], dj[r], d0);
       const double wvv = tau * ((d0 + d1) + (d2 + d3));
-      for (r = 0; r < len; ++r) dj[r] = fma(-yw[r], wvv, dj[r]);
-      const double rj = dj[0];
+      wcol[lc] = wvv;
+      const double rj = fma(-yw[0], wvv, dj[0]);
       double ns = nsq[lc] - rj * rj;
       if (ns < kNormGuard * rsq[lc]) {
         double e0 = 0.0, e1 = 0.0;
-        int q = j + 1;
-        for (; q + 2 <= ell; q += 2) {
-          e0 = fma(d[q], d[q], e0);
-          e1 = fma(d[q + 1], d[q + 1], e1);
+        for (int qn = 1; qn < len; ++qn) {
+          const double v = fma(-yw[qn], wvv, dj[qn]);
+          if (qn & 1) e1 = fma(v, v, e1); else e0 = fma(v, v, e0);
         }
-        if (q < ell) e0 = fma(d[q], d[q], e0);
         ns = e0 + e1;
         rsq[lc] = ns;
       } else {
@@ -376,9 +410,8 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
         cbl = lc;
       }
     }
-    SQR_TRACE(a.trace, 8 * j + 4);
-    // Register-resident spill columns: one warp per column.  Written as an
-    // explicitly instantiated lambda per column so xs stays in registers.
+    SQR_TRACE(a.trace, 8 * j + 1);
+    // Register-resident spill columns: one warp per column, fully updated here.
     if (a.reg_spill) {
       auto spill_col = [&](double(&xc)[kMaxRowsPerLane], const int i) {
         const int lc = a.cap + warp + 8 * i;
@@ -448,7 +481,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       spill_col(xs[3], 3);
       spill_col(xs[4], 4);
     }
-    // Spilled (L2-resident) columns: one warp per column, coalesced rows.
+    // Spilled (L2-resident) columns (no reg mode): one warp per column, full update.
     for (int lc = a.cap + warp; a.warp_spill && !a.reg_spill && lc < ncols; lc += kSqThreads / 32) {
       const int p = pos[lc];
       if (p < 0) continue;
@@ -470,17 +503,17 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
         continue;
       }
       const int pn = (p == j) ? pc : p;
-      double xs[kMaxRowsPerLane];
+      double xg[kMaxRowsPerLane];
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = j + lane + 32 * i;
-        xs[i] = r < ell ? __ldcg(d + r) : 0.0;
+        xg[i] = r < ell ? __ldcg(d + r) : 0.0;
       }
       double part = 0.0;
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = j + lane + 32 * i;
-        if (r < ell) part = fma(yw[r - j], xs[i], part);
+        if (r < ell) part = fma(yw[r - j], xg[i], part);
       }
       const double wvv = tau * warp_sum(part);
       double ex = 0.0;
@@ -488,12 +521,12 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = j + lane + 32 * i;
         if (r < ell) {
-          xs[i] = fma(-yw[r - j], wvv, xs[i]);
-          d[r] = xs[i];
-          if (r > j) ex = fma(xs[i], xs[i], ex);
+          xg[i] = fma(-yw[r - j], wvv, xg[i]);
+          d[r] = xg[i];
+          if (r > j) ex = fma(xg[i], xg[i], ex);
         }
       }
-      const double rj = __shfl_sync(0xffffffffu, xs[0], 0);
+      const double rj = __shfl_sync(0xffffffffu, xg[0], 0);
       double ns = nsq[lc] - rj * rj;
       const bool recompute = ns < kNormGuard * rsq[lc];
       ex = warp_sum(ex);
@@ -503,16 +536,34 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
         if (recompute) rsq[lc] = ex;
         nsq[lc] = ns;
         pos[lc] = pn;
+        if (better(ns, pn, cbv, cbp)) {
+          cbv = ns;
+          cbp = pn;
+          cbl = lc;
+        }
       }
       __syncwarp();
-      if (lane == 0 && better(ns, pn, cbv, cbp)) {
-        cbv = ns;
-        cbp = pn;
-        cbl = lc;
+    }
+    achieved = j + 1;
+    SQR_TRACE(a.trace, 8 * j + 2);
+    if (j + 1 < a.bb) {
+      publish(j + 1);
+      gb.arrive();
+      SQR_TRACE(a.trace, 8 * j + 3);
+      if (warp == 0) {
+        if (lane == 0) gb.wait_lane0();
+        __syncwarp();
+        winner(j + 1);
+      } else {
+        pass2(j, 32);
       }
+      SQR_TRACE(a.trace, 8 * j + 4);
+      __syncthreads();
+    } else {
+      pass2(j, 0);
+      __syncthreads();
     }
     SQR_TRACE(a.trace, 8 * j + 5);
-    achieved = j + 1;
   }
   __syncthreads();
   if (a.reg_spill) {
@@ -586,15 +637,15 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   // At least 32 columns per CTA (amortise the per-step barrier), enough CTAs
   // to keep every column in shared memory when possible, one CTA per SM.
   const int ldS = (int)(ell | 1);
-  const int64_t fixed_per_col = 16 + 4;
-  const int64_t smem_avail = (int64_t)max_smem_optin() - 2048 - (ell + 2) * 8 - 64;
+  const int64_t fixed_per_col = 24 + 4;
+  const int64_t smem_avail = (int64_t)max_smem_optin() - 2048 - 2 * (ell + 2) * 8 - 64;
   const int64_t fit = std::max<int64_t>(1, smem_avail / ((int64_t)ldS * 8 + fixed_per_col));
   const int64_t ntc = std::max<int64_t>(nt, 1);
   int G = (int)std::min<int64_t>(sms, std::max<int64_t>(cdiv(ntc, 32), cdiv(ntc, fit)));
   G = std::max(G, 1);
   const int w = (int)cdiv(ntc, G);
   G = (int)cdiv(ntc, w);
-  const int64_t fixed = (int64_t)w * 16 + (ell + 2) * 8 + (int64_t)w * 4 + 64;
+  const int64_t fixed = (int64_t)w * 24 + 2 * (ell + 2) * 8 + (int64_t)w * 4 + 64;
   const int64_t budget = (int64_t)max_smem_optin() - 2048 - fixed;
   int cap = (int)std::max<int64_t>(0, std::min<int64_t>(w, budget / ((int64_t)ldS * 8)));
   const int64_t smem = (int64_t)cap * ldS * 8 + fixed;

@@ -88,13 +88,38 @@ if os.environ.get("SQR_TRACE"):
     for name, fn in (("sample_qrcp", sample), ("panel", panel)):
         tr.zero_()
         L.sqr_debug_trace(tr.data_ptr())
+        L.sqr_profile_enable(64)
         fn()
         torch.cuda.synchronize()
         L.sqr_debug_trace(None)
+        prof = _lib.profile_collect()
+        L.sqr_profile_enable(0)
         t = tr.cpu().numpy().reshape(256, 8)[:128].astype(np.float64)
-        ok = t[:, 0] > 0
-        t = t[ok]
-        base = t[:, 0:1]
-        d = np.diff(np.concatenate([t[:, :6], t[1:, :1].tolist() + [[t[-1, 5]]]], axis=1), axis=1) / 1e3
-        print(name, "per-step phase us (mean over steps):", np.round(d.mean(axis=0), 2), "steps", len(t))
-        print("   step0", np.round(d[0], 2), "step64", np.round(d[min(64, len(d) - 1)], 2))
+        # per step: deltas between consecutive nonzero stamps (slot order), and to the next step
+        flat = []
+        for j in range(t.shape[0]):
+            for k in range(8):
+                if t[j, k] > 0:
+                    flat.append((j, k, t[j, k]))
+        deltas = {}
+        for (j1, k1, v1), (j2, k2, v2) in zip(flat, flat[1:]):
+            key = f"{k1}->{k2}" if j2 == j1 else f"{k1}->next{k2}"
+            deltas.setdefault(key, []).append((v2 - v1) / 1e3)
+        kern = {k: round(v[0] * 1e3, 1) for k, v in prof.items() if v[1]}
+        print(name, "kernel us:", kern)
+        print("   ", {k: round(float(np.mean(v)), 2) for k, v in deltas.items()})
+
+if only == "build_t":
+    Gd = ColMajor(torch.randn((b, b), dtype=torch.float64, device=dev, generator=g), b, b, b)
+    Gd.t.copy_(Gd.t + Gd.t.T)
+    tau = torch.rand(b, dtype=torch.float64, device=dev, generator=g) + 1.0
+    Tt = ColMajor.empty(b, b, dev)
+    wsb = torch.zeros(200 << 20, dtype=torch.uint8, device=dev)
+    # sqr_build_t computes G from Y; time T-from-G via the driver-internal path: use Y = identity-ish
+    Yi = ColMajor.empty(m, b, dev, zero=True)
+    Yi.t[:, :] = torch.randn((b, m), dtype=torch.float64, device=dev, generator=g) * 1e-3
+    L.sqr_profile_enable(64)
+    for _ in range(5):
+        _lib.check(L.sqr_build_t(Yi.ptr, Yi.ld, m, b, tau.data_ptr(), Tt.ptr, Tt.ld, wsb.data_ptr(), wsb.numel(), s))
+    torch.cuda.synchronize()
+    print({k: (round(v[0] * 1e3 / max(v[1], 1), 1), v[1]) for k, v in _lib.profile_collect().items() if v[1]})
