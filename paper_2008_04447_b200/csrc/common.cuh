@@ -191,6 +191,9 @@ struct GemmDyn {
   const double* pre = nullptr;
   int64_t ldpre = 0;
   int npre = 0;
+  // optional cap: N <= *limit - limit_off (dynamic panel width)
+  const int32_t* limit = nullptr;
+  int limit_off = 0;
 };
 
 __host__ __device__ constexpr int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
@@ -212,7 +215,8 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
                 int64_t ws_bytes, cudaStream_t s);
 int64_t panel_workspace(int64_t w);
 int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
-             double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s);
+             double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s,
+             int64_t c0 = 0);
 int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
             const int32_t* gate, cudaStream_t s);
 int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed, uint64_t offset,

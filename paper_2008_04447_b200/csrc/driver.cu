@@ -25,10 +25,16 @@ struct Carve {
   }
 };
 
+constexpr int64_t kLeaf = 32;
+struct PanelScratch {
+  double *GW, *W, *Tl;  // lw x (lw + bmax), lw x bmax, lw x lw
+  static int64_t doubles(int64_t bmax) { return kLeaf * (kLeaf + bmax) + kLeaf * bmax + kLeaf * kLeaf + 64; }
+};
+
 constexpr int64_t kGemmWsBytes = (int64_t)8 * 148 * 72 * 256 * 8 + 8 * 148 * 8 * 4 + 4096;
 
 struct RqrcpWs {
-  double *Bcur, *Bnext, *Bf, *stau, *Ypan, *Gm, *Wt, *W, *OmT, *gemm;
+  double *Bcur, *Bnext, *Bf, *stau, *Ypan, *Gm, *Wt, *W, *OmT, *gemm, *pscr;
   int64_t* lperm;
   int32_t* moves;
   void *sample, *panel;
@@ -56,8 +62,49 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.Wt = c.take<double>(b * (n + b));
   w.W = c.take<double>(b * n);
   w.OmT = (need_omega || resample) ? c.take<double>(m * ell) : nullptr;
+  w.pscr = c.take<double>(PanelScratch::doubles(b));
   w.total = c.off + 256;
   return w;
+}
+
+// Panel QR (randomized.py:107-130 / reference.py:281-291) as 32-wide leaves
+// on the cooperative panel kernel; between leaves the leaf's reflectors are
+// applied to the rest of the panel in compact-WY form with the DMMA GEMMs:
+//   [G_l | Wt] = Y_l^T [Y_l | P_rest];  T_l = build_t(G_l);  P_rest += Y_l (-T_l^T Wt).
+// The panel width may be dynamic (wstat < 0: st->sample_achieved); leaves
+// and WY updates never touch columns beyond it.
+int panel_factor(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t wstat, double* Y, int64_t ldy,
+                 double* taus, int stop_at_zero, sqr_status* st, void* pws, int64_t pwsb, const PanelScratch& sc,
+                 double* gws, cudaStream_t s) {
+  int rc;
+  for (int64_t c0 = 0; c0 < bb; c0 += kLeaf) {
+    const int64_t lwe = std::min(kLeaf, bb - c0);
+    if ((rc = panel_qr(P, lda, mr, wstat, lwe, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s, c0))) return rc;
+    const int64_t rest = bb - (c0 + lwe);
+    if (rest <= 0 || mr - c0 <= 0) continue;
+    const double* Yl = Y + c0 + c0 * ldy;
+    double* Prest = P + c0 + (c0 + lwe) * lda;
+    const int32_t* lim = wstat < 0 ? &st->sample_achieved : nullptr;
+    GemmDyn d1{&st->stop, nullptr, 0};
+    d1.pre = Yl;
+    d1.ldpre = ldy;
+    d1.npre = (int)lwe;
+    d1.limit = lim;
+    d1.limit_off = (int)c0;
+    const int64_t ld = kLeaf;
+    if ((rc = gemm_tn(lwe, lwe + rest, mr - c0, 1.0, Yl, ldy, Prest, lda, 0.0, nullptr, 0, sc.GW, ld, gws,
+                      kGemmWsBytes, s, d1)))
+      return rc;
+    if ((rc = build_t(sc.GW, ld, taus + c0, lwe, sc.Tl, kLeaf, &st->stop, s))) return rc;
+    GemmDyn d2{&st->stop, nullptr, 0};
+    d2.limit = lim;
+    d2.limit_off = (int)(c0 + lwe);
+    if ((rc = gemm_tn(lwe, rest, lwe, -1.0, sc.Tl, kLeaf, sc.GW + lwe * ld, ld, 0.0, nullptr, 0, sc.W, ld, gws,
+                      kGemmWsBytes, s, d2)))
+      return rc;
+    if ((rc = gemm_nn(mr - c0, rest, lwe, 1.0, Yl, ldy, sc.W, ld, 1.0, Prest, lda, Prest, lda, s, d2))) return rc;
+  }
+  return SQR_OK;
 }
 
 // One compact-WY block reflection of the trailing matrix (randomized.py:203-210)
@@ -141,7 +188,11 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
                           w.sample_bytes, s)))
       return rc;
     if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
-    if ((rc = panel_qr(P, lda, mr, -1, bb, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, s))) return rc;
+    {
+      PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
+      if ((rc = panel_factor(P, lda, mr, bb, -1, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
+        return rc;
+    }
     if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s)))
       return rc;
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
@@ -243,7 +294,12 @@ extern "C" int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t 
     if ((rc = gemm_nn(mr, bb, i0, -1.0, Yg + i0, ldy, Wg + i0 * ldw, ldw, 1.0, A + i0 + i0 * lda, lda, tw.Pn, m,
                       s, gate)))
       return rc;
-    if ((rc = panel_qr(tw.Pn, m, mr, -1, bb, Ypan, ldy, taus + i0, 1, st, w.panel, w.panel_bytes, s))) return rc;
+    {
+      PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
+      if ((rc = panel_factor(tw.Pn, m, mr, bb, -1, Ypan, ldy, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm,
+                             s)))
+        return rc;
+    }
     if ((rc = copy_upper(tw.Pn, m, Rg + i0 + i0 * ldr, ldr, bb, &st->stop, s))) return rc;
     // [Y2^T Y2 | G] = Y2^T [Y2 | A[i0:, tcols]]   (randomized.py:311,322) in one sweep
     GemmDyn shP{&st->stop, &st->bhat, kShiftB};
@@ -295,6 +351,7 @@ extern "C" int64_t sqr_qr_blocked_workspace(int64_t m, int64_t n, int64_t /*k*/,
   c.take<double>(b * (n + b));  // [G | Wt]
   c.take<double>(b * n);        // W
   c.take<sqr_status>(1);
+  c.take<double>(PanelScratch::doubles(b));
   return c.off + 256;
 }
 
@@ -318,6 +375,7 @@ extern "C" int sqr_qr_blocked(double* A, int64_t lda, int64_t m, int64_t n, int6
   double* Wt = c.take<double>(b * (n + b));
   double* W = c.take<double>(b * n);
   sqr_status* st = c.take<sqr_status>(1);
+  double* pscr = c.take<double>(PanelScratch::doubles(b));
   (void)Gm;
   SQR_CUDA(cudaMemsetAsync(st, 0, sizeof(sqr_status), s));
   int rc;
@@ -325,7 +383,10 @@ extern "C" int sqr_qr_blocked(double* A, int64_t lda, int64_t m, int64_t n, int6
     const int64_t bb = std::min(b, k - i0), mr = m - i0, nt = n - i0;
     double* P = A + i0 + i0 * lda;
     double* TJ = T + (i0 / b) * b * b;
-    if ((rc = panel_qr(P, lda, mr, bb, bb, Ypan, m, taus + i0, 0, st, pws, pb, s))) return rc;
+    {
+      PanelScratch sc{pscr, pscr + kLeaf * (kLeaf + b), pscr + kLeaf * (kLeaf + b) + kLeaf * b};
+      if ((rc = panel_factor(P, lda, mr, bb, bb, Ypan, m, taus + i0, 0, st, pws, pb, sc, gws, s))) return rc;
+    }
     if ((rc = trailing_update(P, lda, mr, nt, bb, Ypan, m, taus + i0, TJ, b, Wt, W, b, st, gws, s))) return rc;
   }
   return SQR_OK;

@@ -103,6 +103,8 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (E) E += (int64_t)sh * lde;
     }
   }
+  const int Npart = N;  // split-K partial stride (before the limit, as in splitk_reduce)
+  if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
   if ((int)blockIdx.x * Cfg::BN >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
@@ -165,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (nsplit > 1) {
     // Split-K: store the raw partial as part[split][n][i] (ld MT); the
     // separate splitk_reduce kernel sums the splits in index order.
-    double* mine = part + (int64_t)split * N * MT;
+    double* mine = part + (int64_t)split * Npart * MT;
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -217,8 +219,9 @@ __global__ void __launch_bounds__(256)
       if (E) E += (int64_t)sh * lde;
     }
   }
+  const int64_t stride = (int64_t)N * MT;  // partial layout uses N before the limit
+  if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
   const int64_t total = (int64_t)M * N;
-  const int64_t stride = (int64_t)N * MT;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % M), n = (int)(e / M);
     const double* src = part + (int64_t)n * MT + i;
@@ -309,6 +312,7 @@ __global__ void __launch_bounds__(kThreads, 2)
       if (E) E += (int64_t)sh * lde;
     }
   }
+  if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
   const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
   if (n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;

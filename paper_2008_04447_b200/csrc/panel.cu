@@ -50,6 +50,7 @@ struct PanelArgs {
   double* wpart;  // [G][sw*wmax]   WY partials
   double* wred;   // [sw*wmax]      WY reduced
   unsigned long long* trace;
+  int c0;         // leaf offset: this launch factors panel columns [c0, c0 + wmax), rows [c0, mr)
 };
 
 __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
@@ -60,7 +61,20 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
   if (a.st->stop) return;
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int w = a.wstat < 0 ? min(a.st->sample_achieved, a.wmax) : a.wstat;
+  // Leaf view: columns [c0, c0 + wmax) of the panel, rows [c0, mr).
+  const int lc0 = a.c0;
+  const int wglob = a.wstat < 0 ? a.st->sample_achieved : a.wstat;
+  const bool prior_stop = lc0 > 0 && a.st->bhat < lc0;  // an earlier leaf hit a zero column
+  const int w = prior_stop ? 0 : max(0, min(wglob - lc0, a.wmax));
+  if (lc0 > 0) {
+    if (g == 0)  // explicit Y is zero above the leaf's first row
+      for (int e = tid; e < lc0 * a.wmax; e += kPThreads)
+        a.Y[(int64_t)(lc0 + e / lc0) * a.ldy + (e % lc0)] = 0.0;
+    a.P += lc0 + (int64_t)lc0 * a.ldp;
+    a.Y += lc0 + (int64_t)lc0 * a.ldy;
+    a.taus += lc0;
+    a.mr -= lc0;
+  }
   const int row0 = g * a.h;
   const int nrows = max(0, min(a.h, a.mr - row0));
   GridBarrier gb;
@@ -323,11 +337,13 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
   for (int c = written; c < a.wmax; ++c)
     for (int r = tid; r < nrows; r += kPThreads) a.Y[(int64_t)c * a.ldy + row0 + r] = 0.0;
   if (g == 0 && tid == 0) {
-    a.st->bhat = bhat;
     for (int c = bhat; c < a.wmax; ++c) a.taus[c] = 0.0;
-    if (bhat == 0 && a.stop_at_zero) {
-      a.st->stop = 1;
-      a.st->reason = SQR_STOP_PANEL_ZERO;
+    if (!prior_stop) {
+      a.st->bhat = lc0 + bhat;
+      if (lc0 == 0 && bhat == 0 && a.stop_at_zero) {
+        a.st->stop = 1;
+        a.st->reason = SQR_STOP_PANEL_ZERO;
+      }
     }
   }
 }
@@ -432,8 +448,8 @@ int64_t panel_workspace(int64_t w) {
 // whose slab + WY scratch fits in shared memory.
 int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
              double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes,
-             cudaStream_t s) {
-  if (mr <= 0 || wmax <= 0) return SQR_OK;
+             cudaStream_t s, int64_t c0) {
+  if (mr - c0 <= 0 || wmax <= 0) return SQR_OK;
   if (wmax > 128) {
     set_error("panel_qr: width %lld > 128", (long long)wmax);
     return SQR_EINVAL;
@@ -447,9 +463,13 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   // Fewest CTAs whose row slabs still hold the whole panel in shared memory
   // (less cross-CTA reduction traffic per step), at least 64 rows each.
   const int64_t rows_fit = std::max<int64_t>(64, budget0 / (std::max<int64_t>(wmax, 1) * 8));
-  int G = (int)std::min<int64_t>(std::min(sms, kMaxG), std::max<int64_t>(1, cdiv(mr, rows_fit)));
-  const int h = (int)cdiv(mr, G);
-  G = (int)cdiv(mr, h);
+  // ~256 rows per CTA: enough work per step to cover the barrier, few enough
+  // partials that the per-step reduction stays cheap.
+  const int64_t mrl = mr - c0;
+  const int64_t rows_target = std::max<int64_t>(64, std::min<int64_t>(rows_fit, 256));
+  int G = (int)std::min<int64_t>(std::min(sms, kMaxG), std::max<int64_t>(1, cdiv(mrl, rows_target)));
+  const int h = (int)cdiv(mrl, G);
+  G = (int)cdiv(mrl, h);
   const int hp = h;  // lanes walk rows: stride-1, no padding needed
   const int64_t budget = budget0;
   int sw = 0;
@@ -471,6 +491,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   a.P = P;
   a.ldp = ldp;
   a.mr = (int)mr;
+  a.c0 = (int)c0;
   a.wstat = (int)w;
   a.wmax = (int)wmax;
   a.sw = sw;
