@@ -224,7 +224,7 @@ int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
 int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm, const int32_t* moves,
                 const sqr_status* st, int64_t max_moves, cudaStream_t s);
 int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
-                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, cudaStream_t s);
+                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s);
 int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s);
 int iota(int64_t* p, int64_t n, cudaStream_t s);
 int copy_upper(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, const int32_t* gate,

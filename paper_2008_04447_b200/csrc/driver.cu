@@ -206,7 +206,7 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
           return rc;
         stream_pos += (uint64_t)(ell * (m - a1));
       } else {
-        if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, b, Bn, ell, st, s))) return rc;
+        if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, bb, Bn, ell, st, w.Gm, s))) return rc;
       }
       std::swap(Bc, Bn);
     }
@@ -334,7 +334,7 @@ extern "C" int sqr_trqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t 
     }
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
     if (J + 1 < nblk) {
-      if ((rc = sample_update(w.Bf, ell, ell, Rg + i0 + i0 * ldr, ldr, nt - bb, b, Bn, ell, st, s))) return rc;
+      if ((rc = sample_update(w.Bf, ell, ell, Rg + i0 + i0 * ldr, ldr, nt - bb, bb, Bn, ell, st, w.Gm, s))) return rc;
       std::swap(Bc, Bn);
     }
   }

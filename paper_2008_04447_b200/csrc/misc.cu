@@ -149,81 +149,70 @@ __global__ void apply_moves_kernel(double* X, int64_t ld, int64_t rows, int64_t 
 }
 
 // ------------------------------------------------------------ sample update
-// CTA = 32 trailing columns; 8 threads per column.  Phase 1 solves
-// X = R11^{-1} R12 by row-oriented back substitution (sketch.py:122-129);
-// phase 2 forms S12 - S11 X (sketch.py:147) and copies S22.
-constexpr int kSuCols = 32;
-constexpr int kSuThreads = 256;
+// B_next = [S12 - S11 R11^{-1} R12 ; S22]  (sketch.py:132-149).
+// su_prep (one CTA): the R11 diagonal guard (randomized.py:133-135) and
+// M = S11 R11^{-1} by forward substitution, M R11 = S11 (column c of M from
+// columns < c; M is upper triangular like S11).  The nt-column part is then
+// one DMMA GEMM, B_top = S12 - M R12, plus a copy of S22.
+constexpr int kSuThreads = 128;
 __global__ void __launch_bounds__(kSuThreads, 1)
-    sample_update_kernel(const double* Bf, int64_t ldbf, int ell, const double* R, int64_t ldr,
-                         int nt, double* Bn, int64_t ldbn, sqr_status* st) {
-  extern __shared__ __align__(16) double sm[];
+    su_prep_kernel(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, double* Mout, int64_t ldm,
+                   sqr_status* st) {
+  extern __shared__ __align__(16) double X[];  // M in the upper triangle, R11 (transposed) in the lower
+  __shared__ double rdiag[144];
+  __shared__ int ok;
   if (st->stop) return;
   const int bh = st->sample_achieved;
-  const int ldt = bh | 1;
-  double* Tm = sm;                        // bh x bh (R11, then S11), pitch ldt
-  double* Xs = sm + (size_t)bh * ldt;     // bh x kSuCols, pitch bh+1
-  const int ldx = bh + 1;
   const int tid = threadIdx.x;
-  // _diag_ok (randomized.py:133-135): every CTA checks redundantly.
-  {
-    __shared__ int ok;
-    if (tid == 0) {
-      const double d0 = fabs(R[0]);
-      double dmin = d0;
-      for (int i = 1; i < bh; ++i) dmin = fmin(dmin, fabs(R[(int64_t)i * ldr + i]));
-      ok = (bh > 0) && (dmin > 0x1p-52 * d0);
-    }
-    __syncthreads();
+  const int P = bh | 1;
+  if (tid == 0) {
+    const double d0 = fabs(R[0]);
+    double dmin = d0;
+    for (int i = 1; i < bh; ++i) dmin = fmin(dmin, fabs(R[(int64_t)i * ldr + i]));
+    ok = (bh > 0) && (dmin > 0x1p-52 * d0);
     if (!ok) {
-      if (blockIdx.x == 0 && tid == 0) {
-        st->stop = 1;
-        st->reason = SQR_STOP_R11_SINGULAR;
-      }
-      return;
+      st->stop = 1;
+      st->reason = SQR_STOP_R11_SINGULAR;
     }
   }
-  const int c0 = blockIdx.x * kSuCols;
-  const int nc = min(kSuCols, nt - c0);
-  if (nc <= 0) return;
   for (int e = tid; e < bh * bh; e += kSuThreads) {
-    const int i = e % bh, j = e / bh;
-    Tm[j * ldt + i] = (i <= j) ? R[(int64_t)j * ldr + i] : 0.0;
-  }
-  for (int e = tid; e < bh * nc; e += kSuThreads) {
-    const int i = e % bh, c = e / bh;
-    Xs[c * ldx + i] = R[(int64_t)(bh + c0 + c) * ldr + i];  // R12
+    const int r = e % bh, c = e / bh;
+    if (r <= c) X[c * P + r] = Bf[(int64_t)c * ldbf + r];          // S11(r, c)
+    if (r < c) X[r * P + c] = R[(int64_t)c * ldr + r];             // R11(r, c) at (c, r)
+    if (r == c) rdiag[r] = R[(int64_t)c * ldr + r];
   }
   __syncthreads();
-  const int col = tid >> 3, q = tid & 7;
-  // Back substitution, 8 lanes per column, fixed shuffle tree.
-  for (int i = bh - 1; i >= 0; --i) {
-    double s = 0.0;
-    if (col < nc)
-      for (int l = i + 1 + q; l < bh; l += 8) s = fma(Tm[l * ldt + i], Xs[col * ldx + l], s);
-    s += __shfl_xor_sync(0xffffffffu, s, 4);
-    s += __shfl_xor_sync(0xffffffffu, s, 2);
-    s += __shfl_xor_sync(0xffffffffu, s, 1);
-    if (col < nc && q == 0) Xs[col * ldx + i] = (Xs[col * ldx + i] - s) / Tm[i * ldt + i];
-    __syncwarp();
+  if (!ok) return;
+  // thread i owns row i of M: M(i, c) = (S11(i, c) - sum_{l=i}^{c-1} M(i, l) R11(l, c)) / R11(c, c)
+  for (int i = tid; i < bh; i += kSuThreads) {
+    for (int c = i; c < bh; ++c) {
+      double s0 = 0.0, s1 = 0.0;
+      int l = i;
+      for (; l + 2 <= c; l += 2) {
+        s0 = fma(X[l * P + i], X[l * P + c], s0);
+        s1 = fma(X[(l + 1) * P + i], X[(l + 1) * P + c], s1);
+      }
+      if (l < c) s0 = fma(X[l * P + i], X[l * P + c], s0);
+      X[c * P + i] = (X[c * P + i] - (s0 + s1)) / rdiag[c];
+    }
   }
   __syncthreads();
-  // S11 replaces R11.
   for (int e = tid; e < bh * bh; e += kSuThreads) {
-    const int i = e % bh, j = e / bh;
-    Tm[j * ldt + i] = (i <= j) ? Bf[(int64_t)j * ldbf + i] : 0.0;
+    const int r = e % bh, c = e / bh;
+    Mout[(int64_t)c * ldm + r] = r <= c ? X[c * P + r] : 0.0;
   }
-  __syncthreads();
-  // top = S12 - S11 X
-  for (int e = tid; e < bh * nc; e += kSuThreads) {
-    const int i = e % bh, c = e / bh;
-    double s = 0.0;
-    for (int l = i; l < bh; ++l) s = fma(Tm[l * ldt + i], Xs[c * ldx + l], s);
-    Bn[(int64_t)(c0 + c) * ldbn + i] = Bf[(int64_t)(bh + c0 + c) * ldbf + i] - s;
-  }
-  for (int e = tid; e < (ell - bh) * nc; e += kSuThreads) {
-    const int i = bh + e % (ell - bh), c = e / (ell - bh);
-    Bn[(int64_t)(c0 + c) * ldbn + i] = Bf[(int64_t)(bh + c0 + c) * ldbf + i];
+}
+
+// Rows [rows0, ell) of the sample: B_next(r, c) = Bf(r, bh + c).
+__global__ void copy_s22_kernel(const double* Bf, int64_t ldbf, int ell, int nt, double* Bn, int64_t ldbn,
+                                const sqr_status* st) {
+  if (st->stop) return;
+  const int bh = st->sample_achieved;
+  const int rows = ell - bh;
+  const int64_t total = (int64_t)rows * nt;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = bh + (int)(e % rows), c = (int)(e / rows);
+    Bn[(int64_t)c * ldbn + r] = Bf[(int64_t)(bh + c) * ldbf + r];
   }
 }
 
@@ -292,19 +281,30 @@ int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm
 }
 
 int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
-                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, cudaStream_t s) {
+                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s) {
   if (nt <= 0) return SQR_OK;
-  const int64_t smem = ((bmax | 1) * bmax + (bmax + 1) * kSuCols) * 8;
+  const int64_t smem = (bmax | 1) * bmax * 8;
   static int64_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
-    SQR_CUDA(cudaFuncSetAttribute(sample_update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
+    SQR_CUDA(cudaFuncSetAttribute(su_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  ProfScope ps(kTagSampleUpd, s);
-  sample_update_kernel<<<(unsigned)cdiv(nt, kSuCols), kSuThreads, smem, s>>>(Bf, ldbf, (int)ell, R, ldr,
-                                                                           (int)nt, Bn, ldbn, st);
-  SQR_LAUNCH("sample_update_kernel");
+  {
+    ProfScope ps(kTagSampleUpd, s);
+    su_prep_kernel<<<1, kSuThreads, smem, s>>>(Bf, ldbf, R, ldr, mbuf, bmax, st);
+    SQR_LAUNCH("su_prep_kernel");
+  }
+  // B_top = S12 - M R12 with the block size read on the device (== bmax
+  // whenever the loop continues: a short block stops the factorization).
+  int rc = gemm_nn(bmax, nt, bmax, -1.0, mbuf, bmax, R + bmax * ldr, ldr, 1.0, Bf + bmax * ldbf, ldbf, Bn, ldbn, s,
+                   GemmDyn{&st->stop, nullptr, 0});
+  if (rc) return rc;
+  if (ell > bmax) {
+    ProfScope ps(kTagSampleUpd, s);
+    const int blocks = (int)std::min<int64_t>(cdiv((ell - bmax) * nt, 256), (int64_t)sm_count() * 4);
+    copy_s22_kernel<<<std::max(blocks, 1), 256, 0, s>>>(Bf, ldbf, (int)ell, (int)nt, Bn, ldbn, st);
+    SQR_LAUNCH("copy_s22_kernel");
+  }
   return SQR_OK;
 }
 
@@ -352,7 +352,18 @@ extern "C" int sqr_apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0
 
 extern "C" int sqr_sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr,
                                  int64_t nt, double* Bnext, int64_t ldbn, sqr_status* st, void* stream) {
-  return sqr::sample_update(Bf, ldbf, ell, R, ldr, nt, ell, Bnext, ldbn, st, static_cast<cudaStream_t>(stream));
+  // stand-alone entry: the block size is the sample QRCP's (st->sample_achieved)
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  sqr_status hs;
+  if (cudaMemcpyAsync(&hs, st, sizeof(hs), cudaMemcpyDeviceToHost, s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return sqr::check_cuda(cudaGetLastError(), "sqr_sample_update");
+  const int64_t bh = hs.sample_achieved;
+  double* mbuf = nullptr;
+  if (cudaMallocAsync(reinterpret_cast<void**>(&mbuf), std::max<int64_t>(bh * bh, 1) * 8, s) != cudaSuccess)
+    return sqr::check_cuda(cudaGetLastError(), "cudaMallocAsync");
+  int rc = sqr::sample_update(Bf, ldbf, ell, R, ldr, nt, bh, Bnext, ldbn, st, mbuf, s);
+  cudaFreeAsync(mbuf, s);
+  return rc;
 }
 
 extern "C" int64_t sqr_launch_count(void) { return sqr::g_launches.load(); }
