@@ -171,6 +171,21 @@ int sqr_apply_wy(const double* Y, int64_t ldy, const double* T, int64_t ldt, int
                  double* C, int64_t ldc, int64_t ncols, int transpose, double* workspace,
                  int64_t workspace_bytes, void* stream);
 
+/* --------------------------------------------- multi-GPU building blocks
+ * Used by the column block-cyclic driver (paper_2008_04447_b200/distributed.py)
+ * where each rank owns a subset of the columns. */
+int64_t sqr_block_workspace(int64_t m, int64_t ncols, int64_t b);
+/* dst[:, dst_idx[j]] = src[:, src_idx[j]], j < n, rows [0, rows); NULL index = identity. */
+int sqr_copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* src_idx, double* dst,
+                     int64_t ldd, const int64_t* dst_idx, int64_t n, void* stream);
+/* Panel QR of an mr x w panel (w <= 128), leaves + compact-WY updates; st->bhat/stop. */
+int sqr_panel_factor(double* P, int64_t ldp, int64_t mr, int64_t w, double* Y, int64_t ldy, double* taus,
+                     int stop_at_zero, sqr_status* st, void* workspace, int64_t workspace_bytes, void* stream);
+/* T from (Y, taus), then C := Q^T C for ncols local columns (randomized.py:203-207). */
+int sqr_apply_block_update(double* C, int64_t ldc, int64_t mr, int64_t ncols, int64_t bb, const double* Y,
+                           int64_t ldy, const double* taus, double* T, int64_t ldt, void* workspace,
+                           int64_t workspace_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -52,6 +52,12 @@ SIGNATURES = {
     "sqr_qr_blocked": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
     "sqr_apply_wy": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_i64, c_int, c_ptr, c_i64,
                              c_ptr]),
+    "sqr_block_workspace": (c_i64, [c_i64, c_i64, c_i64]),
+    "sqr_copy_columns": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
+    "sqr_panel_factor": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_int, c_ptr, c_ptr, c_i64,
+                                 c_ptr]),
+    "sqr_apply_block_update": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr,
+                                       c_i64, c_ptr]),
 }
 
 # struct sqr_status (include/sqr.h)

@@ -456,3 +456,86 @@ extern "C" int sqr_panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, doubl
   cudaFreeAsync(ws, s);
   return rc;
 }
+
+// ------------------------------------------------------- multi-GPU building blocks
+// Workspace for sqr_panel_factor / sqr_apply_block_update.
+extern "C" int64_t sqr_block_workspace(int64_t m, int64_t ncols, int64_t b) {
+  Carve c(nullptr);
+  c.take<double>(kGemmWsBytes / 8);
+  c.take<char>(panel_workspace(std::min<int64_t>(b, 128)));
+  c.take<double>(PanelScratch::doubles(b));
+  c.take<double>(b * (ncols + b));
+  c.take<double>(b * std::max<int64_t>(ncols, 1));
+  c.take<sqr_status>(1);
+  return c.off + 256;
+}
+
+namespace {
+struct BlockWs {
+  double *gws, *pscr, *GWt, *W;
+  void* pws;
+  int64_t pwsb;
+  sqr_status* st;
+};
+BlockWs carve_block(void* ws, int64_t ncols, int64_t b) {
+  Carve c(ws);
+  BlockWs w;
+  w.gws = c.take<double>(kGemmWsBytes / 8);
+  w.pwsb = panel_workspace(std::min<int64_t>(b, 128));
+  w.pws = c.take<char>(w.pwsb);
+  w.pscr = c.take<double>(PanelScratch::doubles(b));
+  w.GWt = c.take<double>(b * (ncols + b));
+  w.W = c.take<double>(b * std::max<int64_t>(ncols, 1));
+  w.st = c.take<sqr_status>(1);
+  return w;
+}
+}  // namespace
+
+// Panel of width w (<= b) at P (mr rows) with the leaf kernel + WY updates;
+// st receives bhat / stop (stop_at_zero semantics of randomized.py:120-121).
+extern "C" int sqr_panel_factor(double* P, int64_t ldp, int64_t mr, int64_t w, double* Y, int64_t ldy,
+                                double* taus, int stop_at_zero, sqr_status* st, void* workspace,
+                                int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (w <= 0 || w > 128 || mr <= 0) {
+    set_error("sqr_panel_factor: need 1 <= w <= 128");
+    return SQR_EINVAL;
+  }
+  if (workspace_bytes < sqr_block_workspace(mr, 0, w)) {
+    set_error("sqr_panel_factor: workspace too small");
+    return SQR_EINVAL;
+  }
+  BlockWs bw = carve_block(workspace, 0, w);
+  PanelScratch sc{bw.pscr, bw.pscr + kLeaf * (kLeaf + w), bw.pscr + kLeaf * (kLeaf + w) + kLeaf * w};
+  return panel_factor(P, ldp, mr, w, w, Y, ldy, taus, stop_at_zero, st, bw.pws, bw.pwsb, sc, bw.gws, s);
+}
+
+// One block reflection of ncols columns C (mr rows): T from Y and taus
+// (written to T, ld ldt), then C := (I - Y T Y^T)^T C  (randomized.py:203-207).
+extern "C" int sqr_apply_block_update(double* C, int64_t ldc, int64_t mr, int64_t ncols, int64_t bb,
+                                      const double* Y, int64_t ldy, const double* taus, double* T, int64_t ldt,
+                                      void* workspace, int64_t workspace_bytes, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (bb <= 0 || bb > 128 || mr <= 0) {
+    set_error("sqr_apply_block_update: need 1 <= bb <= 128");
+    return SQR_EINVAL;
+  }
+  if (workspace_bytes < sqr_block_workspace(mr, ncols, bb)) {
+    set_error("sqr_apply_block_update: workspace too small");
+    return SQR_EINVAL;
+  }
+  BlockWs bw = carve_block(workspace, ncols, bb);
+  SQR_CUDA(cudaMemsetAsync(bw.st, 0, sizeof(sqr_status), s));
+  GemmDyn d1{nullptr, nullptr, 0};
+  d1.pre = Y;
+  d1.ldpre = ldy;
+  d1.npre = (int)bb;
+  int rc = gemm_tn(bb, bb + ncols, mr, 1.0, Y, ldy, C, ldc, 0.0, nullptr, 0, bw.GWt, bb, bw.gws, kGemmWsBytes, s, d1);
+  if (rc) return rc;
+  if ((rc = build_t(bw.GWt, bb, taus, bb, T, ldt, nullptr, s))) return rc;
+  if (ncols <= 0) return SQR_OK;
+  rc = gemm_tn(bb, ncols, bb, -1.0, T, ldt, bw.GWt + bb * bb, bb, 0.0, nullptr, 0, bw.W, bb, bw.gws, kGemmWsBytes, s,
+               GemmDyn{});
+  if (rc) return rc;
+  return gemm_nn(mr, ncols, bb, 1.0, Y, ldy, bw.W, bb, 1.0, C, ldc, C, ldc, s, GemmDyn{});
+}

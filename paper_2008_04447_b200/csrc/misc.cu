@@ -246,6 +246,20 @@ __global__ void copy_upper_kernel(const double* src, int64_t lds, double* dst, i
   }
 }
 
+// dst[:, dst_idx[j]] = src[:, src_idx[j]] for j < n (rows [0, rows)); NULL
+// index arrays mean the identity.  Used by the multi-GPU driver to pack /
+// unpack moved columns and to assemble block-cyclic slabs.
+__global__ void copy_columns_kernel(const double* src, int64_t lds, int64_t rows, const int64_t* sidx, double* dst,
+                                    int64_t ldd, const int64_t* didx, int64_t n) {
+  for (int64_t j = blockIdx.y; j < n; j += gridDim.y) {
+    const int64_t cs = sidx ? sidx[j] : j, cd = didx ? didx[j] : j;
+    const double* s = src + cs * lds;
+    double* d = dst + cd * ldd;
+    for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+      d[r] = s[r];
+  }
+}
+
 __global__ void iota_kernel(int64_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = i;
@@ -322,6 +336,16 @@ int copy_upper(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t
   copy_upper_kernel<<<(unsigned)std::min<int64_t>(cdiv(n * n, 256), 256), 256, 0, s>>>(src, lds, dst, ldd, (int)n,
                                                                                      gate);
   SQR_LAUNCH("copy_upper_kernel");
+  return SQR_OK;
+}
+
+int copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* sidx, double* dst, int64_t ldd,
+                 const int64_t* didx, int64_t n, cudaStream_t s) {
+  if (rows <= 0 || n <= 0) return SQR_OK;
+  ProfScope ps(kTagMisc, s);
+  dim3 grid((unsigned)std::min<int64_t>(cdiv(rows, 256), 64), (unsigned)std::min<int64_t>(n, 4096));
+  copy_columns_kernel<<<grid, 256, 0, s>>>(src, lds, rows, sidx, dst, ldd, didx, n);
+  SQR_LAUNCH("copy_columns_kernel");
   return SQR_OK;
 }
 
@@ -411,4 +435,9 @@ extern "C" int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, i
 extern "C" int sqr_debug_trace(void* device_buffer) {
   sqr::g_trace_host_ptr = static_cast<unsigned long long*>(device_buffer);
   return SQR_OK;
+}
+
+extern "C" int sqr_copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* src_idx, double* dst,
+                                int64_t ldd, const int64_t* dst_idx, int64_t n, void* stream) {
+  return sqr::copy_columns(src, lds, rows, src_idx, dst, ldd, dst_idx, n, static_cast<cudaStream_t>(stream));
 }

@@ -1,0 +1,484 @@
+"""Multi-GPU RQRCP: 1-D column block-cyclic layout, one process per GPU
+(north star: "column-partitioned block-cyclically across the
+GPUs ... the replicated pivot decision on the small B is followed by an
+NCCL-over-NVLink broadcast of the panel's Householder vectors and T, and each
+GPU applies the trailing update to its own columns").
+
+Global column block c (columns [c*b, (c+1)*b)) lives on rank c % P.  Per block
+J of the reference loop (randomized.py:185-221):
+
+  1. sample QRCP, replicated: every rank holds the identical sample B and runs
+     the identical deterministic kernel, so pivots agree without messages;
+  2. column moves: the <= 2b moved columns travel point to point (NCCL);
+  3. panel: the owner of block J factors its local panel;
+  4. broadcast of Y (m - i0 rows), taus, bhat and R11 from the owner;
+  5. every rank applies the block reflection to its own trailing columns;
+  6. every rank updates the sample for its own columns (sketch.py:132-149)
+     and the slabs are all-gathered back into the replicated B.
+
+The orchestration is written against two small interfaces -- ``comm``
+(broadcast / all_gather / point-to-point, torch.distributed) and ``ops`` (the
+local compute) -- so the same code runs on B200s (``GpuOps``: libsqr kernels,
+NCCL) and, in the CPU test-suite, on gloo with a NumPy reference backend.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .counters import rqrcp_counters
+
+_DIAG_FLOOR = 2.0 ** -52
+
+
+# ------------------------------------------------------------------ layout
+@dataclass(frozen=True)
+class BlockCyclic:
+    """Column block-cyclic map with block width b over P ranks."""
+
+    n: int
+    b: int
+    P: int
+
+    @property
+    def nblocks(self) -> int:
+        return -(-self.n // self.b)
+
+    def owner(self, p):
+        return (np.asarray(p) // self.b) % self.P
+
+    def local_index(self, p):
+        p = np.asarray(p)
+        c = p // self.b
+        return (c // self.P) * self.b + p % self.b
+
+    def blocks_of(self, r: int):
+        return list(range(r, self.nblocks, self.P))
+
+    def n_local(self, r: int) -> int:
+        return sum(min(self.b, self.n - c * self.b) for c in self.blocks_of(r))
+
+    def global_of_local(self, r: int) -> np.ndarray:
+        """Global position of every local column of rank r, in local order."""
+        out = []
+        for c in self.blocks_of(r):
+            out.extend(range(c * self.b, min(self.n, (c + 1) * self.b)))
+        return np.asarray(out, dtype=np.int64)
+
+    def first_local_at_or_after(self, r: int, p: int) -> int:
+        """Local index of the first local column whose global position >= p."""
+        g = self.global_of_local(r)
+        return int(np.searchsorted(g, p))
+
+
+# -------------------------------------------------------------------- comm
+class TorchComm:
+    """torch.distributed with the process group's backend (NCCL on GPUs, gloo
+    on CPU)."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+
+    def broadcast(self, t: torch.Tensor, src: int) -> torch.Tensor:
+        dist.broadcast(t, src=dist.get_global_rank(self.group, src) if self.group else src, group=self.group)
+        return t
+
+    def all_gather(self, t: torch.Tensor) -> list:
+        outs = [torch.empty_like(t) for _ in range(self.size)]
+        dist.all_gather(outs, t.contiguous(), group=self.group)
+        return outs
+
+    def exchange(self, sends: dict, recv_shapes: dict, like: torch.Tensor) -> dict:
+        """Point-to-point: sends {peer: tensor}, receives {peer: tensor(shape)}."""
+        ops, recvs = [], {}
+        for peer, shape in sorted(recv_shapes.items()):
+            buf = torch.empty(shape, dtype=like.dtype, device=like.device)
+            recvs[peer] = buf
+            ops.append(dist.P2POp(dist.irecv, buf, peer, group=self.group))
+        for peer, t in sorted(sends.items()):
+            ops.append(dist.P2POp(dist.isend, t.contiguous(), peer, group=self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+        return recvs
+
+    def max(self, x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cuda" if dist.get_backend(self.group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self.group)
+        return float(t.item())
+
+
+# ---------------------------------------------------------------- the loop
+@dataclass
+class DistResult:
+    achieved: int
+    nblocks: int
+    reason: str
+    perm: np.ndarray
+    A_local: object          # this rank's columns: R rows / reflector tails packed (LAPACK style)
+    taus: np.ndarray
+    counters: object
+
+
+def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: int, comm, ops,
+                       omega=None) -> DistResult:
+    """Distributed RQRCP (randomized.py:166-224) over ``comm``; ``A_local`` is
+    this rank's block-cyclic column slab (ops-specific storage, m rows)."""
+    ell = b + p
+    lay = BlockCyclic(n, b, comm.size)
+    r = comm.rank
+    gloc = lay.global_of_local(r)
+    perm = np.arange(n, dtype=np.int64)
+    taus = np.zeros(max(k, 1))
+    # 1. sketch: local slab, all-gathered into global column order.
+    B = ops.assemble(comm.all_gather(ops.pad_slab(ops.sketch(A_local, m, ell, seed, omega, gloc), lay, 0)),
+                     lay, ell)
+    achieved, nblocks, reason = 0, 0, "k_reached"
+    first = True
+    while achieved < k:
+        i0 = achieved
+        bb = min(b, k - i0)
+        nt = n - i0
+        # ---- replicated sample QRCP (identical input -> identical pivots)
+        samp = ops.sample_qrcp(B, ell, nt, bb, first)
+        first = False
+        if samp.stop:
+            reason = samp.reason
+            break
+        # ---- column moves (positions relative to i0)
+        moves = samp.moves
+        if len(moves):
+            ps = i0 + moves[:, 1]
+            pd = i0 + moves[:, 0]
+            ops.move_columns(A_local, ps, pd, lay, comm)
+            perm[pd] = perm[ps].copy()
+        # ---- panel on the owner, broadcast of (Y, taus, bhat, R11)
+        J = i0 // b
+        owner = J % comm.size
+        lc = int(lay.local_index(i0)) if owner == r else -1
+        pan = ops.panel(A_local, lc, i0, m, samp.achieved, bb, owner == r)
+        pan = ops.broadcast_panel(pan, owner, comm, m - i0, bb)
+        bhat = pan.bhat
+        if bhat == 0:
+            reason = "panel_zero"
+            break
+        taus[i0:i0 + bb] = pan.taus_host[:bb]
+        # ---- trailing update of my columns at global positions >= i0 + bhat
+        t0 = lay.first_local_at_or_after(r, i0 + bhat)
+        ops.block_update(A_local, t0, i0, m, pan)
+        nblocks += 1
+        achieved = i0 + bhat
+        ncols = n - achieved
+        if bhat < bb:
+            reason = "short_block"
+            break
+        if achieved >= k:
+            reason = "k_reached"
+            break
+        if ncols == 0:
+            reason = "no_trailing"
+            break
+        d = np.abs(np.diag(pan.R11_host))
+        if not (d.size > 0 and d.min() > _DIAG_FLOOR * d[0]):
+            reason = "r11_singular"
+            break
+        # ---- sample update for my columns, all-gathered (sketch.py:132-149)
+        s0 = lay.first_local_at_or_after(r, achieved)
+        mine = gloc[s0:]
+        Bn_loc = ops.sample_update_local(samp, A_local, s0, mine - i0, i0, bb, pan)
+        B = ops.assemble_next(comm.all_gather(ops.pad_slab(Bn_loc, lay, achieved)), lay, achieved, ell)
+    counters = rqrcp_counters(m, n, b, ell, achieved, nblocks,
+                              {"k_reached": 1, "short_block": 5, "no_trailing": 6}.get(reason, 0), False)
+    return DistResult(achieved, nblocks, reason, perm, A_local, taus[:achieved], counters)
+
+
+# ------------------------------------------------------------ GPU backend
+@dataclass
+class _Sample:
+    stop: bool
+    reason: str
+    achieved: int
+    moves: np.ndarray
+    Bf: object
+    st: object
+
+
+@dataclass
+class _Panel:
+    bhat: int
+    Y: object            # (bb, mr) column-major explicit unit-lower Y
+    taus: object         # device (bb,)
+    taus_host: np.ndarray
+    R11: object          # (bb, bb) device
+    R11_host: np.ndarray
+    st: object
+
+
+class GpuOps:
+    """libsqr kernels on torch CUDA tensors; matrices are (ncols, ld) tensors."""
+
+    def __init__(self, device):
+        from . import _lib
+        from ._dev import Workspace
+        self.L = _lib.lib()
+        self.lib = _lib
+        self.dev = torch.device(device)
+        self.Workspace = Workspace
+        self._keep = []
+
+    # helpers
+    def _s(self):
+        return torch.cuda.current_stream(self.dev).cuda_stream
+
+    def _ws(self, nbytes):
+        return self.Workspace.get(nbytes, self.dev)
+
+    def _chk(self, rc, what):
+        self.lib.check(rc, what)
+
+    def _idx(self, a):
+        # Index arrays must outlive the asynchronous launch that reads them: a
+        # temporary freed inside an argument list could be handed to the next
+        # allocation of the same call.  Keep them until the next sync point.
+        t = torch.as_tensor(np.asarray(a, dtype=np.int64), device=self.dev)
+        self._keep.append(t)
+        if len(self._keep) > 64:
+            self._keep = self._keep[-64:]
+        return t
+
+    # 1. sketch of the local slab
+    def sketch(self, A, m, ell, seed, omega, gloc):
+        OmT = torch.empty((ell, m), dtype=torch.float64, device=self.dev)  # Omega^T: m x ell column-major
+        if omega is None:
+            self._chk(self.L.sqr_gaussian(OmT.data_ptr(), m, ell, m, seed & ((1 << 64) - 1), 0, 1, self._s()),
+                      "sqr_gaussian")
+        else:
+            OmT.copy_(torch.as_tensor(np.ascontiguousarray(np.asarray(omega, dtype=np.float64)), device=self.dev))
+        nl = A.shape[0]
+        Bl = torch.empty((max(nl, 1), ell), dtype=torch.float64, device=self.dev)
+        if nl:
+            ws = self._ws(200 << 20)
+            self._chk(self.L.sqr_gemm_tn(ell, nl, m, 1.0, OmT.data_ptr(), m, A.data_ptr(), A.shape[1], 0.0, None, 0,
+                                         Bl.data_ptr(), ell, ws.data_ptr(), ws.numel(), self._s()), "sketch")
+        return Bl
+
+    def _assemble(self, parts, lay, ell, p0):
+        """Columns of the all-gathered slabs (each padded to n_local_max) into
+        global order for positions >= p0."""
+        n = lay.n
+        out = torch.empty((max(n - p0, 1), ell), dtype=torch.float64, device=self.dev)
+        for q, part in enumerate(parts):
+            g = lay.global_of_local(q)
+            g = g[g >= p0]
+            if g.size:
+                self._chk(self.L.sqr_copy_columns(part.data_ptr(), ell, ell, None, out.data_ptr(), ell,
+                                                  self._idx(g - p0).data_ptr(), g.size, self._s()), "assemble")
+        return out
+
+    def assemble(self, parts, lay, ell):
+        return self._assemble(parts, lay, ell, 0)
+
+    def pad_slab(self, Bn, lay, achieved):
+        nmax = max(lay.n_local(q) for q in range(lay.P))
+        out = torch.zeros((nmax, Bn.shape[1]), dtype=torch.float64, device=self.dev)
+        nb = min(Bn.shape[0], nmax)
+        if nb:
+            out[:nb].copy_(Bn[:nb])
+        return out
+
+    def assemble_next(self, parts, lay, achieved, ell):
+        return self._assemble(parts, lay, ell, achieved)
+
+    # 2. replicated sample QRCP
+    def sample_qrcp(self, B, ell, nt, bb, first):
+        from ._dev import status_new, status_read
+        Bf = torch.empty((max(nt, 1), ell), dtype=torch.float64, device=self.dev)
+        lperm = torch.empty(max(nt, 1), dtype=torch.int64, device=self.dev)
+        moves = torch.empty(4 * bb + 8, dtype=torch.int32, device=self.dev)
+        taus = torch.zeros(max(bb, 1), dtype=torch.float64, device=self.dev)
+        st = status_new(self.dev)
+        if not first:  # the sample floor of the first block (randomized.py:179-180)
+            st[32:40].view(torch.float64).fill_(self._floor)
+        self._chk(self.L.sqr_sample_qrcp(B.data_ptr(), ell, ell, nt, bb, Bf.data_ptr(), ell, lperm.data_ptr(),
+                                         moves.data_ptr(), taus.data_ptr(), 1 if first else 0, st.data_ptr(),
+                                         self._s()), "sample_qrcp")
+        s = status_read(st)
+        if first:
+            self._floor = float(s["floor_sq"])
+        stop = bool(s["stop"])
+        reason = {2: "sample_floor", 3: "sample_rank"}.get(int(s["reason"]), "none")
+        nm = int(s["nmoves"])
+        mv = moves[:2 * nm].view(nm, 2).cpu().numpy().astype(np.int64)
+        return _Sample(stop, reason, int(s["sample_achieved"]), mv, Bf, st)
+
+    # 3. point-to-point column moves
+    def move_columns(self, A, ps, pd, lay, comm):
+        r = comm.rank
+        ld = A.shape[1]
+        osrc, odst = lay.owner(ps), lay.owner(pd)
+        lsrc, ldst = lay.local_index(ps), lay.local_index(pd)
+        sends, recv_shapes = {}, {}
+        # pack every outgoing / locally moved source first (reads before writes)
+        mine = np.nonzero(osrc == r)[0]
+        packed = None
+        if mine.size:
+            packed = torch.empty((mine.size, ld), dtype=torch.float64, device=self.dev)
+            self._chk(self.L.sqr_copy_columns(A.data_ptr(), ld, ld, self._idx(lsrc[mine]).data_ptr(),
+                                              packed.data_ptr(), ld, None, mine.size, self._s()), "pack")
+            for q in set(odst[mine].tolist()) - {r}:
+                sel = np.nonzero(odst[mine] == q)[0]
+                sends[q] = packed[self._idx(sel)]
+        for q in set(osrc[odst == r].tolist()) - {r}:
+            recv_shapes[q] = (int(np.count_nonzero((odst == r) & (osrc == q))), ld)
+        recvs = comm.exchange(sends, recv_shapes, A)
+        # unpack: local moves then received columns, in move order per source
+        if mine.size:
+            loc = np.nonzero(odst[mine] == r)[0]
+            if loc.size:
+                self._chk(self.L.sqr_copy_columns(packed.data_ptr(), ld, ld, self._idx(loc).data_ptr(), A.data_ptr(),
+                                                  ld, self._idx(ldst[mine[loc]]).data_ptr(), loc.size, self._s()),
+                          "unpack")
+        for q, buf in recvs.items():
+            idx = np.nonzero((odst == r) & (osrc == q))[0]
+            self._chk(self.L.sqr_copy_columns(buf.data_ptr(), ld, ld, None, A.data_ptr(), ld,
+                                              self._idx(ldst[idx]).data_ptr(), idx.size, self._s()), "unpack")
+
+    # 4. panel on the owner + broadcast
+    def panel(self, A, lc, i0, m, w, bb, is_owner):
+        from ._dev import status_new
+        mr = m - i0
+        Y = torch.zeros((bb, mr), dtype=torch.float64, device=self.dev)
+        taus = torch.zeros(bb, dtype=torch.float64, device=self.dev)
+        R11 = torch.zeros((bb, bb), dtype=torch.float64, device=self.dev)
+        st = status_new(self.dev)
+        if is_owner:
+            ld = A.shape[1]
+            Pp = A.data_ptr() + 8 * (lc * ld + i0)
+            ws = self._ws(self.L.sqr_block_workspace(mr, 0, bb))
+            self._chk(self.L.sqr_panel_factor(Pp, ld, mr, w, Y.data_ptr(), mr, taus.data_ptr(), 1, st.data_ptr(),
+                                              ws.data_ptr(), ws.numel(), self._s()), "panel")
+            R11.copy_(A[lc:lc + bb, i0:i0 + bb])
+        return _Panel(0, Y, taus, None, R11, None, st)
+
+    def broadcast_panel(self, pan, owner, comm, mr, bb):
+        meta = pan.st[:24].view(torch.int32)  # stop, reason, achieved, nblocks, sample_achieved, bhat
+        comm.broadcast(meta, owner)
+        comm.broadcast(pan.Y, owner)
+        comm.broadcast(pan.taus, owner)
+        comm.broadcast(pan.R11, owner)
+        mh = meta.cpu().numpy()
+        pan.bhat = 0 if mh[0] else int(mh[5])
+        pan.taus_host = pan.taus.cpu().numpy()
+        R = pan.R11.cpu().numpy().T[:pan.bhat, :pan.bhat]  # (bb, bb) storage is column-major
+        pan.R11_host = np.triu(R)
+        return pan
+
+    # 5. trailing update of my columns
+    def block_update(self, A, t0, i0, m, pan):
+        ld = A.shape[1]
+        ncols = A.shape[0] - t0
+        bb = pan.Y.shape[0]
+        mr = m - i0
+        T = torch.empty((bb, bb), dtype=torch.float64, device=self.dev)
+        ws = self._ws(self.L.sqr_block_workspace(mr, max(ncols, 0), bb))
+        self._chk(self.L.sqr_apply_block_update(A.data_ptr() + 8 * (t0 * ld + i0), ld, mr, max(ncols, 0), bb,
+                                                pan.Y.data_ptr(), mr, pan.taus.data_ptr(), T.data_ptr(), bb,
+                                                ws.data_ptr(), ws.numel(), self._s()), "block_update")
+        pan.T = T
+
+    # 6. sample update of my columns
+    def sample_update_local(self, samp, A, s0, rel, i0, bb, pan):
+        ell = samp.Bf.shape[1]
+        nloc = len(rel)
+        Bn = torch.empty((max(nloc, 1), ell), dtype=torch.float64, device=self.dev)
+        if nloc == 0:
+            return Bn[:0]
+        # Bf_loc = [S11 | Bf[:, rel]] and R_loc = [R11 | R12 of my columns]
+        Bfl = torch.empty((bb + nloc, ell), dtype=torch.float64, device=self.dev)
+        Bfl[:bb].copy_(samp.Bf[:bb])
+        self._chk(self.L.sqr_copy_columns(samp.Bf.data_ptr(), ell, ell, self._idx(rel).data_ptr(),
+                                          Bfl.data_ptr() + 8 * bb * ell, ell, None, nloc, self._s()), "gather S")
+        Rl = torch.empty((bb + nloc, bb), dtype=torch.float64, device=self.dev)
+        Rl[:bb].copy_(pan.R11)
+        ld = A.shape[1]
+        self._chk(self.L.sqr_copy_columns(A.data_ptr() + 8 * (s0 * ld + i0), ld, bb, None, Rl.data_ptr() + 8 * bb * bb,
+                                          bb, None, nloc, self._s()), "gather R12")
+        self._chk(self.L.sqr_sample_update(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, Bn.data_ptr(), ell,
+                                           samp.st.data_ptr(), self._s()), "sample_update")
+        return Bn[:nloc]
+
+
+# ----------------------------------------------------------------- bench
+def local_giid(m: int, n: int, b: int, seed: int, lay: BlockCyclic, r: int, device) -> torch.Tensor:
+    """This rank's columns of giid(m, n, seed) (column-major stream, rng.py:65-70)."""
+    from . import _lib
+    L = _lib.lib()
+    nl = lay.n_local(r)
+    A = torch.empty((max(nl, 1), m), dtype=torch.float64, device=device)
+    j = 0
+    for c in lay.blocks_of(r):
+        w = min(b, n - c * b)
+        L.sqr_gaussian(A.data_ptr() + 8 * j * m, m, m, w, seed, c * b * m, 0,
+                       torch.cuda.current_stream(device).cuda_stream)
+        j += w
+    return A
+
+
+def bench_main(args, metric, peak, peak_source):
+    """bench.py --gpus N under torchrun: strong scaling of C5 (n = 32768)."""
+    import json
+    import os
+    import time
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    comm = TorchComm()
+    m = n = args.n
+    b, p = args.b, args.p
+    lay = BlockCyclic(n, b, comm.size)
+    A0 = local_giid(m, n, b, 5, lay, comm.rank, dev)
+    ops = GpuOps(dev)
+    torch.cuda.synchronize()
+
+    def step():
+        A = A0.clone()
+        return rqrcp_block_cyclic(A, m, n, n, b, p, 0, comm, ops)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    e0.record()
+    for _ in range(args.steps):
+        res = step()
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = comm.max(e0.elapsed_time(e1) / args.steps)
+    gflop = (2.0 * m * n * n - 2.0 * n ** 3 / 3.0) / 1e9
+    if rank == 0:
+        line = {"metric": metric, "value": gflop / (ms / 1e3), "unit": "GFLOP/s", "n_gpus": comm.size,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": "C5: rqrcp n=32768 b=128 p=8, column block-cyclic", "m": m, "n": n,
+                           "b": b, "p": p, "parallelism": f"column-block-cyclic x{comm.size} (NCCL)",
+                           "achieved_rank": res.achieved,
+                           "l2": "inputs larger than L2; no flush needed"},
+                "roofline": {"bound": "tensor", "achieved": gflop / (ms / 1e3) / 1e3 / comm.size, "peak": peak,
+                             "unit": "TFLOP/s", "frac": gflop / (ms / 1e3) / 1e3 / comm.size / peak,
+                             "traffic": None, "peak_source": peak_source, "kernel": "whole step per GPU"},
+                "cpu_baseline": None, "e2e": None, "wall_s": time.perf_counter() - t0}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+    return 0

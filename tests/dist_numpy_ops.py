@@ -1,0 +1,135 @@
+"""NumPy backend of the distributed RQRCP orchestration, for the CPU (gloo)
+tests only.  Compute comes from the oracle (oracle/port.py); data movement and
+communication are the same as GpuOps (torch tensors + torch.distributed)."""
+import numpy as np
+import torch
+
+from oracle import port as O
+from paper_2008_04447_b200.distributed import _Panel, _Sample
+
+
+class NumpyOps:
+    def __init__(self):
+        self._floor = None
+
+    @staticmethod
+    def mat(A):  # (ncols, ld) storage -> (ld, ncols) writable NumPy view
+        return A.numpy().T
+
+    def sketch(self, A, m, ell, seed, omega, gloc):
+        Om = O.gauss_matrix(ell, m, seed) if omega is None else np.asarray(omega)
+        Bl = Om @ self.mat(A)[:m]
+        return torch.from_numpy(np.ascontiguousarray(Bl.T))
+
+    def _assemble(self, parts, lay, ell, p0):
+        out = torch.zeros((max(lay.n - p0, 1), ell), dtype=torch.float64)
+        for q, part in enumerate(parts):
+            g = lay.global_of_local(q)
+            g = g[g >= p0]
+            if g.size:
+                out[torch.as_tensor(g - p0)] = part[:g.size]
+        return out
+
+    def assemble(self, parts, lay, ell):
+        return self._assemble(parts, lay, ell, 0)
+
+    def pad_slab(self, Bn, lay, achieved):
+        nmax = max(lay.n_local(q) for q in range(lay.P))
+        out = torch.zeros((nmax, Bn.shape[1]), dtype=torch.float64)
+        nb = min(Bn.shape[0], nmax)
+        out[:nb] = Bn[:nb]
+        return out
+
+    def assemble_next(self, parts, lay, achieved, ell):
+        return self._assemble(parts, lay, ell, achieved)
+
+    def sample_qrcp(self, B, ell, nt, bb, first):
+        Bm = B[:nt].numpy().T
+        csq = np.einsum("ij,ij->j", Bm, Bm)
+        if first:
+            self._floor = O.sample_floor_sq(Bm)
+        if csq.size == 0 or csq.max() <= self._floor:
+            return _Sample(True, "sample_floor", 0, np.zeros((0, 2), np.int64), None, None)
+        st = O.sample_pivots(Bm, bb)
+        if st.achieved == 0:
+            return _Sample(True, "sample_rank", 0, np.zeros((0, 2), np.int64), None, None)
+        lp = st.local_perm
+        q = np.nonzero(lp != np.arange(nt))[0]
+        moves = np.stack([q, lp[q]], axis=1).astype(np.int64)
+        return _Sample(False, "none", st.achieved, moves, torch.from_numpy(np.ascontiguousarray(st.B.T)), st)
+
+    def move_columns(self, A, ps, pd, lay, comm):
+        r = comm.rank
+        osrc, odst = lay.owner(ps), lay.owner(pd)
+        lsrc, ldst = lay.local_index(ps), lay.local_index(pd)
+        mine = np.nonzero(osrc == r)[0]
+        packed = A[torch.as_tensor(lsrc[mine])].clone() if mine.size else None
+        sends, shapes = {}, {}
+        for q in set(odst[mine].tolist()) - {r}:
+            sends[q] = packed[torch.as_tensor(np.nonzero(odst[mine] == q)[0])]
+        for q in set(osrc[odst == r].tolist()) - {r}:
+            shapes[q] = (int(np.count_nonzero((odst == r) & (osrc == q))), A.shape[1])
+        recvs = comm.exchange(sends, shapes, A)
+        if mine.size:
+            loc = np.nonzero(odst[mine] == r)[0]
+            if loc.size:
+                A[torch.as_tensor(ldst[mine[loc]])] = packed[torch.as_tensor(loc)]
+        for q, buf in recvs.items():
+            idx = np.nonzero((odst == r) & (osrc == q))[0]
+            A[torch.as_tensor(ldst[idx])] = buf
+
+    def panel(self, A, lc, i0, m, w, bb, is_owner):
+        mr = m - i0
+        Y = torch.zeros((bb, mr), dtype=torch.float64)
+        taus = torch.zeros(bb, dtype=torch.float64)
+        R11 = torch.zeros((bb, bb), dtype=torch.float64)
+        meta = torch.zeros(18, dtype=torch.uint8)
+        if is_owner:
+            M = self.mat(A)
+            work = np.array(M[i0:m, lc:lc + bb], order="F")
+            Yp, tp, bh = O.panel_factor(work, 0, w)
+            M[i0:m, lc:lc + bb] = work
+            Y[:bh] = torch.from_numpy(np.ascontiguousarray(Yp.T))
+            taus[:bh] = torch.from_numpy(tp)
+            R11.copy_(A[lc:lc + bb, i0:i0 + bb])
+            st = torch.zeros(24, dtype=torch.uint8)
+            st.view(torch.int32)[5] = bh
+            if bh == 0:
+                st.view(torch.int32)[0] = 1
+        else:
+            st = torch.zeros(24, dtype=torch.uint8)
+        return _Panel(0, Y, taus, None, R11, None, st)
+
+    def broadcast_panel(self, pan, owner, comm, mr, bb):
+        meta = pan.st[:24].view(torch.int32)
+        comm.broadcast(meta, owner)
+        comm.broadcast(pan.Y, owner)
+        comm.broadcast(pan.taus, owner)
+        comm.broadcast(pan.R11, owner)
+        mh = meta.numpy()
+        pan.bhat = 0 if mh[0] else int(mh[5])
+        pan.taus_host = pan.taus.numpy().copy()
+        pan.R11_host = np.triu(pan.R11.numpy().T[:pan.bhat, :pan.bhat])
+        return pan
+
+    def block_update(self, A, t0, i0, m, pan):
+        Y = pan.Y.numpy().T
+        tau = pan.taus.numpy()
+        T = O.t_factor(Y, tau)
+        pan.T = T
+        C = self.mat(A)[i0:m, t0:]
+        if C.shape[1]:
+            W = T.T @ (Y.T @ C)
+            C -= Y @ W
+
+    def sample_update_local(self, samp, A, s0, rel, i0, bb, pan):
+        ell = samp.Bf.shape[1]
+        if len(rel) == 0:
+            return torch.zeros((0, ell), dtype=torch.float64)
+        Bf = samp.Bf.numpy().T
+        R11 = np.triu(pan.R11.numpy().T)
+        R12 = self.mat(A)[i0:i0 + bb, s0:s0 + len(rel)]
+        X = O.back_solve(R11, R12)
+        top = Bf[:bb, rel] - np.triu(Bf[:bb, :bb]) @ X
+        Bn = np.vstack([top, Bf[bb:, rel]])
+        return torch.from_numpy(np.ascontiguousarray(Bn.T))

@@ -1,0 +1,85 @@
+"""Multi-process (gloo, CPU) test of the column block-cyclic RQRCP
+orchestration (paper_2008_04447_b200/distributed.py): world sizes 2 and 3
+must reproduce the single-process oracle (identical permutation, counters,
+achieved rank; R to 1e-10)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from conftest import gauss
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, m, n, k, b, p, seed, q):
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from dist_numpy_ops import NumpyOps
+        from paper_2008_04447_b200.distributed import BlockCyclic, TorchComm, rqrcp_block_cyclic
+        A = gauss(m, n, 17)
+        lay = BlockCyclic(n, b, world)
+        g = lay.global_of_local(rank)
+        A_loc = torch.from_numpy(np.ascontiguousarray(A[:, g].T))
+        res = rqrcp_block_cyclic(A_loc, m, n, k, b, p, seed, TorchComm(), NumpyOps())
+        parts = [torch.zeros((max(lay.n_local(r) for r in range(world)), m), dtype=torch.float64)
+                 for _ in range(world)]
+        mine = torch.zeros_like(parts[0])
+        mine[:A_loc.shape[0]] = A_loc
+        dist.all_gather(parts, mine)
+        if rank == 0:
+            W = np.zeros((m, n))
+            for r in range(world):
+                gr = lay.global_of_local(r)
+                W[:, gr] = parts[r][:gr.size].numpy().T
+            q.put((res.achieved, res.perm, W, [res.counters.trailing_passes, res.counters.blas3_volume],
+                   res.reason))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,m,n,k,b,p", [(2, 90, 70, 70, 8, 4), (3, 120, 100, 60, 16, 8), (2, 64, 80, 64, 8, 8)])
+def test_block_cyclic_matches_oracle(world, m, n, k, b, p):
+    from oracle import port as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, k, b, p, 5, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    achieved, perm, W, cnt, reason = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    A = gauss(m, n, 17)
+    ref = O.rqrcp(A, k, b=b, p=p, seed=5)
+    assert achieved == ref.achieved_rank
+    assert np.array_equal(perm, ref.perm)
+    assert cnt == [ref.counters.trailing_passes, ref.counters.blas3_volume]
+    R = np.triu(W[:achieved, :])
+    assert np.abs(R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
+
+
+def test_layout_roundtrip():
+    from paper_2008_04447_b200.distributed import BlockCyclic
+    for n, b, P in [(100, 8, 3), (128, 128, 4), (7, 2, 5)]:
+        lay = BlockCyclic(n, b, P)
+        seen = np.concatenate([lay.global_of_local(r) for r in range(P)])
+        assert np.array_equal(np.sort(seen), np.arange(n))
+        for r in range(P):
+            g = lay.global_of_local(r)
+            assert np.all(lay.owner(g) == r)
+            assert np.array_equal(lay.local_index(g), np.arange(g.size))
+        assert sum(lay.n_local(r) for r in range(P)) == n
