@@ -220,7 +220,7 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath)).get(dom)
+            traffic = json.load(open(tpath))[dom]["bytes_per_launch"]
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf, "peak": PEAK_FP64_TFLOPS,

@@ -13,7 +13,8 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsqr.so")
+# SQR_LIB selects an alternative in-tree build (kernel-variant experiments).
+LIB_PATH = os.path.join(HERE, os.environ.get("SQR_LIB", "libsqr.so"))
 
 c_i64 = ctypes.c_int64
 c_u64 = ctypes.c_uint64

@@ -9,11 +9,11 @@
 //            TRQRCP panel/R-row materialisation (randomized.py:305,330), TUXV A V_k
 //            (randomized.py:384).
 //
-// Both stage operands through a 4-deep cp.async ring in padded shared memory
+// Both stage operands through a cp.async ring in padded shared memory
 // (row pitch = 4 mod 16 doubles => conflict-free f64 fragment gathers) and
 // accumulate with m16n8k4 f64 MMAs.  gemm_tn splits K across CTAs when the
 // N-tiles cannot fill 148 SMs; partials are summed in a FIXED split order by
-// the last-arriving CTA of each tile, so results are bitwise deterministic.
+// a separate reduce kernel, so results are bitwise deterministic.
 #include <algorithm>
 
 #include "common.cuh"
@@ -29,6 +29,18 @@ constexpr int kThreads = 128;
 constexpr int kBK = 16;        // K per pipeline stage
 constexpr int kPitchK = kBK + 4;
 constexpr int kStages = 3;
+// gemm_nn runs 4 CTAs/SM with a 2-deep ring: measured on the C5 rank-128
+// update (32768 x 32640 x 128) 29.3 TF vs 24.2 TF at 2 CTAs x 3 stages and
+// 27.0 at 3 x 3 -- the short-K update is latency- not bandwidth-limited, so
+// resident warps beat pipeline depth (prefetching beta*E into registers
+// before the K loop gained nothing and costs the 4th CTA).
+#ifndef SQR_NN_STAGES
+#define SQR_NN_STAGES 2
+#endif
+#ifndef SQR_NN_CTAS
+#define SQR_NN_CTAS 4
+#endif
+constexpr int kStagesNN = SQR_NN_STAGES;
 
 // ---------------------------------------------------------------- gemm_tn
 // Computed as D^T(N x M) = C^T(N x K) X(K x M): MMA rows = n, MMA cols = i.
@@ -245,21 +257,22 @@ __global__ void __launch_bounds__(256)
 // CTA tile 64 m x 128 n; 4 warps = 2 (m) x 2 (n); warp tile 32 m x 64 n.
 // beta * E is read in the epilogue in two halves (32 values per thread in
 // flight each), its latency covered by the SM's other CTA.
-template <int VEC>
+template <int VEC, int BNT = 128>
 struct NnCfg {
-  static constexpr int BM = 64, BN = 128;
+  static constexpr int BM = 64, BN = BNT;
+  static constexpr int NJ = BN / 16;  // n8 fragments per warp (2 x 2 warps)
   static constexpr int PM = BM + 4;   // pitch of the m-contiguous X tile (4 mod 16)
   static constexpr int A_ELEMS = kBK * PM;
   static constexpr int B_ELEMS = BN * kPitchK;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int SMEM = STAGE * kStages * 8;
+  static constexpr int SMEM = STAGE * kStagesNN * 8;
 };
 
-template <int VEC>
+template <int VEC, int BNT>
 __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const double* __restrict__ X,
                                               int64_t ldx, const double* __restrict__ Y, int64_t ldy,
                                               int M, int N, int K, int m0, int n0, int k0) {
-  using Cfg = NnCfg<VEC>;
+  using Cfg = NnCfg<VEC, BNT>;
   const int tid = threadIdx.x;
   constexpr int CPM = Cfg::BM / VEC;  // chunks per k-row of X
 #pragma unroll 4
@@ -295,13 +308,15 @@ __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const doub
   }
 }
 
-template <int VEC>
-__global__ void __launch_bounds__(kThreads, 2)
+// CTA tile 64 m x BN n; 4 warps = 2 (m) x 2 (n); warp tile 32 m x BN/2 n.
+template <int VEC, int BNT>
+__global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
     gemm_nn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
                    const double* __restrict__ Y, int64_t ldy, double beta, const double* E,
                    int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
-  using Cfg = NnCfg<VEC>;
-  extern __shared__ __align__(16) double smem[];
+  using Cfg = NnCfg<VEC, BNT>;
+  constexpr int NJ = Cfg::NJ;
+    extern __shared__ __align__(16) double smem[];
   if (dyn.stop && *dyn.stop) return;
   if (dyn.shift) {
     const int sh = *dyn.shift;
@@ -317,52 +332,52 @@ __global__ void __launch_bounds__(kThreads, 2)
   if (n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 64;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * (Cfg::BN / 2);
   const int nk = (int)cdiv(K, kBK);
 
-  double acc[2][8][4];
+  double acc[2][NJ][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b)
+    for (int b = 0; b < NJ; ++b)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
 
 #pragma unroll
-  for (int s = 0; s < kStages - 1; ++s) {
+  for (int s = 0; s < kStagesNN - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * Cfg::STAGE;
-      nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
+      nn_load_stage<VEC, BNT>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
     }
     cp_async_commit();
   }
   for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<kStages - 2>();
+    cp_async_wait<kStagesNN - 2>();
     __syncthreads();
     {
-      const int ls = kt + kStages - 1;
+      const int ls = kt + kStagesNN - 1;
       if (ls < nk) {
-        double* st = smem + (ls % kStages) * Cfg::STAGE;
-        nn_load_stage<VEC>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
+        double* st = smem + (ls % kStagesNN) * Cfg::STAGE;
+        nn_load_stage<VEC, BNT>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
       }
       cp_async_commit();
     }
-    const double* sA = smem + (kt % kStages) * Cfg::STAGE;
+    const double* sA = smem + (kt % kStagesNN) * Cfg::STAGE;
     const double* sB = sA + Cfg::A_ELEMS;
 #pragma unroll
     for (int kk = 0; kk < kBK; kk += 4) {
-      double a[2][2], b[8];
+      double a[2][2], b[NJ];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi) {
         a[mi][0] = sA[(kk + t) * Cfg::PM + wm + mi * 16 + g];
         a[mi][1] = sA[(kk + t) * Cfg::PM + wm + mi * 16 + g + 8];
       }
 #pragma unroll
-      for (int nj = 0; nj < 8; ++nj) b[nj] = sB[(wn + nj * 8 + g) * kPitchK + kk + t];
+      for (int nj = 0; nj < NJ; ++nj) b[nj] = sB[(wn + nj * 8 + g) * kPitchK + kk + t];
 #pragma unroll
       for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-        for (int nj = 0; nj < 8; ++nj) dmma16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
+        for (int nj = 0; nj < NJ; ++nj) dmma16x8x4(acc[mi][nj], a[mi][0], a[mi][1], b[nj]);
     }
   }
   cp_async_wait<0>();
@@ -372,28 +387,28 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
       const int m = m0 + wm + mi * 16 + g + h * 8;
-      double ev[8][2];
+      double el[NJ][2];
       if (beta != 0.0) {
 #pragma unroll
-        for (int nj = 0; nj < 8; ++nj)
+        for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
             const int n = n0 + wn + nj * 8 + 2 * t + e;
-            ev[nj][e] = (m < M && n < N) ? E[(int64_t)n * lde + m] : 0.0;
+            el[nj][e] = (m < M && n < N) ? E[(int64_t)n * lde + m] : 0.0;
           }
       }
       if (m >= M) continue;
 #pragma unroll
-      for (int nj = 0; nj < 8; ++nj)
+      for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
           const int n = n0 + wn + nj * 8 + 2 * t + e;
           if (n >= N) continue;
           double v = alpha * acc[mi][nj][h * 2 + e];
-          if (beta != 0.0) v = fma(beta, ev[nj][e], v);
+          if (beta != 0.0) v = fma(beta, el[nj][e], v);
           D[(int64_t)n * ldd + m] = v;
         }
-  }
+    }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -464,21 +479,24 @@ int dispatch_tn_vec(int M, int N, int K, double alpha, const double* X, int64_t 
   return launch_tn<MT, 1>(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
 }
 
+#ifndef SQR_NN_BN
+#define SQR_NN_BN 64
+#endif
 template <int VEC>
 int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* Y,
               int64_t ldy, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
               GemmDyn dyn, cudaStream_t s) {
-  using Cfg = NnCfg<VEC>;
+  using Cfg = NnCfg<VEC, SQR_NN_BN>;
   static bool configured = false;
   if (!configured) {
-    SQR_CUDA(cudaFuncSetAttribute(gemm_nn_kernel<VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    SQR_CUDA(cudaFuncSetAttribute(gemm_nn_kernel<VEC, SQR_NN_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   Cfg::SMEM));
     configured = true;
   }
   dim3 grid((unsigned)cdiv(M, Cfg::BM), (unsigned)cdiv(N, Cfg::BN));
   ProfScope ps(kTagGemmNn, s);
-  gemm_nn_kernel<VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde,
-                                                       D, ldd, dyn);
+  gemm_nn_kernel<VEC, SQR_NN_BN><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde,
+                                                                  D, ldd, dyn);
   SQR_LAUNCH("gemm_nn_kernel");
   return SQR_OK;
 }
