@@ -37,6 +37,7 @@ struct RqrcpWs {
   double *Bcur, *Bnext, *Bf, *stau, *Ypan, *Gm, *Wt, *W, *OmT, *gemm, *pscr;
   int64_t* lperm;
   int32_t* moves;
+  int32_t* snap;  // {stop .. bhat} of the block whose bulk update is in flight
   void *sample, *panel;
   int64_t sample_bytes, panel_bytes;
   int64_t total;
@@ -63,6 +64,7 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.W = c.take<double>(b * n);
   w.OmT = (need_omega || resample) ? c.take<double>(m * ell) : nullptr;
   w.pscr = c.take<double>(PanelScratch::doubles(b));
+  w.snap = c.take<int32_t>(8);
   w.total = c.off + 256;
   return w;
 }
@@ -115,7 +117,7 @@ int panel_factor(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t wstat, 
 // with C starting bhat columns right of P (device-side shift).
 int trailing_update(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, const double* Y,
                     int64_t ldy, const double* taus, double* T, int64_t ldt, double* GWt, double* W,
-                    int64_t ldw, sqr_status* st, double* gws, cudaStream_t s) {
+                    int64_t ldw, sqr_status* st, double* gws, cudaStream_t s, bool skip_pass2 = false) {
   GemmDyn d1{&st->stop, &st->bhat, kShiftB};
   d1.pre = Y;
   d1.ldpre = ldy;
@@ -128,8 +130,51 @@ int trailing_update(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, 
   if (nt <= 1) return SQR_OK;
   const double* Wt = GWt + bb * ldw;
   rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, Wt, ldw, 0.0, nullptr, 0, W, ldw, gws, kGemmWsBytes, s, d2);
-  if (rc) return rc;
+  if (rc || skip_pass2) return rc;
   return gemm_nn(mr, nt, bb, 1.0, Y, ldy, W, ldw, 1.0, P, lda, P, lda, s, d3);
+}
+
+// Lookahead schedule of one block's second sweep (randomized.py:207-221):
+// the R12 rows [0, bb) are updated first; then the bulk rows [bb, mr) run on
+// the caller's stream while a high-priority side stream finishes the block
+// (finish_block, sample update, next block's sample QRCP), which only reads
+// R11/R12 and the sample.  The bulk GEMM gates on a snapshot of {stop, bhat}
+// so the side stream's status writes cannot reach it.
+struct Lookahead {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  bool on = false;
+  ~Lookahead() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
+  }
+  int init() {
+    static const bool disabled = [] {
+      const char* e = getenv("SQR_NO_LOOKAHEAD");
+      return e && *e && *e != '0';
+    }();
+    if (disabled) return SQR_OK;
+    int lo = 0, hi = 0;
+    SQR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SQR_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+    SQR_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    SQR_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    on = true;
+    return SQR_OK;
+  }
+};
+
+int pass2_split(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, const double* Y, int64_t ldy,
+                const double* W, int64_t ldw, sqr_status* st, int32_t* snap, cudaStream_t s, cudaEvent_t fork) {
+  SQR_CUDA(cudaMemcpyAsync(snap, st, 6 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+  GemmDyn d3{&snap[0], &snap[5], kShiftD};
+  const int64_t top = std::min(bb, mr);
+  int rc = gemm_nn(top, nt, bb, 1.0, Y, ldy, W, ldw, 1.0, P, lda, P, lda, s, d3);
+  if (rc) return rc;
+  SQR_CUDA(cudaEventRecord(fork, s));
+  if (mr > top) rc = gemm_nn(mr - top, nt, bb, 1.0, Y + top, ldy, W, ldw, 1.0, P + top, lda, P + top, lda, s, d3);
+  return rc;
 }
 
 }  // namespace
@@ -180,11 +225,14 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
   const int64_t nblk = cdiv(k, b);
   double* Bc = w.Bcur;
   double* Bn = w.Bnext;
+  Lookahead la;
+  if (!resample && (rc = la.init())) return rc;
   for (int64_t J = 0; J < nblk; ++J) {
     const int64_t i0 = J * b, bb = std::min(b, k - i0), nt = n - i0, mr = m - i0;
     double* P = A + i0 + i0 * lda;
     double* TJ = T + J * b * b;
-    if ((rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
+    if ((J == 0 || !la.on) &&
+        (rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
                           w.sample_bytes, s)))
       return rc;
     if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
@@ -192,6 +240,27 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
       PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
       if ((rc = panel_factor(P, lda, mr, bb, -1, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
         return rc;
+    }
+    if (la.on) {
+      // Second sweep split around the side stream (see Lookahead).
+      if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s,
+                                true)))
+        return rc;
+      if (nt > 1 && (rc = pass2_split(P, lda, mr, nt, bb, w.Ypan, m, w.W, b, st, w.snap, s, la.fork))) return rc;
+      if (nt <= 1) SQR_CUDA(cudaEventRecord(la.fork, s));
+      cudaStream_t s2 = la.side;
+      SQR_CUDA(cudaStreamWaitEvent(s2, la.fork, 0));
+      if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s2))) return rc;
+      if (J + 1 < nblk) {
+        std::swap(Bc, Bn);
+        if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, bb, Bc, ell, st, w.Gm, s2))) return rc;
+        if ((rc = sample_qrcp(Bc, ell, ell, nt - bb, std::min(b, k - i0 - b), w.Bf, ell, w.lperm, w.moves, w.stau,
+                              false, st, w.sample, w.sample_bytes, s2)))
+          return rc;
+      }
+      SQR_CUDA(cudaEventRecord(la.join, s2));
+      SQR_CUDA(cudaStreamWaitEvent(s, la.join, 0));
+      continue;
     }
     if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s)))
       return rc;

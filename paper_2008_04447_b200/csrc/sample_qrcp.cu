@@ -50,8 +50,7 @@ struct SampleArgs {
   double* taus;
   sqr_status* st;
   unsigned* bar;
-  double* cval;    // [2][G]
-  int* cpos;       // [2][G]
+  double2* cand;   // [2][G] {norm^2, position bits}: one 16-byte record per CTA
   double* ccol;    // [2][G][ell]
   double* psum;    // [G]
   double* pmax;    // [G]
@@ -229,10 +228,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
     int l = lane < (kSqThreads >> 5) ? wl_s[lane] : -1;
     warp_argmax(v, p, l);
     const int par = jn & 1;
-    if (warp == 0 && lane == 0) {
-      a.cval[par * G + g] = v;
-      a.cpos[par * G + g] = p;
-    }
+    if (warp == 0 && lane == 0) a.cand[par * G + g] = make_double2(v, __longlong_as_double((long long)p));
     double* dst = a.ccol + ((size_t)par * G + g) * ell;
     if (l >= 0 && (!a.reg_spill || l < a.cap)) {
       if (warp == 0) {
@@ -267,16 +263,26 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
     const int par = jn & 1;
     double bv = -1.0;
     int bp = INT_MAX, bl = -1;
-    for (int i = lane; i < G; i += 32) {
-      const double v = __ldcg(a.cval + par * G + i);
-      const int p = __ldcg(a.cpos + par * G + i);
-      if (better(v, p, bv, bp)) {
-        bv = v;
-        bp = p;
-        bl = i;
+    {
+      // all records in flight at once (G <= 160), then a local + warp argmax
+      double2 rec[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        rec[k] = i < G ? __ldcg(a.cand + par * G + i) : make_double2(-1.0, __longlong_as_double((long long)INT_MAX));
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int p = (int)__double_as_longlong(rec[k].y);
+        if (better(rec[k].x, p, bv, bp)) {
+          bv = rec[k].x;
+          bp = p;
+          bl = lane + 32 * k;
+        }
       }
     }
     warp_argmax(bv, bp, bl);
+    if (lane == 0) SQR_TRACE(a.trace, 8 * (jn - 1) + 7);
     const int len = ell - jn;
     double* ysh = ybuf + par * (ell + 2);
     double x[kMaxRowsPerLane];
@@ -411,20 +417,41 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       }
     }
     SQR_TRACE(a.trace, 8 * j + 1);
-    // Register-resident spill columns: one warp per column, fully updated here.
+    // Register-resident spill columns: warp q owns columns cap + q + 8 i
+    // (i < 5), lanes own rows.  The five columns' warp reductions are
+    // interleaved (one shuffle chain of depth 5 instead of five), and the
+    // exact-recompute reduction only runs when the guard fires.
     if (a.reg_spill) {
-      auto spill_col = [&](double(&xc)[kMaxRowsPerLane], const int i) {
+      int pcol[kSpillPerWarp];
+      double dot[kSpillPerWarp];
+#pragma unroll
+      for (int i = 0; i < kSpillPerWarp; ++i) {
         const int lc = a.cap + warp + 8 * i;
-        if (lc >= ncols) return;
-        const int p = pos[lc];
-        if (p < 0) return;
-        if (p == pc) {
+        pcol[i] = lc < ncols ? pos[lc] : -1;
+        dot[i] = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
+          const int r = lane + 32 * qq;
+          if (r >= j && r < ell) dot[i] = fma(yw[r - j], xs[i][qq], dot[i]);
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int i = 0; i < kSpillPerWarp; ++i) dot[i] += __shfl_xor_sync(0xffffffffu, dot[i], o);
+      double ex[kSpillPerWarp], rjv[kSpillPerWarp];
+#pragma unroll
+      for (int i = 0; i < kSpillPerWarp; ++i) {
+        const int lc = a.cap + warp + 8 * i;
+        ex[i] = 0.0;
+        rjv[i] = 0.0;
+        if (pcol[i] < 0) continue;
+        if (pcol[i] == pc) {  // the winner: its final column goes to Bf (xs untouched)
 #pragma unroll
           for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
             const int r = lane + 32 * qq;
-            if (r < ell) a.Bf[(int64_t)j * a.ldbf + r] = r < j ? xc[qq] : (r == j ? beta : yw[r - j]);
+            if (r < ell) a.Bf[(int64_t)j * a.ldbf + r] = r < j ? xs[i][qq] : (r == j ? beta : yw[r - j]);
           }
-          __syncwarp();
           if (lane == 0) {
             a.lperm[j] = col0 + lc;
             if (col0 + lc != j) {
@@ -432,38 +459,58 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
               a.moves[2 * slot] = j;
               a.moves[2 * slot + 1] = col0 + lc;
             }
-            pos[lc] = -1;
           }
-          __syncwarp();
-          return;
+          continue;
         }
-        const int pn = (p == j) ? pc : p;
-        double part = 0.0;
-#pragma unroll
-        for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
-          const int r = lane + 32 * qq;
-          if (r >= j && r < ell) part = fma(yw[r - j], xc[qq], part);
-        }
-        const double wvv = tau * warp_sum(part);
-        double ex = 0.0, rjv = 0.0;
+        const double wvv = tau * dot[i];
 #pragma unroll
         for (int qq = 0; qq < kMaxRowsPerLane; ++qq) {
           const int r = lane + 32 * qq;
           if (r >= j && r < ell) {
-            xc[qq] = fma(-yw[r - j], wvv, xc[qq]);
-            if (r > j) ex = fma(xc[qq], xc[qq], ex);
+            xs[i][qq] = fma(-yw[r - j], wvv, xs[i][qq]);
+            if (r > j) ex[i] = fma(xs[i][qq], xs[i][qq], ex[i]);
           }
-          // select, not xc[j >> 5]: a dynamic index would demote xs to local memory
-          asm("{ .reg .pred p; setp.eq.s32 p, %2, %3; selp.f64 %0, %1, %0, p; }" : "+d"(rjv) : "d"(xc[qq]), "r"(j >> 5), "r"(qq));
+          // select, not xs[i][j >> 5]: a dynamic index would demote xs to local memory
+          asm("{ .reg .pred p; setp.eq.s32 p, %2, %3; selp.f64 %0, %1, %0, p; }"
+              : "+d"(rjv[i]) : "d"(xs[i][qq]), "r"(j >> 5), "r"(qq));
         }
-        const double rj = __shfl_sync(0xffffffffu, rjv, j & 31);
-        double ns = nsq[lc] - rj * rj;
-        const bool recompute = ns < kNormGuard * rsq[lc];
-        ex = warp_sum(ex);
-        ns = recompute ? ex : fmax(ns, 0.0);
-        __syncwarp();
-        if (lane == 0) {
-          if (recompute) rsq[lc] = ex;
+      }
+      bool need = false;
+      double nsv[kSpillPerWarp];
+#pragma unroll
+      for (int i = 0; i < kSpillPerWarp; ++i) {
+        const int lc = a.cap + warp + 8 * i;
+        const double rj = __shfl_sync(0xffffffffu, rjv[i], j & 31);
+        nsv[i] = 0.0;
+        if (pcol[i] < 0 || pcol[i] == pc) continue;
+        nsv[i] = nsq[lc] - rj * rj;
+        need |= nsv[i] < kNormGuard * rsq[lc];
+      }
+      if (need) {  // warp-uniform
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int i = 0; i < kSpillPerWarp; ++i) ex[i] += __shfl_xor_sync(0xffffffffu, ex[i], o);
+      }
+      __syncwarp();
+      if (lane == 0) {
+#pragma unroll
+        for (int i = 0; i < kSpillPerWarp; ++i) {
+          const int lc = a.cap + warp + 8 * i;
+          const int p = pcol[i];
+          if (p < 0) continue;
+          if (p == pc) {
+            pos[lc] = -1;
+            continue;
+          }
+          const int pn = (p == j) ? pc : p;
+          double ns = nsv[i];
+          if (ns < kNormGuard * rsq[lc]) {
+            ns = ex[i];
+            rsq[lc] = ns;
+          } else {
+            ns = fmax(ns, 0.0);
+          }
           nsq[lc] = ns;
           pos[lc] = pn;
           if (better(ns, pn, cbv, cbp)) {
@@ -472,14 +519,8 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
             cbl = lc;
           }
         }
-        __syncwarp();
-      };
-      static_assert(kSpillPerWarp == 5, "unrolled below");
-      spill_col(xs[0], 0);
-      spill_col(xs[1], 1);
-      spill_col(xs[2], 2);
-      spill_col(xs[3], 3);
-      spill_col(xs[4], 4);
+      }
+      __syncwarp();
     }
     // Spilled (L2-resident) columns (no reg mode): one warp per column, full update.
     for (int lc = a.cap + warp; a.warp_spill && !a.reg_spill && lc < ncols; lc += kSqThreads / 32) {
@@ -552,6 +593,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
       SQR_TRACE(a.trace, 8 * j + 3);
       if (warp == 0) {
         if (lane == 0) gb.wait_lane0();
+        if (lane == 0) SQR_TRACE(a.trace, 8 * j + 6);
         __syncwarp();
         winner(j + 1);
       } else {
@@ -615,7 +657,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
 struct SampleWorkspace {
   static int64_t bytes(int64_t ell, int64_t nt) {
     const int64_t G = 148;
-    return 64 + 2 * G * 8 + 2 * G * 4 + 2 * G * ell * 8 + 2 * G * 8 + nt * ell * 8 + 1024;
+    return 64 + 2 * G * 16 + 2 * G * ell * 8 + 2 * G * 8 + nt * ell * 8 + 1024;
   }
 };
 
@@ -641,7 +683,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   const int64_t smem_avail = (int64_t)max_smem_optin() - 2048 - 2 * (ell + 2) * 8 - 64;
   const int64_t fit = std::max<int64_t>(1, smem_avail / ((int64_t)ldS * 8 + fixed_per_col));
   const int64_t ntc = std::max<int64_t>(nt, 1);
-  int G = (int)std::min<int64_t>(sms, std::max<int64_t>(cdiv(ntc, 32), cdiv(ntc, fit)));
+  int G = (int)std::min<int64_t>(std::min(sms, 148), std::max<int64_t>(cdiv(ntc, 32), cdiv(ntc, fit)));
   G = std::max(G, 1);
   const int w = (int)cdiv(ntc, G);
   G = (int)cdiv(ntc, w);
@@ -671,10 +713,8 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   a.st = st;
   a.bar = reinterpret_cast<unsigned*>(p);
   p += 64;
-  a.cval = reinterpret_cast<double*>(p);
-  p += 2 * 148 * 8;
-  a.cpos = reinterpret_cast<int*>(p);
-  p += 2 * 148 * 4;
+  a.cand = reinterpret_cast<double2*>(p);
+  p += 2 * 148 * 16;
   a.ccol = reinterpret_cast<double*>(p);
   p += 2 * 148 * ell * 8;
   a.psum = reinterpret_cast<double*>(p);

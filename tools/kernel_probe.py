@@ -81,11 +81,22 @@ def panel():
 
 
 timed("panel", panel)
+pf_ws = torch.zeros(int(L.sqr_block_workspace(m, n, b)), dtype=torch.uint8, device=dev)
+
+
+def panel_leaves():
+    P.t.copy_(P0)
+    st.zero_()
+    _lib.check(L.sqr_panel_factor(P.ptr, P.ld, m, b, Y.ptr, Y.ld, taus.data_ptr(), 1, st.data_ptr(),
+                                  pf_ws.data_ptr(), pf_ws.numel(), s))
+
+
+timed("panel_leaves", panel_leaves)
 
 if os.environ.get("SQR_TRACE"):
     import numpy as np
     tr = torch.zeros(8 * 256, dtype=torch.int64, device=dev)
-    for name, fn in (("sample_qrcp", sample), ("panel", panel)):
+    for name, fn in (("sample_qrcp", sample), ("panel", panel), ("panel_leaves", panel_leaves)):
         tr.zero_()
         L.sqr_debug_trace(tr.data_ptr())
         L.sqr_profile_enable(64)
