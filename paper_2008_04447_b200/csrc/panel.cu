@@ -19,6 +19,7 @@
 // stops the panel (randomized.py:120-121) after the remaining panel columns
 // have received every earlier reflector, as in the reference loop.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -348,6 +349,178 @@ __global__ void __launch_bounds__(kPThreads, 1) panel_kernel(PanelArgs a) {
   }
 }
 
+// Leaf kernel (w <= 32 columns): the same column step as panel_kernel with
+// the CTA's rows held in REGISTERS, one row (RPT rows) per thread, all 32
+// columns.  The step loop is fully unrolled so every column index is static;
+// the per-step partials [sum a_r^2, sum a_r P_rc] are reduced inside a warp
+// by a transpose butterfly (31 shuffles for 32 values, lane v ends with
+// value v), across warps through shared memory, and across CTAs by the same
+// fixed-order read of the G partials as panel_kernel.  Deterministic.
+constexpr int kLThreads = 256;
+constexpr int kLWarps = kLThreads / 32;
+constexpr int kLW = 32;
+
+template <int RPT>
+__global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
+  __shared__ double red[kLWarps][kLW];
+  __shared__ double vals[kLW];
+  __shared__ double rowv[kLW];
+  __shared__ double wv[kLW];
+  if (a.st->stop) return;
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int lc0 = a.c0;
+  const int wglob = a.wstat < 0 ? a.st->sample_achieved : a.wstat;
+  const bool prior_stop = lc0 > 0 && a.st->bhat < lc0;  // an earlier leaf hit a zero column
+  const int w = prior_stop ? 0 : max(0, min(wglob - lc0, a.wmax));
+  if (lc0 > 0) {
+    if (g == 0)  // explicit Y is zero above the leaf's first row
+      for (int e = tid; e < lc0 * a.wmax; e += kLThreads)
+        a.Y[(int64_t)(lc0 + e / lc0) * a.ldy + (e % lc0)] = 0.0;
+    a.P += lc0 + (int64_t)lc0 * a.ldp;
+    a.Y += lc0 + (int64_t)lc0 * a.ldy;
+    a.taus += lc0;
+    a.mr -= lc0;
+  }
+  SQR_TRACE(a.trace, 8 * 40 + 0);
+  GridBarrier gb;
+  gb.init(a.bar);
+  int rows[RPT];
+  double x[RPT][kLW];
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    rows[i] = g * kLThreads * RPT + i * kLThreads + tid;
+#pragma unroll
+    for (int c = 0; c < kLW; ++c)
+      x[i][c] = (rows[i] < a.mr && c < w) ? a.P[(int64_t)c * a.ldp + rows[i]] : 0.0;
+  }
+  int bhat = w;
+  SQR_TRACE(a.trace, 8 * 40 + 1);
+#pragma unroll
+  for (int t = 0; t < kLW; ++t) {
+    if (t >= w) break;
+    const int par = t & 1;
+    // ---- partials of step t over my rows > t: q[0] = |a|^2, q[v] = a . P_{t+v}
+    double q[kLW];
+#pragma unroll
+    for (int v = 0; v < kLW; ++v) q[v] = 0.0;
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      const bool in = rows[i] > t;
+      const double av = in ? x[i][t] : 0.0;
+#pragma unroll
+      for (int v = 0; v < kLW - t; ++v) q[v] = fma(av, x[i][t + v], q[v]);
+    }
+    // ---- warp transpose butterfly: lane l ends with the warp sum of value l
+#pragma unroll
+    for (int k = 16; k >= 1; k >>= 1) {
+      const bool upper = (lane & k) != 0;
+#pragma unroll
+      for (int i = 0; i < k; ++i) {
+        const double send = upper ? q[i] : q[i + k];
+        const double keep = upper ? q[i + k] : q[i];
+        q[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
+      }
+    }
+    red[warp][lane] = q[0];
+    __syncthreads();
+    if (tid < kLW - t) {
+      double s = 0.0;
+#pragma unroll
+      for (int wi = 0; wi < kLWarps; ++wi) s += red[wi][tid];
+      a.part[((size_t)par * (kLW + 1) + tid) * G + g] = s;
+    }
+    // the owner of row t (CTA 0, thread t) publishes it
+    if (g == 0 && tid == t) {
+#pragma unroll
+      for (int v = 0; v < kLW - t; ++v) a.rowt[par * (kLW + 1) + v] = x[0][t + v];
+    }
+    SQR_TRACE(a.trace, 8 * t + 1);
+    gb.sync();
+    SQR_TRACE(a.trace, 8 * t + 2);
+    {
+      const int L = min(kLW - t, w - t);
+      if (tid < L) rowv[tid] = __ldcg(a.rowt + par * (kLW + 1) + tid);
+      // 8 lanes per value (32 values x 8 = 256 threads), G/8 loads each in flight
+      const int v = tid >> 3, qd = tid & 7;
+      if (v < L) {
+        double xr[kMaxG / 8];
+        const double* src = a.part + ((size_t)par * (kLW + 1) + v) * G;
+#pragma unroll
+        for (int i = 0; i < kMaxG / 8; ++i) {
+          const int gi = qd + 8 * i;
+          xr[i] = gi < G ? __ldcg(src + gi) : 0.0;
+        }
+        double sacc = 0.0;
+#pragma unroll
+        for (int i = 0; i < kMaxG / 8; ++i) sacc += xr[i];
+        const unsigned gm = 0xffu << (lane & 24);  // this value's 8-lane group
+        sacc += __shfl_xor_sync(gm, sacc, 4);
+        sacc += __shfl_xor_sync(gm, sacc, 2);
+        sacc += __shfl_xor_sync(gm, sacc, 1);
+        if (qd == 0) vals[v] = sacc;
+      }
+    }
+    __syncthreads();
+    SQR_TRACE(a.trace, 8 * t + 3);
+    const double at = rowv[0], sa = vals[0];
+    const double nrm = sqrt(fma(at, at, sa));
+    if (nrm == 0.0 && a.stop_at_zero) {
+      bhat = t;
+      break;
+    }
+    double beta = 0.0, tau = 0.0, y0 = 1.0;
+    if (nrm != 0.0) {
+      beta = (at >= 0.0 ? -1.0 : 1.0) * nrm;
+      y0 = at - beta;
+      tau = 2.0 / (1.0 + sa / (y0 * y0));
+    }
+    if (tid >= 1 && tid < min(kLW - t, w - t)) wv[tid] = tau * (rowv[tid] + vals[tid] / y0);
+    if (g == 0 && tid == 0) a.taus[t] = tau;
+    __syncthreads();
+    // ---- apply reflector t to my rows (row t keeps beta and its R entries)
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+      if (rows[i] > t) {
+        const double yr = nrm != 0.0 ? x[i][t] / y0 : 0.0;
+        x[i][t] = yr;
+#pragma unroll
+        for (int v = 1; v < kLW - t; ++v) x[i][t + v] = fma(-yr, wv[v], x[i][t + v]);
+      } else if (rows[i] == t) {
+        x[i][t] = beta;
+#pragma unroll
+        for (int v = 1; v < kLW - t; ++v) x[i][t + v] -= wv[v];
+      }
+    }
+    SQR_TRACE(a.trace, 8 * t + 4);
+  }
+  // ---- write back: packed R / reflector tails into P, explicit Y
+#pragma unroll
+  for (int i = 0; i < RPT; ++i) {
+    const int R = rows[i];
+    if (R >= a.mr) continue;
+#pragma unroll
+    for (int c = 0; c < kLW; ++c) {
+      if (c < w) a.P[(int64_t)c * a.ldp + R] = x[i][c];
+      if (c < a.wmax) {
+        const double y = c < bhat ? (R > c ? x[i][c] : (R == c ? 1.0 : 0.0)) : 0.0;
+        a.Y[(int64_t)c * a.ldy + R] = y;
+      }
+    }
+  }
+  SQR_TRACE(a.trace, 8 * 40 + 2);
+  if (g == 0 && tid == 0) {
+    for (int c = bhat; c < a.wmax; ++c) a.taus[c] = 0.0;
+    if (!prior_stop) {
+      a.st->bhat = lc0 + bhat;
+      if (lc0 == 0 && bhat == 0 && a.stop_at_zero) {
+        a.st->stop = 1;
+        a.st->reason = SQR_STOP_PANEL_ZERO;
+      }
+    }
+  }
+}
+
 // T from G = Y^T Y and taus (one CTA), householder.py:52-61.
 //  1. 32 x 32 diagonal blocks, one warp each, by the reference recurrence
 //     T[:c, c] = -tau_c T[:c, :c] G[:c, c] (lane i keeps row i of its block
@@ -459,6 +632,38 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
     return SQR_EINVAL;
   }
   const int sms = sm_count();
+  const int64_t mrl0 = mr - c0;
+  if (wmax <= kLW && mrl0 <= (int64_t)std::min(sms, 148) * kLThreads * 2 && getenv("SQR_NO_LEAF") == nullptr) {
+    // register-resident leaf kernel: one (or two) rows per thread
+    const int rpt = mrl0 <= (int64_t)std::min(sms, 148) * kLThreads ? 1 : 2;
+    const int G = (int)cdiv(mrl0, (int64_t)kLThreads * rpt);
+    PanelArgs a{};
+    a.P = P;
+    a.ldp = ldp;
+    a.mr = (int)mr;
+    a.c0 = (int)c0;
+    a.wstat = (int)w;
+    a.wmax = (int)wmax;
+    a.stop_at_zero = stop_at_zero;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.taus = taus;
+    a.st = st;
+    char* p = static_cast<char*>(ws);
+    a.bar = reinterpret_cast<unsigned*>(p);
+    p += 64;
+    a.part = reinterpret_cast<double*>(p);
+    p += 2 * 148 * (128 + 1) * 8;
+    a.rowt = reinterpret_cast<double*>(p);
+    a.trace = g_trace_host_ptr;
+    void* args[] = {&a};
+    SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+    ProfScope ps(kTagPanel, s);
+    count_launch();
+    const void* fn = rpt == 1 ? (const void*)leaf_kernel<1> : (const void*)leaf_kernel<2>;
+    SQR_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kLThreads), args, 0, s));
+    return SQR_OK;
+  }
   const int64_t budget0 = (int64_t)max_smem_optin() - 4 * 1024;  // static smem of the kernel
   // Fewest CTAs whose row slabs still hold the whole panel in shared memory
   // (less cross-CTA reduction traffic per step), at least 64 rows each.

@@ -105,7 +105,11 @@ if os.environ.get("SQR_TRACE"):
         L.sqr_debug_trace(None)
         prof = _lib.profile_collect()
         L.sqr_profile_enable(0)
-        t = tr.cpu().numpy().reshape(256, 8)[:128].astype(np.float64)
+        t_all = tr.cpu().numpy().reshape(256, 8).astype(np.float64)
+        if t_all[40, 0] > 0:
+            print("   leaf raw", t_all[40, :3] - t_all[40, 0], "step0", t_all[0, :8] - t_all[40, 0], "step31", t_all[31, :8] - t_all[40, 0],
+                  "us (last leaf)")
+        t = t_all[:40]
         # per step: deltas between consecutive nonzero stamps (slot order), and to the next step
         flat = []
         for j in range(t.shape[0]):
