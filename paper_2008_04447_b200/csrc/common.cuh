@@ -214,6 +214,10 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
                 int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st, void* ws,
                 int64_t ws_bytes, cudaStream_t s);
 int64_t panel_workspace(int64_t w);
+int64_t panel_block_max_rows();
+int64_t panel_block_workspace();
+int panel_block(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
+                double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s);
 int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
              double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s,
              int64_t c0 = 0);

@@ -4,6 +4,7 @@
 // sqr_status that the downstream kernels of the same and later blocks test,
 // so the loop shape is static and can be captured in a CUDA graph.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -78,6 +79,9 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
 int panel_factor(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t wstat, double* Y, int64_t ldy,
                  double* taus, int stop_at_zero, sqr_status* st, void* pws, int64_t pwsb, const PanelScratch& sc,
                  double* gws, cudaStream_t s) {
+  static const bool no_block = getenv("SQR_NO_BLOCKPANEL") != nullptr;
+  if (!no_block && mr <= panel_block_max_rows() && bb <= 128)
+    return panel_block(P, lda, mr, wstat, bb, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s);
   int rc;
   for (int64_t c0 = 0; c0 < bb; c0 += kLeaf) {
     const int64_t lwe = std::min(kLeaf, bb - c0);

@@ -613,8 +613,9 @@ __global__ void __launch_bounds__(kTThreads, 1)
 
 int64_t panel_workspace(int64_t w) {
   const int64_t G = 148, sw = 128;
-  return 64 + 2 * G * (sw + 1) * 8 + 2 * (sw + 1) * 8 + G * sw * std::max<int64_t>(w, 1) * 8 +
-         sw * std::max<int64_t>(w, 1) * 8 + 4096;
+  return std::max<int64_t>(panel_block_workspace(),
+                           64 + 2 * G * (sw + 1) * 8 + 2 * (sw + 1) * 8 + G * sw * std::max<int64_t>(w, 1) * 8 +
+                               sw * std::max<int64_t>(w, 1) * 8 + 4096);
 }
 
 // Rows per CTA >= 64 and at most one CTA per SM; the largest sub-panel width

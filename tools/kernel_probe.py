@@ -106,7 +106,12 @@ if os.environ.get("SQR_TRACE"):
         prof = _lib.profile_collect()
         L.sqr_profile_enable(0)
         t_all = tr.cpu().numpy().reshape(256, 8).astype(np.float64)
-        if t_all[40, 0] > 0:
+        if name == "panel_leaves":
+            base = t_all[40, 7]
+            for li in range(4):
+                print("   leaf", li, ((t_all[40 + li] - base) / 1e3).round(2).tolist(), "T done", round((t_all[44 + li, 0] - base) / 1e3, 2))
+            print("   leaf0 steps (pre-barrier, post-barrier):", [(round((t_all[s, 1] - base) / 1e3, 1), round((t_all[s, 2] - base) / 1e3, 1)) for s in range(0, 32, 4)])
+        if t_all[40, 0] > 0 and name != "panel_leaves":
             print("   leaf raw", t_all[40, :3] - t_all[40, 0], "step0", t_all[0, :8] - t_all[40, 0], "step31", t_all[31, :8] - t_all[40, 0],
                   "us (last leaf)")
         t = t_all[:40]
