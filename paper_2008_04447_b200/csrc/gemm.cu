@@ -97,6 +97,64 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
   }
 }
 
+// Aligned (16-byte) fast path of tn_load_stage: the per-thread source rows
+// (prefix / C selection, bounds) are resolved once per CTA, so a stage costs
+// one add and one cp.async per 16-byte chunk.
+template <int MT>
+struct TnLoader2 {
+  static constexpr int CPR = kBK / 2;             // 16-byte chunks per k-row
+  static constexpr int RSTEP = kThreads / CPR;    // rows covered per pass
+  static constexpr int NA = 64 / RSTEP;
+  static constexpr int NB = (MT + RSTEP - 1) / RSTEP;
+  const double* asrc[NA];
+  const double* bsrc;
+  int64_t bstep;
+  uint32_t adst, bdst;
+  int kc, r0, M;
+  unsigned aok, bok;
+  __device__ __forceinline__ void init(const double* X, int64_t ldx, const double* C, int64_t ldc, int M_,
+                                       int N, int n0, const GemmDyn& dyn, const double* sA, const double* sB) {
+    const int tid = threadIdx.x;
+    r0 = tid / CPR;
+    kc = (tid % CPR) * 2;
+    M = M_;
+    aok = 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int n = n0 + r0 + RSTEP * i;
+      const bool ok = n < N;
+      aok |= (ok ? 1u : 0u) << i;
+      asrc[i] = !ok ? C
+                    : (n < dyn.npre ? dyn.pre + (int64_t)n * dyn.ldpre : C + (int64_t)(n - dyn.npre) * ldc);
+    }
+    bok = 0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) bok |= ((r0 + RSTEP * i) < M ? 1u : 0u) << i;
+    bsrc = X + (int64_t)r0 * ldx;
+    bstep = (int64_t)RSTEP * ldx;
+    adst = smem_u32(sA + r0 * kPitchK + kc);
+    bdst = smem_u32(sB + r0 * kPitchK + kc);
+  }
+  __device__ __forceinline__ void load(uint32_t stage_off, int k0, int kend) const {
+    const int k = k0 + kc;
+    const int sz = k < kend ? (k + 1 < kend ? 16 : 8) : 0;
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const bool ok = (aok >> i) & 1u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(adst + stage_off + i * RSTEP * kPitchK * 8),
+                   "l"(ok ? asrc[i] + k : asrc[i]), "r"(ok ? sz : 0));
+    }
+    const double* b = bsrc + k;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const bool ok = (bok >> i) & 1u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(bdst + stage_off + i * RSTEP * kPitchK * 8),
+                   "l"(ok ? b : bsrc), "r"(ok ? sz : 0));
+      b += bstep;
+    }
+  }
+};
+
 template <int MT, int VEC>
 __global__ void __launch_bounds__(kThreads, 2)
     gemm_tn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
@@ -135,11 +193,16 @@ __global__ void __launch_bounds__(kThreads, 2)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
 
+  TnLoader2<MT> ld2;
+  if constexpr (VEC == 2) ld2.init(X, ldx, C, ldc, M, N, n0, dyn, smem, smem + Cfg::A_ELEMS);
 #pragma unroll
   for (int s = 0; s < kStages - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * Cfg::STAGE;
-      tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + s * kBK, kend, dyn);
+      if constexpr (VEC == 2)
+        ld2.load((uint32_t)(s * Cfg::STAGE * 8), kbeg + s * kBK, kend);
+      else
+        tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + s * kBK, kend, dyn);
     }
     cp_async_commit();
   }
@@ -151,8 +214,11 @@ __global__ void __launch_bounds__(kThreads, 2)
       const int ls = kt + kStages - 1;
       if (ls < nk) {
         double* st = smem + (ls % kStages) * Cfg::STAGE;
-        tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + ls * kBK,
-                               kend, dyn);
+        if constexpr (VEC == 2)
+          ld2.load((uint32_t)((ls % kStages) * Cfg::STAGE * 8), kbeg + ls * kBK, kend);
+        else
+          tn_load_stage<MT, VEC>(st, st + Cfg::A_ELEMS, X, ldx, C, ldc, M, N, n0, kbeg + ls * kBK,
+                                 kend, dyn);
       }
       cp_async_commit();
     }
@@ -308,6 +374,69 @@ __device__ __forceinline__ void nn_load_stage(double* sA, double* sB, const doub
   }
 }
 
+// Aligned fast path of nn_load_stage (addresses and bounds resolved once).
+template <int BNT>
+struct NnLoader2 {
+  static constexpr int BM = 64;
+  static constexpr int ACH = BM / 2;                 // 16-byte chunks per k-row of X
+  static constexpr int AR = kThreads / ACH;          // k-rows per pass
+  static constexpr int NA = kBK / AR;
+  static constexpr int BCH = kBK / 2;                // chunks per n-row of Y
+  static constexpr int BR = kThreads / BCH;          // n-rows per pass
+  static constexpr int NB = BNT / BR;
+  const double* asrc;
+  int64_t astep;
+  const double* bsrc;
+  int64_t bstep;
+  uint32_t adst, bdst;
+  int akr, bkc, K, asz;
+  bool aok;
+  unsigned bok;
+  __device__ __forceinline__ void init(const double* X, int64_t ldx, const double* Y, int64_t ldy, int M, int N,
+                                       int K_, int m0, int n0, const double* sA, const double* sB, int pm) {
+    const int tid = threadIdx.x;
+    K = K_;
+    akr = tid / ACH;
+    const int mc = (tid % ACH) * 2;
+    aok = m0 + mc < M;
+    asz = m0 + mc + 1 < M ? 16 : 8;  // odd M: the last pair is half valid
+    asrc = X + (int64_t)akr * ldx + m0 + mc;
+    astep = (int64_t)AR * ldx;
+    adst = smem_u32(sA + akr * pm + mc);
+    const int br = tid / BCH;
+    bkc = (tid % BCH) * 2;
+    bok = 0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) bok |= ((n0 + br + BR * i) < N ? 1u : 0u) << i;
+    bsrc = Y + (int64_t)(n0 + br) * ldy + bkc;
+    bstep = (int64_t)BR * ldy;
+    bdst = smem_u32(sB + br * kPitchK + bkc);
+  }
+  // A chunk needs m < M and k < K.
+  __device__ __forceinline__ void load(uint32_t stage_off, int pm, int k0, const double* X,
+                                       const double* Y) const {
+    const double* a = asrc + (int64_t)k0 * (astep / AR);
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+      const int k = k0 + akr + AR * i;
+      const bool ok = aok && k < K;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(adst + stage_off + i * AR * pm * 8),
+                   "l"(ok ? a : X), "r"(ok ? asz : 0));
+      a += astep;
+    }
+    const int k = k0 + bkc;
+    const int sz = k < K ? (k + 1 < K ? 16 : 8) : 0;
+    const double* b = bsrc + k0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const bool ok = (bok >> i) & 1u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(bdst + stage_off + i * BR * kPitchK * 8),
+                   "l"(ok ? b : Y), "r"(ok ? sz : 0));
+      b += bstep;
+    }
+  }
+};
+
 // CTA tile 64 m x BN n; 4 warps = 2 (m) x 2 (n); warp tile 32 m x BN/2 n.
 template <int VEC, int BNT>
 __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
@@ -343,11 +472,16 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
 #pragma unroll
       for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
 
+  NnLoader2<BNT> ld2;
+  if constexpr (VEC == 2) ld2.init(X, ldx, Y, ldy, M, N, K, m0, n0, smem, smem + Cfg::A_ELEMS, Cfg::PM);
 #pragma unroll
   for (int s = 0; s < kStagesNN - 1; ++s) {
     if (s < nk) {
       double* st = smem + s * Cfg::STAGE;
-      nn_load_stage<VEC, BNT>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
+      if constexpr (VEC == 2)
+        ld2.load((uint32_t)(s * Cfg::STAGE * 8), Cfg::PM, s * kBK, X, Y);
+      else
+        nn_load_stage<VEC, BNT>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, s * kBK);
     }
     cp_async_commit();
   }
@@ -358,7 +492,10 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
       const int ls = kt + kStagesNN - 1;
       if (ls < nk) {
         double* st = smem + (ls % kStagesNN) * Cfg::STAGE;
-        nn_load_stage<VEC, BNT>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
+        if constexpr (VEC == 2)
+          ld2.load((uint32_t)((ls % kStagesNN) * Cfg::STAGE * 8), Cfg::PM, ls * kBK, X, Y);
+        else
+          nn_load_stage<VEC, BNT>(st, st + Cfg::A_ELEMS, X, ldx, Y, ldy, M, N, K, m0, n0, ls * kBK);
       }
       cp_async_commit();
     }
