@@ -151,55 +151,82 @@ __global__ void apply_moves_kernel(double* X, int64_t ld, int64_t rows, int64_t 
 // ------------------------------------------------------------ sample update
 // B_next = [S12 - S11 R11^{-1} R12 ; S22]  (sketch.py:132-149).
 // su_prep (one CTA): the R11 diagonal guard (randomized.py:133-135) and
-// M = S11 R11^{-1} by forward substitution, M R11 = S11 (column c of M from
-// columns < c; M is upper triangular like S11).  The nt-column part is then
-// one DMMA GEMM, B_top = S12 - M R12, plus a copy of S22.
-constexpr int kSuThreads = 128;
+// M = S11 R11^{-1} (sketch.py:132-149: the sample update's S11 R11^{-1}),
+// M R11 = S11 with M upper triangular like S11.  One warp per row i of M,
+// right-looking: lane l keeps the running sums p[c] = sum_{l' < c} M(i,l') R(l',c)
+// for c = l + 32q; each step finishes M(i,c) = (S11(i,c) - p[c]) / R(c,c) in
+// the owning lane, broadcasts it with one shuffle and folds it into the
+// remaining sums (4 FMAs per lane) -- ~1 shuffle + 1 division per step
+// instead of a warp reduction.  Every CTA also evaluates the reference's
+// diagonal test (randomized.py:217-219); CTA 0 records the stop.
+constexpr int kSuThreads = 256;
+constexpr int kSuRows = kSuThreads / 32;
 __global__ void __launch_bounds__(kSuThreads, 1)
     su_prep_kernel(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, double* Mout, int64_t ldm,
-                   sqr_status* st) {
-  extern __shared__ __align__(16) double X[];  // M in the upper triangle, R11 (transposed) in the lower
-  __shared__ double rdiag[144];
-  __shared__ int ok;
+                   int bmax, sqr_status* st) {
+  extern __shared__ __align__(16) double Rs[];  // R11 transposed: Rs[l * P + c] = R(l, c), P odd
+  __shared__ double rdiag[128];
+  __shared__ double wmin[kSuRows];
   if (st->stop) return;
   const int bh = st->sample_achieved;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int P = bh | 1;
-  if (tid == 0) {
-    const double d0 = fabs(R[0]);
-    double dmin = d0;
-    for (int i = 1; i < bh; ++i) dmin = fmin(dmin, fabs(R[(int64_t)i * ldr + i]));
-    ok = (bh > 0) && (dmin > 0x1p-52 * d0);
-    if (!ok) {
+  double dm = INFINITY;
+  for (int i = tid; i < bh; i += kSuThreads) {
+    const double d = R[(int64_t)i * ldr + i];
+    rdiag[i] = d;
+    if (i > 0) dm = fmin(dm, fabs(d));
+  }
+  for (int e = tid; e < bh * bh; e += kSuThreads) {
+    const int l = e % bh, c = e / bh;  // coalesced along l
+    if (l < c) Rs[l * P + c] = R[(int64_t)c * ldr + l];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dm = fmin(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+  if (lane == 0) wmin[warp] = dm;
+  __syncthreads();
+  double dmin = wmin[0];
+  for (int w = 1; w < kSuRows; ++w) dmin = fmin(dmin, wmin[w]);
+  const double d0 = bh > 0 ? fabs(rdiag[0]) : 0.0;
+  dmin = fmin(dmin, d0);
+  const bool ok = (bh > 0) && (dmin > 0x1p-52 * d0);
+  if (!ok) {
+    if (blockIdx.x == 0 && tid == 0) {
       st->stop = 1;
       st->reason = SQR_STOP_R11_SINGULAR;
     }
+    return;
   }
-  for (int e = tid; e < bh * bh; e += kSuThreads) {
-    const int r = e % bh, c = e / bh;
-    if (r <= c) X[c * P + r] = Bf[(int64_t)c * ldbf + r];          // S11(r, c)
-    if (r < c) X[r * P + c] = R[(int64_t)c * ldr + r];             // R11(r, c) at (c, r)
-    if (r == c) rdiag[r] = R[(int64_t)c * ldr + r];
+  const int i = blockIdx.x * kSuRows + warp;
+  if (i >= bmax) return;
+  double p[4], sv[4], mv[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = lane + 32 * q;
+    p[q] = 0.0;
+    mv[q] = 0.0;
+    sv[q] = (i < bh && c >= i && c < bh) ? Bf[(int64_t)c * ldbf + i] : 0.0;
   }
-  __syncthreads();
-  if (!ok) return;
-  // thread i owns row i of M: M(i, c) = (S11(i, c) - sum_{l=i}^{c-1} M(i, l) R11(l, c)) / R11(c, c)
-  for (int i = tid; i < bh; i += kSuThreads) {
+  if (i < bh) {
     for (int c = i; c < bh; ++c) {
-      double s0 = 0.0, s1 = 0.0;
-      int l = i;
-      for (; l + 2 <= c; l += 2) {
-        s0 = fma(X[l * P + i], X[l * P + c], s0);
-        s1 = fma(X[(l + 1) * P + i], X[(l + 1) * P + c], s1);
+      const int qc = c >> 5, lc = c & 31;
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q == qc) v = (sv[q] - p[q]) / rdiag[c];  // meaningful in lane lc
+      v = __shfl_sync(0xffffffffu, v, lc);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int cc = lane + 32 * q;
+        if (q == qc && lane == lc) mv[q] = v;
+        if (cc > c && cc < bh) p[q] = fma(v, Rs[c * P + cc], p[q]);
       }
-      if (l < c) s0 = fma(X[l * P + i], X[l * P + c], s0);
-      X[c * P + i] = (X[c * P + i] - (s0 + s1)) / rdiag[c];
     }
   }
-  __syncthreads();
-  for (int e = tid; e < bh * bh; e += kSuThreads) {
-    const int r = e % bh, c = e / bh;
-    Mout[(int64_t)c * ldm + r] = r <= c ? X[c * P + r] : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = lane + 32 * q;
+    if (c < bmax) Mout[(int64_t)c * ldm + i] = (i < bh && c >= i && c < bh) ? mv[q] : 0.0;
   }
 }
 
@@ -297,6 +324,10 @@ int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm
 int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
                   int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s) {
   if (nt <= 0) return SQR_OK;
+  if (bmax > 128) {
+    set_error("sample_update: block size %lld > 128", (long long)bmax);
+    return SQR_EINVAL;
+  }
   const int64_t smem = (bmax | 1) * bmax * 8;
   static int64_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
@@ -305,7 +336,8 @@ int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, 
   }
   {
     ProfScope ps(kTagSampleUpd, s);
-    su_prep_kernel<<<1, kSuThreads, smem, s>>>(Bf, ldbf, R, ldr, mbuf, bmax, st);
+    su_prep_kernel<<<(unsigned)cdiv(bmax, (int64_t)kSuRows), kSuThreads, smem, s>>>(Bf, ldbf, R, ldr, mbuf, bmax,
+                                                                                  (int)bmax, st);
     SQR_LAUNCH("su_prep_kernel");
   }
   // B_top = S12 - M R12 with the block size read on the device (== bmax

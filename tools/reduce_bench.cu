@@ -49,7 +49,23 @@ __global__ void __launch_bounds__(kT, 1) step_kernel(unsigned* ctr, double* part
     const int par = it & 1;
     // partials: value v of CTA g
     if (tid < L) part[((size_t)par * 256 + tid) * G + g] = acc + tid + g;
-    b.sync();
+    if (MODE == 5) {
+      cg::cluster_group cl = cg::this_cluster();
+      // arrive: CTA-level sync, cluster-level sync, leader does the global atomic
+      __syncthreads();
+      cl.sync();
+      b.target += gridDim.x / CL;
+      if (cl.block_rank() == 0 && tid == 0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(ctr) : "memory");
+        while ((int)(ld_rlx(ctr) - b.target) < 0) {
+        }
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      }
+      cl.sync();
+    } else {
+      b.sync();
+    }
     if (MODE == 0) {
       for (int v0 = 0; v0 < L; v0 += kT / 4) {
         const int v = v0 + (tid >> 2), q = tid & 3;
@@ -114,6 +130,8 @@ __global__ void __launch_bounds__(kT, 1) step_kernel(unsigned* ctr, double* part
       b.sync();
       if (tid < L) vals[tid] = __ldcg(red + par * 256 + tid);
       __syncthreads();
+    } else if (MODE == 5) {
+      // (no reduction) barrier variant measured below
     } else if (MODE == 4) {
       if (tid < L) vals[tid] = __ldcg(part + (size_t)par * 256 * G + tid);
       __syncthreads();
@@ -194,6 +212,10 @@ int main() {
       printf("G=%d L=%3d  A(all read) %.2f  C(2 barriers) %.2f  D(barrier) %.2f  E(same %d) %.2f us\n", G, L,
              run<0, 1>(G, L, iters, ctr, part, red, sink), run<2, 1>(G, L, iters, ctr, part, red, sink),
              run<3, 1>(G, L, iters, ctr, part, red, sink), L, run<4, 1>(G, L, iters, ctr, part, red, sink));
+      printf("      H(barrier hier) cl2 %.2f", run<5, 2>(G, L, iters, ctr, part, red, sink));
+      if (G <= 132) printf(" cl4 %.2f", run<5, 4>(G, L, iters, ctr, part, red, sink));
+      if (G <= 120) printf(" cl8 %.2f", run<5, 8>(G, L, iters, ctr, part, red, sink));
+      printf("\n");
       printf("      B cluster2 %.2f", run<1, 2>(G, L, iters, ctr, part, red, sink));
       if (G <= 132) printf("  cluster4 %.2f", run<1, 4>(G, L, iters, ctr, part, red, sink));
       if (G <= 120) printf("  cluster8 %.2f", run<1, 8>(G, L, iters, ctr, part, red, sink));
