@@ -221,6 +221,8 @@ int panel_block(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, dou
 int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
              double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s,
              int64_t c0 = 0);
+int build_t_fast(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
+                 const int32_t* gate, cudaStream_t s);
 int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
             const int32_t* gate, cudaStream_t s);
 int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed, uint64_t offset,

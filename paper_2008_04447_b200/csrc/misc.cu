@@ -130,9 +130,20 @@ __global__ void apply_moves_kernel(double* X, int64_t ld, int64_t rows, int64_t 
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const int64_t r0 = (int64_t)blockIdx.x * kMoveRows;
   const int64_t r = r0 + lane;
-  for (int m = warp; m < nm; m += nw) {
-    const int src = moves[2 * m + 1];
-    buf[m * kMoveRows + lane] = (r < rows) ? X[(col0 + src) * ld + r] : 0.0;
+  // 8 moves per thread in flight (the loads are independent; storing each to
+  // shared memory before issuing the next would serialise on HBM latency)
+  for (int m0 = warp; m0 < nm; m0 += 8 * nw) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int m = m0 + u * nw;
+      v[u] = (m < nm && r < rows) ? __ldcs(X + (col0 + moves[2 * m + 1]) * ld + r) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int m = m0 + u * nw;
+      if (m < nm) buf[m * kMoveRows + lane] = v[u];
+    }
   }
   __syncthreads();
   for (int m = warp; m < nm; m += nw) {
@@ -177,9 +188,20 @@ __global__ void __launch_bounds__(kSuThreads, 1)
     rdiag[i] = d;
     if (i > 0) dm = fmin(dm, fabs(d));
   }
-  for (int e = tid; e < bh * bh; e += kSuThreads) {
-    const int l = e % bh, c = e / bh;  // coalesced along l
-    if (l < c) Rs[l * P + c] = R[(int64_t)c * ldr + l];
+  for (int e0 = tid; e0 < bh * bh; e0 += 8 * kSuThreads) {  // 8 loads in flight per thread
+    double rv[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kSuThreads;
+      const int l = e % bh, c = e / bh;  // coalesced along l
+      rv[u] = (e < bh * bh && l < c) ? R[(int64_t)c * ldr + l] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kSuThreads;
+      const int l = e % bh, c = e / bh;
+      if (e < bh * bh && l < c) Rs[l * P + c] = rv[u];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dm = fmin(dm, __shfl_xor_sync(0xffffffffu, dm, o));

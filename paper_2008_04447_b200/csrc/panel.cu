@@ -521,94 +521,6 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
   }
 }
 
-// T from G = Y^T Y and taus (one CTA), householder.py:52-61.
-//  1. 32 x 32 diagonal blocks, one warp each, by the reference recurrence
-//     T[:c, c] = -tau_c T[:c, :c] G[:c, c] (lane i keeps row i of its block
-//     in registers);
-//  2. blocks merged left to right with the composition rule of
-//     wy_compose (householder.py:94-104): T_AB = -T_AA G_AB T_BB.
-// tau = 0 (identity / padded reflectors) gives zero rows and columns, as in
-// the recurrence.
-constexpr int kTThreads = 256;
-constexpr int kTB = 32;
-__global__ void __launch_bounds__(kTThreads, 1)
-    build_t_kernel(const double* Gm, int64_t ldg, const double* taus, int j, double* T, int64_t ldt,
-                   const int32_t* gate) {
-  extern __shared__ __align__(16) double smt[];
-  if (gate && *gate) return;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int P = j | 1;
-  // One j x j array: T in the upper triangle, the symmetric G in the strict
-  // lower one (G(r, c), r < c, stored at M(c, r)).  M(r, c) = M[c * P + r].
-  double* M = smt;
-  double* Xs = M + (size_t)j * P;  // j x kTB scratch
-  for (int e = tid; e < j * j; e += kTThreads) {  // coalesced read of G(r, c)
-    const int r = e % j, c = e / j;
-    const double gv = Gm[(int64_t)c * ldg + r];
-    if (r < c) M[r * P + c] = gv;   // strict lower half of M holds G
-    if (r <= c) M[c * P + r] = 0.0; // upper half (T) starts at zero
-  }
-  __syncthreads();
-  const int nb = (j + kTB - 1) / kTB;
-  if (warp < nb) {
-    const int o = warp * kTB, bs = min(kTB, j - o);
-    double trow[kTB];
-#pragma unroll
-    for (int l = 0; l < kTB; ++l) trow[l] = 0.0;
-    for (int c = 0; c < bs; ++c) {
-      const double tc = taus[o + c];
-      double s = 0.0, s2 = 0.0;
-#pragma unroll
-      for (int l = 0; l < kTB; l += 2) {
-        if (l >= lane && l < c) s = fma(trow[l], M[(o + l) * P + o + c], s);  // G(o+l, o+c)
-        if (l + 1 >= lane && l + 1 < c) s2 = fma(trow[l + 1], M[(o + l + 1) * P + o + c], s2);
-      }
-      s += s2;
-      const double v = (lane < c) ? -tc * s : (lane == c ? tc : 0.0);
-#pragma unroll
-      for (int l = 0; l < kTB; ++l)
-        if (l == c) trow[l] = v;
-    }
-    __syncwarp();
-    if (lane < bs) {
-#pragma unroll
-      for (int l = 0; l < kTB; ++l)
-        if (l >= lane && l < bs) M[(o + l) * P + o + lane] = trow[l];  // T(o+lane, o+l)
-    }
-  }
-  __syncthreads();
-  for (int a = kTB; a < j; a += kTB) {
-    const int bsz = min(kTB, j - a);
-    // X = G[0:a, a:a+bsz] T[a:a+bsz, a:a+bsz]   (T_BB upper triangular)
-    for (int e = tid; e < a * bsz; e += kTThreads) {
-      const int i = e % a, c = e / a;
-      double s = 0.0;
-      for (int l = 0; l <= c; ++l) s = fma(M[i * P + a + l], M[(a + c) * P + a + l], s);
-      Xs[c * P + i] = s;
-    }
-    __syncthreads();
-    // T[0:a, a:a+bsz] = -T[0:a, 0:a] X           (T_AA upper triangular)
-    for (int e = tid; e < a * bsz; e += kTThreads) {
-      const int i = e % a, c = e / a;
-      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;  // 4 chains for ILP
-      int l = i;
-      for (; l + 4 <= a; l += 4) {
-        s0 = fma(M[l * P + i], Xs[c * P + l], s0);
-        s1 = fma(M[(l + 1) * P + i], Xs[c * P + l + 1], s1);
-        s2 = fma(M[(l + 2) * P + i], Xs[c * P + l + 2], s2);
-        s3 = fma(M[(l + 3) * P + i], Xs[c * P + l + 3], s3);
-      }
-      for (; l < a; ++l) s0 = fma(M[l * P + i], Xs[c * P + l], s0);
-      M[(a + c) * P + i] = -((s0 + s1) + (s2 + s3));
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < j * j; e += kTThreads) {
-    const int r = e % j, c = e / j;
-    T[(int64_t)c * ldt + r] = r <= c ? M[c * P + r] : 0.0;
-  }
-}
-
 }  // namespace
 
 int64_t panel_workspace(int64_t w) {
@@ -735,17 +647,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
 
 int build_t(const double* Gm, int64_t ldg, const double* taus, int64_t j, double* T, int64_t ldt,
             const int32_t* gate, cudaStream_t s) {
-  if (j <= 0) return SQR_OK;
-  const int64_t smem = ((int64_t)(j | 1) * j + (int64_t)(j | 1) * kTB) * 8;
-  static int configured = 0;
-  if (smem > configured) {
-    SQR_CUDA(cudaFuncSetAttribute(build_t_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = (int)smem;
-  }
-  ProfScope ps(kTagBuildT, s);
-  build_t_kernel<<<1, kTThreads, smem, s>>>(Gm, ldg, taus, (int)j, T, ldt, gate);
-  SQR_LAUNCH("build_t_kernel");
-  return SQR_OK;
+  return build_t_fast(Gm, ldg, taus, j, T, ldt, gate, s);  // build_t.cu
 }
 
 }  // namespace sqr

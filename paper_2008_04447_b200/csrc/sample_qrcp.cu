@@ -115,9 +115,18 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
 
   if (g == 0 && tid == 0) a.st->nmoves = 0;
   const int nld = a.reg_spill ? min(ncols, a.cap) : ncols;
-  for (int64_t e = tid; e < (int64_t)nld * ell; e += kSqThreads) {
-    const int lc = (int)(e / ell), r = (int)(e % ell);
-    colp(lc)[r] = a.B[(int64_t)(col0 + lc) * a.ldb + r];
+  for (int64_t e0 = tid; e0 < (int64_t)nld * ell; e0 += 8 * kSqThreads) {  // 8 loads in flight
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = e0 + u * kSqThreads;
+      v[u] = e < (int64_t)nld * ell ? a.B[(int64_t)(col0 + (int)(e / ell)) * a.ldb + (int)(e % ell)] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t e = e0 + u * kSqThreads;
+      if (e < (int64_t)nld * ell) colp((int)(e / ell))[(int)(e % ell)] = v[u];
+    }
   }
   double xs[kSpillPerWarp][kMaxRowsPerLane];  // this warp's spill columns (reg mode)
 #pragma unroll
