@@ -16,6 +16,7 @@
 // with the reference's 2^-40 guard and exact recompute.
 #include <float.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 
@@ -661,6 +662,320 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
   }
 }
 
+// ---------------------------------------------------------------------------
+// Thread-per-column variant (nt <= 256 G, ell <= 144): thread t of CTA g owns
+// sample column 256 g + t for the whole launch.  Rows [RS, ell) (the last 64,
+// RS = ell - 64) live in REGISTERS, rows [0, RS) in shared memory (row-major
+// over the 256 columns: conflict-free), so the dot / update / downdate of a
+// step are thread-local and touch shared memory only for the first RS rows.
+// The reflector is kept as a full-length vector yf (zeros above the pivot row)
+// so the register loop needs no predicate.  The update is applied at once
+// (no deferred pass), the CTA candidate's updated column is published by its
+// owner, and one grid barrier per step remains.  Same arithmetic and the same
+// downdate guard / exact recompute / tie rule as sample_qrcp_kernel.
+constexpr int kRT = 256;
+constexpr int kRR = 64;  // register rows
+
+struct RegArgs {
+  const double* B;
+  int64_t ldb;
+  int ell, nt, bb, first, RS;
+  double* Bf;
+  int64_t ldbf;
+  int64_t* lperm;
+  int32_t* moves;
+  double* taus;
+  sqr_status* st;
+  unsigned* bar;
+  double2* cand;
+  double* ccol;
+  double* psum;
+  double* pmax;
+  unsigned long long* trace;
+};
+
+__device__ __forceinline__ void add_move(const RegArgs& a, int dst, int src) {
+  const int slot = atomicAdd(&a.st->nmoves, 1);
+  a.moves[2 * slot] = dst;
+  a.moves[2 * slot + 1] = src;
+}
+
+__global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
+  extern __shared__ __align__(16) double sm[];
+  double* cs = sm;                     // [RS][kRT]
+  double* yf = cs + (size_t)a.RS * kRT;  // [ell]
+  __shared__ double wv_s[kRT / 32];
+  __shared__ int wp_s[kRT / 32], wl_s[kRT / 32];
+  __shared__ double sred[32];
+  struct Bcast {
+    int go, pc;
+    double beta, tau;
+  };
+  __shared__ Bcast bc_s;
+  if (a.st->stop) return;
+  GridBarrier gb;
+  gb.init(a.bar);
+  const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int ell = a.ell, RS = a.RS;
+  const int col = g * kRT + tid;
+  const bool own = col < a.nt;
+  if (g == 0 && tid == 0) a.st->nmoves = 0;
+  for (int r = ell + tid; r < RS + kRR; r += kRT) yf[r] = 0.0;  // register rows beyond ell (ell < 64)
+
+  // ---- load my column: rows [0, RS) to shared memory, [RS, ell) to registers
+  double xr[kRR];
+  {
+    const double* src = a.B + (int64_t)col * a.ldb;
+    for (int r = 0; r < RS; ++r) cs[r * kRT + tid] = own ? src[r] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kRR; ++q) xr[q] = (own && RS + q < ell) ? src[RS + q] : 0.0;
+  }
+  double nsq = 0.0;
+  {
+    double s0 = 0.0, s1 = 0.0;
+    for (int r = 0; r < RS; ++r) {
+      const double v = cs[r * kRT + tid];
+      s0 = fma(v, v, s0);
+    }
+#pragma unroll
+    for (int q = 0; q < kRR; q += 2) {
+      s0 = fma(xr[q], xr[q], s0);
+      s1 = fma(xr[q + 1], xr[q + 1], s1);
+    }
+    nsq = s0 + s1;
+  }
+  double rsq = nsq;
+  int pos = own ? col : -1;
+  double cbv = own ? nsq : -1.0;
+  int cbp = own ? col : INT_MAX;
+  int cbl = own ? tid : -1;
+  {
+    const double s = block_sum(own ? nsq : 0.0, sred);
+    double mx = own ? nsq : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sred[warp] = mx;
+    __syncthreads();
+    if (tid == 0) {
+      for (int i = 1; i < (kRT >> 5); ++i) mx = fmax(mx, sred[i]);
+      mx = fmax(mx, sred[0]);
+      a.psum[g] = s;
+      a.pmax[g] = mx;
+    }
+  }
+  gb.sync();
+  double total = 0.0, gmax = 0.0;
+  for (int i = 0; i < G; ++i) {
+    total += __ldcg(a.psum + i);
+    gmax = fmax(gmax, __ldcg(a.pmax + i));
+  }
+  const double fro = sqrt(total);
+  const double rank_floor_sq = (kRankFloor * fro) * (kRankFloor * fro);
+  const double sample_floor = a.first ? kSampleFloor * kSampleFloor * gmax : __ldcg(&a.st->floor_sq);
+  if (a.nt == 0 || gmax <= sample_floor) {
+    if (g == 0 && tid == 0) {
+      if (a.first) a.st->floor_sq = sample_floor;
+      a.st->stop = 1;
+      a.st->reason = SQR_STOP_SAMPLE_FLOOR;
+      a.st->sample_achieved = 0;
+    }
+    return;
+  }
+  if (g == 0 && tid == 0 && a.first) a.st->floor_sq = sample_floor;
+
+  // value of row r of my column (r < RS: shared memory; else a register select)
+  auto rowval = [&](int r) -> double {
+    if (r < RS) return cs[r * kRT + tid];
+    double v = 0.0;
+#pragma unroll
+    for (int q = 0; q < kRR; ++q)
+      if (RS + q == r) v = xr[q];
+    return v;
+  };
+  // CTA candidate for step jn -> publish (value, position, column rows jn..)
+  auto publish = [&](int jn) {
+    warp_argmax(cbv, cbp, cbl);
+    if (lane == 0) {
+      wv_s[warp] = cbv;
+      wp_s[warp] = cbp;
+      wl_s[warp] = cbl;
+    }
+    __syncthreads();
+    double v = lane < (kRT >> 5) ? wv_s[lane] : -1.0;
+    int p = lane < (kRT >> 5) ? wp_s[lane] : INT_MAX;
+    int l = lane < (kRT >> 5) ? wl_s[lane] : -1;
+    warp_argmax(v, p, l);
+    const int par = jn & 1;
+    if (tid == 0) a.cand[par * G + g] = make_double2(v, __longlong_as_double((long long)p));
+    if (l >= 0 && tid == __shfl_sync(0xffffffffu, l, 0)) {
+      double* dst = a.ccol + ((size_t)par * G + g) * ell;
+      for (int r = jn; r < RS; ++r) dst[r] = cs[r * kRT + tid];
+#pragma unroll
+      for (int q = 0; q < kRR; ++q)
+        if (RS + q >= jn && RS + q < ell) dst[RS + q] = xr[q];
+    }
+  };
+  // global winner of step jn + its reflector into yf (warp 0, lane 0 waited)
+  auto winner = [&](int jn) {
+    const int par = jn & 1;
+    double bv = -1.0;
+    int bp = INT_MAX, bl = -1;
+    {
+      double2 rec[5];
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int i = lane + 32 * k;
+        rec[k] = i < G ? __ldcg(a.cand + par * G + i) : make_double2(-1.0, __longlong_as_double((long long)INT_MAX));
+      }
+#pragma unroll
+      for (int k = 0; k < 5; ++k) {
+        const int p = (int)__double_as_longlong(rec[k].y);
+        if (better(rec[k].x, p, bv, bp)) {
+          bv = rec[k].x;
+          bp = p;
+          bl = lane + 32 * k;
+        }
+      }
+    }
+    warp_argmax(bv, bp, bl);
+    const int len = ell - jn;
+    double x[kMaxRowsPerLane];
+    double s1 = 0.0, nrm = 0.0, beta = 0.0, tau = 0.0, y0 = 1.0;
+    const bool go = bv > rank_floor_sq;  // reference.py:123-124
+    if (go) {
+      const double* u = a.ccol + ((size_t)par * G + bl) * ell + jn;
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = lane + 32 * i;
+        x[i] = r < len ? __ldcg(u + r) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i)
+        if (lane + 32 * i >= 1) s1 = fma(x[i], x[i], s1);
+      s1 = warp_sum(s1);
+      const double u0 = __shfl_sync(0xffffffffu, x[0], 0);
+      nrm = sqrt(fma(u0, u0, s1));
+      if (nrm != 0.0) {
+        beta = (u0 >= 0.0 ? -1.0 : 1.0) * nrm;
+        y0 = u0 - beta;
+        tau = 2.0 / (1.0 + s1 / (y0 * y0));
+      }
+      for (int r = lane; r < jn; r += 32) yf[r] = 0.0;
+#pragma unroll
+      for (int i = 0; i < kMaxRowsPerLane; ++i) {
+        const int r = lane + 32 * i;
+        if (r < len) yf[jn + r] = (r == 0) ? 1.0 : (nrm != 0.0 ? x[i] / y0 : 0.0);
+      }
+    }
+    if (lane == 0) {
+      bc_s.go = go;
+      bc_s.pc = bp;
+      bc_s.beta = beta;
+      bc_s.tau = tau;
+    }
+  };
+
+  publish(0);
+  gb.sync();
+  if (warp == 0) winner(0);
+  __syncthreads();
+
+  int achieved = 0;
+  for (int j = 0; j < a.bb; ++j) {
+    SQR_TRACE(a.trace, 8 * j + 0);
+    if (!bc_s.go) break;  // uniform across the grid
+    const int pc = bc_s.pc;
+    const double beta = bc_s.beta, tau = bc_s.tau;
+    if (g == 0 && tid == 0) a.taus[j] = tau;
+    cbv = -1.0;
+    cbp = INT_MAX;
+    cbl = -1;
+    if (pos == pc) {
+      // the pivot: R part rows < j, beta, reflector tail -> Bf column j
+      double* bfj = a.Bf + (int64_t)j * a.ldbf;
+      for (int r = 0; r < min(j, RS); ++r) bfj[r] = cs[r * kRT + tid];
+#pragma unroll
+      for (int q = 0; q < kRR; ++q)
+        if (RS + q < j) bfj[RS + q] = xr[q];
+      bfj[j] = beta;
+      for (int r = j + 1; r < ell; ++r) bfj[r] = yf[r];
+      a.lperm[j] = col;
+      if (col != j) add_move(a, j, col);
+      pos = -1;
+    } else if (pos >= 0) {
+      const int pn = (pos == j) ? pc : pos;  // the column at position j moves to pc
+      pos = pn;
+      double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+      for (int r = j; r < RS; ++r) d0 = fma(yf[r], cs[r * kRT + tid], d0);
+#pragma unroll
+      for (int q = 0; q < kRR; q += 4) {
+        d1 = fma(yf[RS + q], xr[q], d1);
+        d2 = fma(yf[RS + q + 1], xr[q + 1], d2);
+        d3 = fma(yf[RS + q + 2], xr[q + 2], d3);
+        d0 = fma(yf[RS + q + 3], xr[q + 3], d0);
+      }
+      const double wvv = tau * ((d0 + d1) + (d2 + d3));
+      for (int r = j; r < RS; ++r) cs[r * kRT + tid] = fma(-yf[r], wvv, cs[r * kRT + tid]);
+#pragma unroll
+      for (int q = 0; q < kRR; ++q) xr[q] = fma(-yf[RS + q], wvv, xr[q]);
+      const double rj = rowval(j);
+      double ns = nsq - rj * rj;
+      if (ns < kNormGuard * rsq) {
+        double e0 = 0.0, e1 = 0.0;
+        for (int r = j + 1; r < RS; ++r) {
+          const double v = cs[r * kRT + tid];
+          e0 = fma(v, v, e0);
+        }
+#pragma unroll
+        for (int q = 0; q < kRR; ++q)
+          if (RS + q > j) e1 = fma(xr[q], xr[q], e1);
+        ns = e0 + e1;
+        rsq = ns;
+      } else {
+        ns = fmax(ns, 0.0);
+      }
+      nsq = ns;
+      cbv = ns;
+      cbp = pn;
+      cbl = tid;
+    }
+    achieved = j + 1;
+    if (j + 1 < a.bb) {
+      publish(j + 1);
+      SQR_TRACE(a.trace, 8 * j + 2);
+      gb.arrive();
+      SQR_TRACE(a.trace, 8 * j + 3);
+      if (warp == 0) {
+        if (lane == 0) gb.wait_lane0();
+        if (lane == 0) SQR_TRACE(a.trace, 8 * j + 6);
+        __syncwarp();
+        winner(j + 1);
+      }
+      __syncthreads();
+      SQR_TRACE(a.trace, 8 * j + 4);
+    }
+  }
+  __syncthreads();
+  // remaining columns go to their final positions
+  if (pos >= 0) {
+    double* dst = a.Bf + (int64_t)pos * a.ldbf;
+    for (int r = 0; r < RS; ++r) dst[r] = cs[r * kRT + tid];
+#pragma unroll
+    for (int q = 0; q < kRR; ++q)
+      if (RS + q < ell) dst[RS + q] = xr[q];
+    a.lperm[pos] = col;
+    if (pos != col) add_move(a, pos, col);
+  }
+  if (g == 0 && tid == 0) {
+    a.st->sample_achieved = achieved;
+    if (achieved == 0) {
+      a.st->stop = 1;
+      a.st->reason = SQR_STOP_SAMPLE_RANK;
+    }
+  }
+}
+
 }  // namespace
 
 struct SampleWorkspace {
@@ -685,6 +1000,48 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     return SQR_EINVAL;
   }
   const int sms = sm_count();
+  static const bool no_reg = getenv("SQR_NO_REGSAMPLE") != nullptr;
+  if (!no_reg && ell <= 144 && nt <= (int64_t)std::min(sms, 148) * kRT) {
+    RegArgs a{};
+    a.B = B;
+    a.ldb = ldb;
+    a.ell = (int)ell;
+    a.nt = (int)nt;
+    a.bb = (int)bb;
+    a.first = first;
+    a.RS = (int)std::max<int64_t>(0, ell - kRR);
+    a.Bf = Bf;
+    a.ldbf = ldbf;
+    a.lperm = lperm;
+    a.moves = moves;
+    a.taus = taus;
+    a.st = st;
+    char* p = static_cast<char*>(ws);
+    a.bar = reinterpret_cast<unsigned*>(p);
+    p += 64;
+    a.cand = reinterpret_cast<double2*>(p);
+    p += 2 * 148 * 16;
+    a.ccol = reinterpret_cast<double*>(p);
+    p += 2 * 148 * ell * 8;
+    a.psum = reinterpret_cast<double*>(p);
+    p += 148 * 8;
+    a.pmax = reinterpret_cast<double*>(p);
+    a.trace = g_trace_host_ptr;
+    const int G = (int)std::max<int64_t>(1, cdiv(nt, (int64_t)kRT));
+    const int smem = (int)(((int64_t)a.RS * kRT + std::max<int64_t>(ell, a.RS + kRR) + 2) * 8);
+    static int configured = 0;
+    if (smem > configured) {
+      SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      configured = smem;
+    }
+    void* args[] = {&a};
+    SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
+    ProfScope ps(kTagSample, s);
+    count_launch();
+    SQR_CUDA(cudaLaunchCooperativeKernel((const void*)sample_qrcp_reg_kernel, dim3(G), dim3(kRT), args,
+                                         (size_t)smem, s));
+    return SQR_OK;
+  }
   // At least 32 columns per CTA (amortise the per-step barrier), enough CTAs
   // to keep every column in shared memory when possible, one CTA per SM.
   const int ldS = (int)(ell | 1);
