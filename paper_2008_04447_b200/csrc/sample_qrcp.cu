@@ -664,17 +664,26 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
 
 // ---------------------------------------------------------------------------
 // Thread-per-column variant (nt <= 256 G, ell <= 144): thread t of CTA g owns
-// sample column 256 g + t for the whole launch.  Rows [RS, ell) (the last 64,
-// RS = ell - 64) live in REGISTERS, rows [0, RS) in shared memory (row-major
+// sample column 256 g + t for the whole launch.  Rows [RS, ell) (the last 48,
+// RS = ell - 48) live in REGISTERS, rows [0, RS) in shared memory (row-major
 // over the 256 columns: conflict-free), so the dot / update / downdate of a
-// step are thread-local and touch shared memory only for the first RS rows.
-// The reflector is kept as a full-length vector yf (zeros above the pivot row)
-// so the register loop needs no predicate.  The update is applied at once
-// (no deferred pass), the CTA candidate's updated column is published by its
-// owner, and one grid barrier per step remains.  Same arithmetic and the same
-// downdate guard / exact recompute / tie rule as sample_qrcp_kernel.
+// step are thread-local.  The reflector is kept as a full-length vector (zeros
+// above the pivot row) so the register loops need no predicate.  Register
+// rows are updated at once; the shared-memory rows' rank-1 update is deferred
+// to the barrier wait (warps 1-7, while warp 0 selects the winner), and the
+// published candidate column gets it applied on the fly.  One grid barrier per
+// step; same arithmetic, downdate guard / exact recompute and tie rule as
+// sample_qrcp_kernel.
 constexpr int kRT = 256;
-constexpr int kRR = 64;  // register rows
+constexpr int kRR = 48;  // register rows
+
+// shared-memory pair load the compiler may not CSE (keeps 64 y values from
+// staying live across the dot and the update loops)
+__device__ __forceinline__ double2 lds2(const double* p) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+  return v;
+}
 
 struct RegArgs {
   const double* B;
@@ -702,8 +711,13 @@ __device__ __forceinline__ void add_move(const RegArgs& a, int dst, int src) {
 
 __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   extern __shared__ __align__(16) double sm[];
-  double* cs = sm;                     // [RS][kRT]
-  double* yf = cs + (size_t)a.RS * kRT;  // [ell]
+  const int ell = a.ell, RS = a.RS;
+  const int YP = ((max(ell, RS + kRR) + 1) | 1) + 1;  // even pitch of a reflector buffer
+  double* cs = sm;                                     // [RS][kRT]
+  double* ybase = cs + (size_t)RS * kRT;               // [2][YP]: reflectors by step parity
+  const int yoff = RS & 1;                             // makes &y[RS] 16-byte aligned
+  double* wcol = ybase + 2 * YP + 2;                   // [kRT]: tau (y . d_c) of the current step
+  __shared__ __align__(16) double stg[kRR];            // publish staging of register rows
   __shared__ double wv_s[kRT / 32];
   __shared__ int wp_s[kRT / 32], wl_s[kRT / 32];
   __shared__ double sred[32];
@@ -717,11 +731,11 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   gb.init(a.bar);
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  const int ell = a.ell, RS = a.RS;
   const int col = g * kRT + tid;
   const bool own = col < a.nt;
+  auto ybuf = [&](int par) -> double* { return ybase + par * YP + yoff; };
   if (g == 0 && tid == 0) a.st->nmoves = 0;
-  for (int r = ell + tid; r < RS + kRR; r += kRT) yf[r] = 0.0;  // register rows beyond ell (ell < 64)
+  for (int e = tid; e < 2 * YP; e += kRT) ybase[e] = 0.0;  // zero rows beyond ell (ell < 64)
 
   // ---- load my column: rows [0, RS) to shared memory, [RS, ell) to registers
   double xr[kRR];
@@ -784,16 +798,9 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   }
   if (g == 0 && tid == 0 && a.first) a.st->floor_sq = sample_floor;
 
-  // value of row r of my column (r < RS: shared memory; else a register select)
-  auto rowval = [&](int r) -> double {
-    if (r < RS) return cs[r * kRT + tid];
-    double v = 0.0;
-#pragma unroll
-    for (int q = 0; q < kRR; ++q)
-      if (RS + q == r) v = xr[q];
-    return v;
-  };
-  // CTA candidate for step jn -> publish (value, position, column rows jn..)
+  // CTA candidate for step jn -> publish (value, position, column rows jn..).
+  // Shared-memory rows still miss the deferred update of step jn-1 (w, y of
+  // parity (jn-1)&1): it is applied on the fly.
   auto publish = [&](int jn) {
     warp_argmax(cbv, cbp, cbl);
     if (lane == 0) {
@@ -808,15 +815,21 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     warp_argmax(v, p, l);
     const int par = jn & 1;
     if (tid == 0) a.cand[par * G + g] = make_double2(v, __longlong_as_double((long long)p));
-    if (l >= 0 && tid == __shfl_sync(0xffffffffu, l, 0)) {
+    if (l >= 0 && warp == (l >> 5)) {
       double* dst = a.ccol + ((size_t)par * G + g) * ell;
-      for (int r = jn; r < RS; ++r) dst[r] = cs[r * kRT + tid];
+      if (tid == l) {
 #pragma unroll
-      for (int q = 0; q < kRR; ++q)
-        if (RS + q >= jn && RS + q < ell) dst[RS + q] = xr[q];
+        for (int q = 0; q < kRR; q += 2) *reinterpret_cast<double2*>(stg + q) = make_double2(xr[q], xr[q + 1]);
+      }
+      __syncwarp();
+      const double* yp = ybuf((jn - 1) & 1);
+      const double wl = jn > 0 ? wcol[l] : 0.0;
+      for (int r = jn + lane; r < RS; r += 32) dst[r] = fma(-yp[r], wl, cs[r * kRT + l]);
+      for (int q = lane; q < kRR; q += 32)
+        if (RS + q >= jn && RS + q < ell) dst[RS + q] = stg[q];
     }
   };
-  // global winner of step jn + its reflector into yf (warp 0, lane 0 waited)
+  // global winner of step jn + its reflector (warp 0, lane 0 waited)
   auto winner = [&](int jn) {
     const int par = jn & 1;
     double bv = -1.0;
@@ -861,6 +874,7 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
         y0 = u0 - beta;
         tau = 2.0 / (1.0 + s1 / (y0 * y0));
       }
+      double* yf = ybuf(par);
       for (int r = lane; r < jn; r += 32) yf[r] = 0.0;
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
@@ -875,6 +889,17 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       bc_s.tau = tau;
     }
   };
+  // deferred rank-1 update of the shared-memory rows [jd, RS) with step jd's
+  // (wcol, y), by threads [t0, kRT): rows outer, columns inner (coalesced)
+  auto smem_update = [&](int jd, int t0) {
+    const double* yp = ybuf(jd & 1);
+    const int nthr = kRT - t0;
+    const int ncell = (RS - jd) * kRT;
+    for (int e = tid - t0; e < ncell; e += nthr) {
+      const int r = jd + e / kRT, c = e % kRT;
+      cs[r * kRT + c] = fma(-yp[r], wcol[c], cs[r * kRT + c]);
+    }
+  };
 
   publish(0);
   gb.sync();
@@ -887,10 +912,12 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     if (!bc_s.go) break;  // uniform across the grid
     const int pc = bc_s.pc;
     const double beta = bc_s.beta, tau = bc_s.tau;
+    const double* yf = ybuf(j & 1);
     if (g == 0 && tid == 0) a.taus[j] = tau;
     cbv = -1.0;
     cbp = INT_MAX;
     cbl = -1;
+    double wvv = 0.0;
     if (pos == pc) {
       // the pivot: R part rows < j, beta, reflector tail -> Bf column j
       double* bfj = a.Bf + (int64_t)j * a.ldbf;
@@ -907,24 +934,41 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       const int pn = (pos == j) ? pc : pos;  // the column at position j moves to pc
       pos = pn;
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
-      for (int r = j; r < RS; ++r) d0 = fma(yf[r], cs[r * kRT + tid], d0);
-#pragma unroll
-      for (int q = 0; q < kRR; q += 4) {
-        d1 = fma(yf[RS + q], xr[q], d1);
-        d2 = fma(yf[RS + q + 1], xr[q + 1], d2);
-        d3 = fma(yf[RS + q + 2], xr[q + 2], d3);
-        d0 = fma(yf[RS + q + 3], xr[q + 3], d0);
+      {
+        int r = j;
+        for (; r + 2 <= RS; r += 2) {
+          d2 = fma(yf[r], cs[r * kRT + tid], d2);
+          d3 = fma(yf[r + 1], cs[(r + 1) * kRT + tid], d3);
+        }
+        if (r < RS) d2 = fma(yf[r], cs[r * kRT + tid], d2);
       }
-      const double wvv = tau * ((d0 + d1) + (d2 + d3));
-      for (int r = j; r < RS; ++r) cs[r * kRT + tid] = fma(-yf[r], wvv, cs[r * kRT + tid]);
 #pragma unroll
-      for (int q = 0; q < kRR; ++q) xr[q] = fma(-yf[RS + q], wvv, xr[q]);
-      const double rj = rowval(j);
+      for (int q = 0; q < kRR; q += 2) {
+        const double2 yv = lds2(yf + RS + q);
+        d0 = fma(yv.x, xr[q], d0);
+        d1 = fma(yv.y, xr[q + 1], d1);
+      }
+      wvv = tau * ((d0 + d1) + (d2 + d3));
+#pragma unroll
+      for (int q = 0; q < kRR; q += 2) {
+        const double2 yv = lds2(yf + RS + q);
+        xr[q] = fma(-yv.x, wvv, xr[q]);
+        xr[q + 1] = fma(-yv.y, wvv, xr[q + 1]);
+      }
+      double rj;
+      if (j < RS) {
+        rj = fma(-yf[j], wvv, cs[j * kRT + tid]);
+      } else {
+        rj = 0.0;
+#pragma unroll
+        for (int q = 0; q < kRR; ++q)
+          if (RS + q == j) rj = xr[q];
+      }
       double ns = nsq - rj * rj;
       if (ns < kNormGuard * rsq) {
         double e0 = 0.0, e1 = 0.0;
         for (int r = j + 1; r < RS; ++r) {
-          const double v = cs[r * kRT + tid];
+          const double v = fma(-yf[r], wvv, cs[r * kRT + tid]);
           e0 = fma(v, v, e0);
         }
 #pragma unroll
@@ -940,7 +984,9 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       cbp = pn;
       cbl = tid;
     }
+    wcol[tid] = wvv;  // 0 for the pivot and for finished / absent columns
     achieved = j + 1;
+    SQR_TRACE(a.trace, 8 * j + 1);
     if (j + 1 < a.bb) {
       publish(j + 1);
       SQR_TRACE(a.trace, 8 * j + 2);
@@ -951,9 +997,15 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
         if (lane == 0) SQR_TRACE(a.trace, 8 * j + 6);
         __syncwarp();
         winner(j + 1);
+      } else {
+        smem_update(j, 32);
       }
       __syncthreads();
       SQR_TRACE(a.trace, 8 * j + 4);
+    } else {
+      __syncthreads();
+      smem_update(j, 0);
+      __syncthreads();
     }
   }
   __syncthreads();
@@ -1028,7 +1080,8 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     a.pmax = reinterpret_cast<double*>(p);
     a.trace = g_trace_host_ptr;
     const int G = (int)std::max<int64_t>(1, cdiv(nt, (int64_t)kRT));
-    const int smem = (int)(((int64_t)a.RS * kRT + std::max<int64_t>(ell, a.RS + kRR) + 2) * 8);
+    const int YP = (int)(((std::max<int64_t>(ell, a.RS + kRR) + 1) | 1) + 1);
+    const int smem = (int)(((int64_t)a.RS * kRT + 2 * YP + 2 + kRT) * 8);
     static int configured = 0;
     if (smem > configured) {
       SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

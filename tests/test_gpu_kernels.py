@@ -84,8 +84,13 @@ def test_gemm_nn(M, N, K, off):
 
 
 # ------------------------------------------------------------ sample QRCP
+# shapes cover the thread-per-column kernel (nt <= 148*256, ell <= 144: odd ell,
+# ell below / at the 48 register rows, ell = 144) and the smem/L2 kernel
+# (nt > 37888 or ell > 144)
 @pytest.mark.parametrize("ell,nt,bb,seed", [(40, 1000, 32, 1), (12, 40, 6, 5), (136, 6000, 128, 2), (72, 2000, 64, 3),
-                                            (40, 20000, 32, 4), (9, 9, 9, 6)])
+                                            (40, 20000, 32, 4), (9, 9, 9, 6), (137, 3000, 128, 7), (144, 700, 128, 8),
+                                            (47, 257, 40, 9), (48, 513, 48, 12), (40, 40000, 32, 10),
+                                            (150, 600, 100, 11)])
 def test_sample_qrcp_matches_oracle(ell, nt, bb, seed):
     B = gauss(ell, nt, seed)
     st_ref = O.sample_pivots(B, bb)
@@ -175,3 +180,48 @@ def test_panel_zero_column_stops_like_reference():
     assert relerr(Pd.numpy(), work) <= 1e-11
     assert relerr(Y.numpy()[:, :5], Yref) <= 1e-11
     assert np.all(Y.numpy()[:, 5:] == 0.0)
+
+
+# ------------------------------------------------ whole-panel factor (C ABI)
+def _panel_factor_dev(P, w, stop_at_zero=1):
+    mr = P.shape[0]
+    Pd = upload(P, DEV)
+    Y = ColMajor.empty(mr, w, DEV)
+    taus = torch.zeros(w, dtype=torch.float64, device=DEV)
+    st = status_new(DEV)
+    ws = torch.zeros(int(L.sqr_block_workspace(mr, w, w)), dtype=torch.uint8, device=DEV)
+    _lib.check(L.sqr_panel_factor(Pd.ptr, Pd.ld, mr, w, Y.ptr, Y.ld, taus.data_ptr(), stop_at_zero, st.data_ptr(),
+                                  ws.data_ptr(), ws.numel(), stream_handle()))
+    return Pd.numpy(), Y.numpy(), taus.cpu().numpy(), status_read(st)
+
+
+# single-launch block kernel (mr <= 148*256) and the leaf + GEMM path beyond it
+@pytest.mark.parametrize("mr,w,seed", [(1000, 32, 1), (5000, 100, 2), (32768, 128, 3), (37888, 128, 4),
+                                       (40000, 64, 5), (257, 13, 6), (300, 33, 7), (64, 64, 8)])
+def test_panel_factor_matches_oracle(mr, w, seed):
+    P = gauss(mr, w, seed)
+    work = P.copy(order="F")
+    Yref, tref, done = O.panel_factor(work, 0, w)
+    Pg, Yg, tg, s = _panel_factor_dev(P, w)
+    assert int(s["bhat"]) == done == w
+    assert relerr(Pg, work) <= 1e-11
+    assert relerr(Yg, Yref) <= 1e-11
+    assert relerr(tg, tref) <= 1e-12
+
+
+@pytest.mark.parametrize("mr,w,zc", [(300, 24, 5), (2000, 100, 40), (2000, 100, 0), (50000, 64, 37)])
+def test_panel_factor_zero_column(mr, w, zc):
+    P = gauss(mr, w, 9)
+    P[:, zc] = 0.0  # exactly zero column: beta == 0 at step zc
+    work = P.copy(order="F")
+    Yref, tref, done = O.panel_factor(work, 0, w)
+    assert done == zc
+    Pg, Yg, tg, s = _panel_factor_dev(P, w)
+    assert int(s["bhat"]) == zc
+    assert relerr(Pg, work) <= 1e-11
+    if zc:
+        assert relerr(Yg[:, :zc], Yref) <= 1e-11
+        assert relerr(tg[:zc], tref[:zc]) <= 1e-12
+    assert np.all(Yg[:, zc:] == 0.0) and np.all(tg[zc:] == 0.0)
+    if zc == 0:
+        assert int(s["stop"]) == 1 and int(s["reason"]) == 4
