@@ -148,6 +148,20 @@ int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b
               double* taus, double* T, sqr_status* st, void* workspace, int64_t workspace_bytes,
               void* stream);
 
+/* sqr_rqrcp + R streamed to pinned host memory while the factorization runs:
+ * each column block of R (rows [0, i0+bb), columns [i0, i0+bb)) is final right
+ * after its panel (later column moves only touch later columns) and is copied
+ * to R_host (column-major, ldrh >= min(k, m)) on an internal copy stream,
+ * overlapping the remaining blocks; entries below the diagonal are not
+ * written.  The copies are joined into `stream`.  Workspace:
+ * sqr_rqrcp_stream_r_workspace() (adds one b x b staging slot per block).
+ * Replaces the reference's host-resident result of randomized.py:227-229. */
+int64_t sqr_rqrcp_stream_r_workspace(int64_t m, int64_t n, int64_t k, int64_t b, int64_t p);
+int sqr_rqrcp_stream_r(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+                       uint64_t seed, const double* omegaT, int64_t ldo, int resample, int64_t* perm,
+                       double* taus, double* T, sqr_status* st, void* workspace, int64_t workspace_bytes,
+                       double* R_host, int64_t ldrh, void* stream);
+
 /* Truncated RQRCP (randomized.py:250-341).  A is permuted in place but never
  * updated.  Outputs Yg (m x k, ldy), Wg (k x n, ldw: W^T rows), Rg (k x n,
  * ldr), perm, taus, T blocks, status. */

@@ -46,6 +46,9 @@ SIGNATURES = {
     "sqr_rqrcp_workspace": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),
     "sqr_rqrcp": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_u64, c_ptr, c_i64, c_int, c_ptr,
                           c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
+    "sqr_rqrcp_stream_r_workspace": (c_i64, [c_i64] * 5),
+    "sqr_rqrcp_stream_r": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_u64, c_ptr, c_i64, c_int,
+                                   c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_trqrcp_workspace": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),
     "sqr_trqrcp": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_u64, c_ptr, c_i64, c_ptr, c_i64,
                            c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),

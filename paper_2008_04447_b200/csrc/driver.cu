@@ -195,11 +195,65 @@ extern "C" int64_t sqr_rqrcp_workspace(int64_t m, int64_t n, int64_t /*k*/, int6
   return carve_rqrcp(nullptr, m, n, b, p, true, true).total;
 }
 
-extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
-                         uint64_t seed, const double* omegaT, int64_t ldo, int resample, int64_t* perm,
-                         double* taus, double* T, sqr_status* st, void* workspace, int64_t workspace_bytes,
-                         void* stream) {
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+namespace sqr {
+namespace {
+// Streams the finished R columns to pinned host memory while later blocks run.
+// Column block [i0, i0+bb) never changes after its panel (later column moves
+// only touch columns >= the next block), so right after the panel its rows
+// above the block go out with one 2D copy and its diagonal block, with the
+// reflector tails zeroed, through a per-block staging slot.
+struct RSink {
+  double* host = nullptr;
+  int64_t ldh = 0;
+  double* stage = nullptr;  // nblk x b x b
+  cudaStream_t cs = nullptr;
+  cudaEvent_t ev = nullptr;
+  ~RSink() {
+    if (ev) cudaEventDestroy(ev);
+    if (cs) cudaStreamDestroy(cs);
+  }
+  int init(double* h, int64_t l, double* st) {
+    host = h;
+    ldh = l;
+    stage = st;
+    if (!host) return SQR_OK;
+    SQR_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    SQR_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    return SQR_OK;
+  }
+  int block(const double* A, int64_t lda, int64_t i0, int64_t bb, int64_t b, int64_t J, cudaStream_t s) {
+    if (!host) return SQR_OK;
+    double* slot = stage + J * b * b;
+    int rc = copy_upper(A + i0 + i0 * lda, lda, slot, bb, bb, nullptr, s);
+    if (rc) return rc;
+    SQR_CUDA(cudaEventRecord(ev, s));
+    SQR_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+    if (i0 > 0)
+      SQR_CUDA(cudaMemcpy2DAsync(host + i0 * ldh, ldh * 8, A + i0 * lda, lda * 8, i0 * 8, bb,
+                                 cudaMemcpyDeviceToHost, cs));
+    SQR_CUDA(cudaMemcpy2DAsync(host + i0 + i0 * ldh, ldh * 8, slot, bb * 8, bb * 8, bb, cudaMemcpyDeviceToHost,
+                               cs));
+    return SQR_OK;
+  }
+  // rows [0, rows) of the columns [c0, n) left of no block (truncated runs), then join
+  int finish(const double* A, int64_t lda, int64_t rows, int64_t c0, int64_t n, cudaStream_t s) {
+    if (!host) return SQR_OK;
+    if (c0 < n && rows > 0) {
+      SQR_CUDA(cudaEventRecord(ev, s));
+      SQR_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      SQR_CUDA(cudaMemcpy2DAsync(host + c0 * ldh, ldh * 8, A + c0 * lda, lda * 8, rows * 8, n - c0,
+                                 cudaMemcpyDeviceToHost, cs));
+    }
+    SQR_CUDA(cudaEventRecord(ev, cs));
+    SQR_CUDA(cudaStreamWaitEvent(s, ev, 0));
+    return SQR_OK;
+  }
+};
+
+int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p, uint64_t seed,
+               const double* omegaT, int64_t ldo, int resample, int64_t* perm, double* taus, double* T,
+               sqr_status* st, void* workspace, int64_t workspace_bytes, double* R_host, int64_t ldrh,
+               cudaStream_t s) {
   const int64_t ell = b + p;
   if (m <= 0 || n <= 0 || k < 1 || k > std::min(m, n) || b < 1 || p < 0 || ell >= m || lda < m) {
     set_error("sqr_rqrcp: invalid arguments m=%lld n=%lld k=%lld b=%lld p=%lld", (long long)m, (long long)n,
@@ -212,10 +266,15 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
     return SQR_EINVAL;
   }
   RqrcpWs w = carve_rqrcp(workspace, m, n, b, p, omegaT == nullptr, resample != 0);
-  if (workspace == nullptr || workspace_bytes < w.total) {
-    set_error("sqr_rqrcp: workspace %lld < %lld bytes", (long long)workspace_bytes, (long long)w.total);
+  const int64_t stage_bytes = R_host ? cdiv(k, b) * b * b * 8 : 0;
+  if (workspace == nullptr || workspace_bytes < w.total + stage_bytes) {
+    set_error("sqr_rqrcp: workspace %lld < %lld bytes", (long long)workspace_bytes,
+              (long long)(w.total + stage_bytes));
     return SQR_EINVAL;
   }
+  RSink sink;
+  int rcs = sink.init(R_host, ldrh, reinterpret_cast<double*>(static_cast<char*>(workspace) + w.total));
+  if (rcs) return rcs;
   SQR_CUDA(cudaMemsetAsync(st, 0, sizeof(sqr_status), s));
   int rc = iota(perm, n, s);
   if (rc) return rc;
@@ -249,6 +308,7 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
       if ((rc = panel_factor(P, lda, mr, bb, -1, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
         return rc;
     }
+    if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
     if (la.on) {
       // Second sweep split around the side stream (see Lookahead).
       if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s,
@@ -288,7 +348,33 @@ extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k
       std::swap(Bc, Bn);
     }
   }
-  return SQR_OK;
+  return sink.finish(A, lda, std::min(k, m), std::min(k, n), n, s);
+}
+}  // namespace
+}  // namespace sqr
+
+extern "C" int sqr_rqrcp(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+                         uint64_t seed, const double* omegaT, int64_t ldo, int resample, int64_t* perm,
+                         double* taus, double* T, sqr_status* st, void* workspace, int64_t workspace_bytes,
+                         void* stream) {
+  return rqrcp_impl(A, lda, m, n, k, b, p, seed, omegaT, ldo, resample, perm, taus, T, st, workspace,
+                    workspace_bytes, nullptr, 0, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int64_t sqr_rqrcp_stream_r_workspace(int64_t m, int64_t n, int64_t k, int64_t b, int64_t p) {
+  return sqr_rqrcp_workspace(m, n, k, b, p) + cdiv(k, b) * b * b * 8;
+}
+
+extern "C" int sqr_rqrcp_stream_r(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t b, int64_t p,
+                                  uint64_t seed, const double* omegaT, int64_t ldo, int resample, int64_t* perm,
+                                  double* taus, double* T, sqr_status* st, void* workspace,
+                                  int64_t workspace_bytes, double* R_host, int64_t ldrh, void* stream) {
+  if (R_host == nullptr || ldrh < std::min(k, m)) {
+    set_error("sqr_rqrcp_stream_r: R_host missing or ldrh < min(k, m)");
+    return SQR_EINVAL;
+  }
+  return rqrcp_impl(A, lda, m, n, k, b, p, seed, omegaT, ldo, resample, perm, taus, T, st, workspace,
+                    workspace_bytes, R_host, ldrh, static_cast<cudaStream_t>(stream));
 }
 
 // ------------------------------------------------------------ TRQRCP

@@ -575,7 +575,18 @@ def _empty(m, n, dev, truncated=False):
     return pf
 
 
-def _randomized(A, k, b, p, seed, resample, omega=None, _status=None):
+def _check_out(out, rows, n):
+    """`out=`: a Fortran-ordered float64 host array of shape (>= rows, n) that
+    receives R while the factorization runs (pinned memory for full speed).
+    Its strictly lower part is never written: pass it zeroed."""
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.ndim != 2:
+        raise ValueError("out must be a 2-D float64 numpy array")
+    if not out.flags.f_contiguous or out.shape[0] < rows or out.shape[1] != n:
+        raise ValueError(f"out must be Fortran-ordered with shape (>= {rows}, {n})")
+    return out
+
+
+def _randomized(A, k, b, p, seed, resample, omega=None, _status=None, out=None):
     M, _ = _load(A)
     m, n = M.m, M.n
     _check_block_args(m, n, k, b, p)
@@ -594,18 +605,31 @@ def _randomized(A, k, b, p, seed, resample, omega=None, _status=None):
     taus = torch.zeros(k, dtype=torch.float64, device=dev)
     Tb = torch.zeros((nblk, b * b), dtype=torch.float64, device=dev)
     st = status_new(dev)
-    ws = _ws(L.sqr_rqrcp_workspace(m, n, k, b, p), dev)
-    _lib.check(L.sqr_rqrcp(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
-                           OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
-                           1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws), ws.numel(),
-                           stream_handle()), "sqr_rqrcp")
+    if out is None:
+        ws = _ws(L.sqr_rqrcp_workspace(m, n, k, b, p), dev)
+        _lib.check(L.sqr_rqrcp(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
+                               OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
+                               1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws), ws.numel(),
+                               stream_handle()), "sqr_rqrcp")
+    else:
+        # R streamed to the host buffer block by block, overlapped with the later blocks
+        out = _check_out(out, min(k, m), n)
+        ws = _ws(L.sqr_rqrcp_stream_r_workspace(m, n, k, b, p), dev)
+        _lib.check(L.sqr_rqrcp_stream_r(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
+                                        OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
+                                        1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws),
+                                        ws.numel(), out.ctypes.data, out.shape[0], stream_handle()),
+                   "sqr_rqrcp_stream_r")
     s = status_read(st)
     if _status is not None:
         _status.append(s)
     ach, nb = int(s["achieved"]), int(s["nblocks"])
     cnt = rqrcp_counters(m, n, b, ell, ach, nb, int(s["reason"]), resample)
     pf = PivotedFactorization(m, n, None, None, None, ach, cnt)
-    pf._Rd = _upper_rows(M, ach)
+    if out is None:
+        pf._Rd = _upper_rows(M, ach)
+    else:
+        pf._R = out[:ach]
     pf._permd = perm
     widths = [(J * b, min(b, ach - J * b)) for J in range(nb)]
     pf._blocks_fn = lambda: _packed_blocks(M, taus, Tb, b, widths, m)
@@ -613,14 +637,16 @@ def _randomized(A, k, b, p, seed, resample, omega=None, _status=None):
     return pf
 
 
-def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None) -> PivotedFactorization:
-    """Blocked randomized QRCP with sample updates (randomized.py:227-229)."""
-    return _randomized(A, k, b, p, seed, False, omega)
+def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, out=None) -> PivotedFactorization:
+    """Blocked randomized QRCP with sample updates (randomized.py:227-229).
+
+    `out` (extension): host array receiving R during the factorization (see _check_out)."""
+    return _randomized(A, k, b, p, seed, False, omega, out=out)
 
 
-def rsrqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0) -> PivotedFactorization:
+def rsrqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, out=None) -> PivotedFactorization:
     """Blocked randomized QRCP re-sketching every block (randomized.py:232-234)."""
-    return _randomized(A, k, b, p, seed, True, None)
+    return _randomized(A, k, b, p, seed, True, None, out=out)
 
 
 def ssrqrcp(A, k: int, p: int = 8, seed: int = 0, omega=None) -> PivotedFactorization:

@@ -178,3 +178,18 @@ def test_zero_and_rank_zero():
     assert res.achieved_rank == 0
     pf = G.rqrcp(np.eye(5), 0)
     assert pf.achieved_rank == 0 and pf.R.shape == (0, 5)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k,b", [(2000, 1500, 1500, 64), (1200, 900, 300, 32), (700, 700, 650, 128)])
+def test_rqrcp_streams_r_to_host(m, n, k, b):
+    """rqrcp(..., out=R): R arrives on the host during the factorization and is
+    identical to the device-materialised R; the strict lower part is untouched."""
+    A = gauss(m, n, 21)
+    ref = G.rqrcp(A, k, b=b, p=8, seed=0)
+    out = np.zeros((min(k, m), n), order="F")
+    got = G.rqrcp(A, k, b=b, p=8, seed=0, out=out)
+    assert got.achieved_rank == ref.achieved_rank
+    assert np.array_equal(got.perm, ref.perm)
+    assert np.array_equal(got.R, ref.R)
+    assert np.all(np.tril(out[: got.achieved_rank], -1) == 0.0)
