@@ -463,7 +463,6 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * (Cfg::BN / 2);
   const int nk = (int)cdiv(K, kBK);
-
   double acc[2][NJ][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -519,33 +518,41 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
   }
   cp_async_wait<0>();
 
+  // Epilogue in 4 row chunks (mi, h); the beta*E loads of chunk c+1 are issued
+  // before the stores of chunk c (E and D may alias in place, so the compiler
+  // cannot hoist them itself: without this the chunks pay 4 serial round trips).
+  auto load_e = [&](int c, double (&el)[NJ][2]) {
+    const int mi = c >> 1, h = c & 1;
+    const int m = m0 + wm + mi * 16 + g + h * 8;
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+    for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int m = m0 + wm + mi * 16 + g + h * 8;
-      double el[NJ][2];
-      if (beta != 0.0) {
-#pragma unroll
-        for (int nj = 0; nj < NJ; ++nj)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int n = n0 + wn + nj * 8 + 2 * t + e;
-            el[nj][e] = (m < M && n < N) ? E[(int64_t)n * lde + m] : 0.0;
-          }
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn + nj * 8 + 2 * t + e;
+        el[nj][e] = (beta != 0.0 && m < M && n < N) ? E[(int64_t)n * lde + m] : 0.0;
       }
-      if (m >= M) continue;
+  };
+  double ea[NJ][2], eb[NJ][2];
+  load_e(0, ea);
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj)
+  for (int c = 0; c < 4; ++c) {
+    double (&cur)[NJ][2] = (c & 1) ? eb : ea;
+    double (&nxt)[NJ][2] = (c & 1) ? ea : eb;
+    if (c + 1 < 4) load_e(c + 1, nxt);
+    const int mi = c >> 1, h = c & 1;
+    const int m = m0 + wm + mi * 16 + g + h * 8;
+    if (m >= M) continue;
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int n = n0 + wn + nj * 8 + 2 * t + e;
-          if (n >= N) continue;
-          double v = alpha * acc[mi][nj][h * 2 + e];
-          if (beta != 0.0) v = fma(beta, el[nj][e], v);
-          D[(int64_t)n * ldd + m] = v;
-        }
-    }
+    for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int n = n0 + wn + nj * 8 + 2 * t + e;
+        if (n >= N) continue;
+        double v = alpha * acc[mi][nj][h * 2 + e];
+        if (beta != 0.0) v = fma(beta, cur[nj][e], v);
+        D[(int64_t)n * ldd + m] = v;
+      }
+  }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
