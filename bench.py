@@ -57,7 +57,7 @@ def rqrcp_flops_by_kernel(m, n, k, b, p):
         total += mr * bb * bb               # T
         if ntr > 0:
             tn += 2.0 * bb * mr * ntr + 2.0 * bb * bb * ntr   # Y^T C, T^T W
-            nn += 2.0 * bb * mr * ntr                          # C -= Y W
+            nn += 2.0 * bb * mr * ntr + 2.0 * bb * bb * ntr   # C -= Y W; sample update M R12
             total += 4.0 * bb * mr * ntr + 2.0 * bb * bb * ntr + 3.0 * bb * bb * ntr
     return {"gemm_tn": tn, "gemm_nn": nn, "algorithmic_total": total}
 
@@ -142,6 +142,15 @@ def host_cores():
     return os.cpu_count() or 1
 
 
+def base_config(args, parallelism="single GPU"):
+    """The workload description shared by both arms (BASELINE configs[4], C5)."""
+    m = n = args.n
+    return {"workload": f"C5: rqrcp(A, k={n}, b={args.b}, p={args.p}, seed=0), A = giid({m}, {n}, seed=5) "
+                        "from the reference stream",
+            "m": m, "n": n, "k": n, "b": args.b, "p": args.p, "parallelism": parallelism,
+            "flop_convention": "LAPACK 2mn^2-2n^3/3 = %.1f GFLOP" % lapack_gflop(m, n)}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -160,8 +169,7 @@ def run_reference(args):
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
-        "config": {"workload": f"rqrcp n={n_s} (bounded CPU sample of C5 n=32768)", "b": args.b, "p": args.p,
-                   "flop_convention": "LAPACK 2mn^2-2n^3/3"},
+        "config": dict(base_config(args, "host cores"), cpu_sample=f"each step: {sample}"),
         "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": host_cores(), "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -173,9 +181,9 @@ def run_reference(args):
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
-    if ws > 1:
+    if ws > 1 or args.force_distributed:
         from paper_2008_04447_b200 import distributed
-        return distributed.bench_main(args, METRIC, PEAK_FP64_TFLOPS, PEAK_SOURCE)
+        return distributed.bench_main(args, sys.modules[__name__])
     torch.cuda.set_device(local)
     import paper_2008_04447_b200 as G
     from paper_2008_04447_b200 import _lib
@@ -272,13 +280,11 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C5: rqrcp(A, k=32768, b=128, p=8, seed=0), A = giid(32768, 32768, seed=5) "
-                               "from the reference stream generated on device",
-                   "m": m, "n": n, "k": k, "b": b, "p": p, "parallelism": "single GPU",
-                   "flop_convention": "LAPACK 2mn^2-2n^3/3 = %.1f GFLOP" % gflop,
-                   "algorithmic_gflop": fl["algorithmic_total"] / 1e9,
-                   "l2": "inputs (8.6 GB) larger than L2 (126 MB); no flush needed",
-                   "achieved_rank": ach},
+        "config": dict(base_config(args),
+                   input="generated on the device from the reference stream",
+                   algorithmic_gflop=fl["algorithmic_total"] / 1e9,
+                   l2="inputs (8.6 GB) larger than L2 (126 MB); no flush needed",
+                   achieved_rank=ach),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -296,10 +302,12 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--n", type=int, default=32768)
+    ap.add_argument("--matrix-n", dest="n", type=int, default=32768)
     ap.add_argument("--b", type=int, default=128)
     ap.add_argument("--p", type=int, default=8)
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--force-distributed", action="store_true",
+                    help="run the multi-GPU (block-cyclic, NCCL) driver even at world size 1 (testing)")
     ap.add_argument("--cpu-sample-n", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -430,8 +430,13 @@ def local_giid(m: int, n: int, b: int, seed: int, lay: BlockCyclic, r: int, devi
     return A
 
 
-def bench_main(args, metric, peak, peak_source):
-    """bench.py --gpus N under torchrun: strong scaling of C5 (n = 32768)."""
+def bench_main(args, bench):
+    """bench.py --gpus N under torchrun: strong scaling of C5 (n = 32768).
+
+    ``bench`` is the bench.py module (metric, peak, config and clock helpers).
+    Per rank: device time of the K timed steps with CUDA events between two
+    barriers, max over ranks; e2e = the same call with this rank's columns
+    uploaded from pinned host memory and its factored columns read back."""
     import json
     import os
     import time
@@ -442,6 +447,8 @@ def bench_main(args, metric, peak, peak_source):
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
     comm = TorchComm()
+    from . import _lib
+    L = _lib.lib()
     m = n = args.n
     b, p = args.b, args.p
     lay = BlockCyclic(n, b, comm.size)
@@ -449,36 +456,71 @@ def bench_main(args, metric, peak, peak_source):
     ops = GpuOps(dev)
     torch.cuda.synchronize()
 
-    def step():
-        A = A0.clone()
-        return rqrcp_block_cyclic(A, m, n, n, b, p, 0, comm, ops)
+    def step(A_src):
+        A = A_src.clone()
+        return rqrcp_block_cyclic(A, m, n, n, b, p, 0, comm, ops), A
 
     for _ in range(args.warmup):
-        step()
+        step(A0)
     torch.cuda.synchronize()
     dist.barrier()
+    launches0 = L.sqr_launch_count()
+    L.sqr_profile_enable(20000 * max(1, args.steps))
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    e0.record()
-    for _ in range(args.steps):
-        res = step()
-    e1.record()
-    torch.cuda.synchronize()
+    with bench.ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            res, _ = step(A0)
+        e1.record()
+        torch.cuda.synchronize()
     dist.barrier()
+    launches = L.sqr_launch_count() - launches0
+    prof = _lib.profile_collect()
+    L.sqr_profile_enable(0)
     ms = comm.max(e0.elapsed_time(e1) / args.steps)
-    gflop = (2.0 * m * n * n - 2.0 * n ** 3 / 3.0) / 1e9
+    gflop = bench.lapack_gflop(m, n)
+    value = gflop / (ms / 1e3)
+    # roofline of this rank's dominant GEMM class: its local share of the flops
+    fl = bench.rqrcp_flops_by_kernel(m, n, n, b, p)
+    dom = max(("gemm_tn", "gemm_nn"), key=lambda t: prof[t][0])
+    share = lay.n_local(comm.rank) / n
+    dom_ms = prof[dom][0] / args.steps
+    ach_tf = fl[dom] * share / (dom_ms / 1e3) / 1e12 if dom_ms > 0 else None
+    # e2e: pinned host columns in, factored columns out
+    e2e = None
+    if args.e2e_steps > 0:
+        A_host = torch.empty_like(A0, device="cpu").pin_memory()
+        A_host.copy_(A0)
+        out_host = torch.empty_like(A_host).pin_memory()
+        torch.cuda.synchronize()
+        dist.barrier()
+        ts = []
+        for _ in range(args.e2e_steps):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            Ad = A_host.to(dev, non_blocking=True)
+            r2, A_fact = step(Ad)
+            out_host.copy_(A_fact, non_blocking=True)
+            torch.cuda.synchronize()
+            ts.append(comm.max(time.perf_counter() - t0))
+        t_e2e = float(np.median(ts))
+        e2e = {"value": gflop / t_e2e, "unit": "GFLOP/s", "h2d_bytes_per_step": int(A_host.numel() * 8),
+               "d2h_bytes_per_step": int(out_host.numel() * 8), "ms_per_step": t_e2e * 1e3,
+               "steps": args.e2e_steps, "api": "distributed.rqrcp_block_cyclic on this rank's pinned columns",
+               "per_rank_bytes": True}
+    clocks = clk.summary()
     if rank == 0:
-        line = {"metric": metric, "value": gflop / (ms / 1e3), "unit": "GFLOP/s", "n_gpus": comm.size,
+        line = {"metric": bench.METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": comm.size,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": "C5: rqrcp n=32768 b=128 p=8, column block-cyclic", "m": m, "n": n,
-                           "b": b, "p": p, "parallelism": f"column-block-cyclic x{comm.size} (NCCL)",
-                           "achieved_rank": res.achieved,
-                           "l2": "inputs larger than L2; no flush needed"},
-                "roofline": {"bound": "tensor", "achieved": gflop / (ms / 1e3) / 1e3 / comm.size, "peak": peak,
-                             "unit": "TFLOP/s", "frac": gflop / (ms / 1e3) / 1e3 / comm.size / peak,
-                             "traffic": None, "peak_source": peak_source, "kernel": "whole step per GPU"},
-                "cpu_baseline": None, "e2e": None, "wall_s": time.perf_counter() - t0}
+                "config": dict(bench.base_config(args, f"column block-cyclic x{comm.size} (NCCL)"),
+                               achieved_rank=res.achieved, l2="inputs larger than L2; no flush needed"),
+                "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach_tf, "peak": bench.PEAK_FP64_TFLOPS,
+                             "unit": "TFLOP/s", "frac": (ach_tf / bench.PEAK_FP64_TFLOPS) if ach_tf else None,
+                             "traffic": None, "peak_source": bench.PEAK_SOURCE, "rank": 0},
+                "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
+                "clocks": clocks}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0

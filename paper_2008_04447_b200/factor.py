@@ -293,9 +293,20 @@ class PivotedFactorization:
         self._perm = None if perm is None else np.asarray(perm, dtype=np.int64)
         self.achieved_rank = int(achieved_rank)
         self.counters = counters or CommCounters()
-        self._Rd = None        # torch (achieved, n) row-major, upper trapezoidal
+        self._Rd_val = None    # torch (achieved, n) row-major, upper trapezoidal
+        self._Rd_fn = None     # lazy producer of _Rd_val (R extracted only when asked for)
         self._permd = None     # torch int64 (n,)
         self._blocks_fn = None
+
+    @property
+    def _Rd(self):
+        if self._Rd_val is None and self._Rd_fn is not None:
+            self._Rd_val, self._Rd_fn = self._Rd_fn(), None
+        return self._Rd_val
+
+    @_Rd.setter
+    def _Rd(self, v):
+        self._Rd_val, self._Rd_fn = v, None
 
     # lazily materialised reference fields
     @property
@@ -627,7 +638,7 @@ def _randomized(A, k, b, p, seed, resample, omega=None, _status=None, out=None):
     cnt = rqrcp_counters(m, n, b, ell, ach, nb, int(s["reason"]), resample)
     pf = PivotedFactorization(m, n, None, None, None, ach, cnt)
     if out is None:
-        pf._Rd = _upper_rows(M, ach)
+        pf._Rd_fn = lambda: _upper_rows(M, ach)
     else:
         pf._R = out[:ach]
     pf._permd = perm
