@@ -104,6 +104,13 @@ int sqr_gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, 
 int sqr_sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb,
                     double* Bf, int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus,
                     int first, sqr_status* st, void* stream);
+/* Same with caller-owned scratch (>= sqr_sample_qrcp_workspace(l, nt) bytes,
+ * whose first 64 bytes -- the grid-barrier word -- the call resets on the
+ * stream): no allocation, so it can be issued every block by an orchestrator. */
+int64_t sqr_sample_qrcp_workspace(int64_t ell, int64_t nt);
+int sqr_sample_qrcp_ws(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf,
+                       int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st,
+                       void* workspace, int64_t workspace_bytes, void* stream);
 
 /* Apply the block's column moves to rows [0, rows) of X (ld) starting at
  * column col0, and to the int64 vector perm (may be NULL) starting at col0
@@ -132,6 +139,11 @@ int sqr_build_t(const double* Y, int64_t ldy, int64_t m, int64_t j, const double
  * 217-219).  Bf is the factored sample from sqr_sample_qrcp (l x (nt+b)). */
 int sqr_sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr,
                       int64_t nt, double* Bnext, int64_t ldbn, sqr_status* st, void* stream);
+/* Same, with the block size b (= the sample QRCP's sample_achieved) given by
+ * the caller and a caller-owned b*b scratch `mbuf`: never synchronises the
+ * host (the multi-GPU orchestrator already knows b). */
+int sqr_sample_update_b(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
+                        int64_t b, double* Bnext, int64_t ldbn, sqr_status* st, double* mbuf, void* stream);
 
 /* ------------------------------------------------------------- drivers
  * Full RQRCP (randomized.py:166-224, resample=0) / RSRQRCP (resample=1) on the

@@ -38,11 +38,16 @@ SIGNATURES = {
                             c_ptr, c_i64, c_ptr]),
     "sqr_sample_qrcp": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_int,
                                 c_ptr, c_ptr]),
+    "sqr_sample_qrcp_workspace": (c_i64, [c_i64, c_i64]),
+    "sqr_sample_qrcp_ws": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_int,
+                                   c_ptr, c_ptr, c_i64, c_ptr]),
     "sqr_apply_moves": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
     "sqr_panel_qr": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_int, c_ptr,
                              c_ptr]),
     "sqr_build_t": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_sample_update": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
+    "sqr_sample_update_b": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr,
+                                    c_ptr]),
     "sqr_rqrcp_workspace": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),
     "sqr_rqrcp": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_i64, c_i64, c_u64, c_ptr, c_i64, c_int, c_ptr,
                           c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),

@@ -444,6 +444,19 @@ extern "C" int sqr_sample_update(const double* Bf, int64_t ldbf, int64_t ell, co
   return rc;
 }
 
+// Same update with the block size b supplied by the caller (the sample
+// QRCP's sample_achieved, already known to a host orchestrator) and a
+// caller-owned b*b scratch: no host synchronisation (multi-GPU driver).
+extern "C" int sqr_sample_update_b(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr,
+                                   int64_t nt, int64_t b, double* Bnext, int64_t ldbn, sqr_status* st, double* mbuf,
+                                   void* stream) {
+  if (b < 1 || b > ell || mbuf == nullptr) {
+    sqr::set_error("sqr_sample_update_b: need 1 <= b <= ell and a b*b scratch");
+    return SQR_EINVAL;
+  }
+  return sqr::sample_update(Bf, ldbf, ell, R, ldr, nt, b, Bnext, ldbn, st, mbuf, static_cast<cudaStream_t>(stream));
+}
+
 extern "C" int64_t sqr_launch_count(void) { return sqr::g_launches.load(); }
 
 extern "C" int sqr_profile_enable(int64_t max_launches) {

@@ -1177,3 +1177,12 @@ extern "C" int sqr_sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_
   cudaFreeAsync(ws, static_cast<cudaStream_t>(stream));
   return rc;
 }
+
+extern "C" int64_t sqr_sample_qrcp_workspace(int64_t ell, int64_t nt) { return sqr::sample_qrcp_workspace(ell, nt); }
+
+extern "C" int sqr_sample_qrcp_ws(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf,
+                                  int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus, int first,
+                                  sqr_status* st, void* workspace, int64_t workspace_bytes, void* stream) {
+  return sqr::sample_qrcp(B, ldb, ell, nt, bb, Bf, ldbf, lperm, moves, taus, first, st, workspace, workspace_bytes,
+                          static_cast<cudaStream_t>(stream));
+}

@@ -23,6 +23,7 @@ NCCL) and, in the CPU test-suite, on gloo with a NumPy reference backend.
 """
 from __future__ import annotations
 
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -35,9 +36,20 @@ _DIAG_FLOOR = 2.0 ** -52
 
 
 # ------------------------------------------------------------------ layout
+@functools.lru_cache(maxsize=64)
+def _local_columns(n: int, b: int, P: int, r: int) -> np.ndarray:
+    nblk = -(-n // b)
+    cols = [np.arange(c * b, min(n, (c + 1) * b), dtype=np.int64) for c in range(r, nblk, P)]
+    out = np.concatenate(cols) if cols else np.zeros(0, dtype=np.int64)
+    out.setflags(write=False)
+    return out
+
+
 @dataclass(frozen=True)
 class BlockCyclic:
-    """Column block-cyclic map with block width b over P ranks."""
+    """Column block-cyclic map with block width b over P ranks.  The per-rank
+    column lists are computed once and cached (the driver asks for them every
+    block)."""
 
     n: int
     b: int
@@ -59,19 +71,19 @@ class BlockCyclic:
         return list(range(r, self.nblocks, self.P))
 
     def n_local(self, r: int) -> int:
-        return sum(min(self.b, self.n - c * self.b) for c in self.blocks_of(r))
+        return int(_local_columns(self.n, self.b, self.P, r).size)
+
+    def n_local_max(self) -> int:
+        return self.n_local(0)  # rank 0 owns the first block, so never fewer columns
 
     def global_of_local(self, r: int) -> np.ndarray:
-        """Global position of every local column of rank r, in local order."""
-        out = []
-        for c in self.blocks_of(r):
-            out.extend(range(c * self.b, min(self.n, (c + 1) * self.b)))
-        return np.asarray(out, dtype=np.int64)
+        """Global position of every local column of rank r, in local order
+        (read-only cached array)."""
+        return _local_columns(self.n, self.b, self.P, r)
 
     def first_local_at_or_after(self, r: int, p: int) -> int:
         """Local index of the first local column whose global position >= p."""
-        g = self.global_of_local(r)
-        return int(np.searchsorted(g, p))
+        return int(np.searchsorted(self.global_of_local(r), p))
 
 
 # -------------------------------------------------------------------- comm
@@ -134,6 +146,8 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
     lay = BlockCyclic(n, b, comm.size)
     r = comm.rank
     gloc = lay.global_of_local(r)
+    if hasattr(ops, "begin"):
+        ops.begin(lay, m, ell)
     perm = np.arange(n, dtype=np.int64)
     taus = np.zeros(max(k, 1))
     # 1. sketch: local slab, all-gathered into global column order.
@@ -221,7 +235,12 @@ class _Panel:
 
 
 class GpuOps:
-    """libsqr kernels on torch CUDA tensors; matrices are (ncols, ld) tensors."""
+    """libsqr kernels on torch CUDA tensors; matrices are (ncols, ld) tensors.
+
+    Every per-block buffer is allocated once per factorization shape and
+    reused; per block the host reads back two small control records (the
+    sample QRCP status + moves, and the broadcast panel tail: status, taus,
+    R11) and uploads one packed index array for the column moves."""
 
     def __init__(self, device):
         from . import _lib
@@ -231,6 +250,7 @@ class GpuOps:
         self.dev = torch.device(device)
         self.Workspace = Workspace
         self._keep = []
+        self._shape = None
 
     # helpers
     def _s(self):
@@ -246,11 +266,36 @@ class GpuOps:
         # Index arrays must outlive the asynchronous launch that reads them: a
         # temporary freed inside an argument list could be handed to the next
         # allocation of the same call.  Keep them until the next sync point.
-        t = torch.as_tensor(np.asarray(a, dtype=np.int64), device=self.dev)
+        t = torch.as_tensor(np.asarray(a, dtype=np.int64)).pin_memory().to(self.dev, non_blocking=True)
         self._keep.append(t)
         if len(self._keep) > 64:
             self._keep = self._keep[-64:]
         return t
+
+    def begin(self, lay, m, ell):
+        """Per-shape persistent buffers (allocated on the first call of a
+        factorization of this shape)."""
+        key = (lay.n, lay.b, lay.P, m, ell)
+        if self._shape == key:
+            return
+        self._shape = key
+        n, b = lay.n, lay.b
+        f64 = dict(dtype=torch.float64, device=self.dev)
+        self.Bglob = torch.zeros((max(n, 1), ell), **f64)            # replicated sample, global positions
+        self.Bf = torch.zeros((max(n, 1), ell), **f64)
+        self.lperm = torch.zeros(max(n, 1), dtype=torch.int64, device=self.dev)
+        self.ctl = torch.zeros(128 + 4 * (4 * b + 8), dtype=torch.uint8, device=self.dev)
+        self.staus = torch.zeros(b, **f64)
+        # panel broadcast record: [Y (b x m) | taus (b) | R11 (b x b) | status (9 doubles)]
+        self.pbuf = torch.zeros(b * m + b + b * b + 9, **f64)
+        self.T = torch.zeros((b, b), **f64)
+        nmax = lay.n_local_max()
+        self.slab = torch.zeros((max(nmax, 1), ell), **f64)
+        self.Bfl = torch.zeros((b + max(nmax, 1), ell), **f64)
+        self.Rl = torch.zeros((b + max(nmax, 1), b), **f64)
+        self.mbuf = torch.zeros(b * b, **f64)
+        self.sws = torch.zeros(int(self.L.sqr_sample_qrcp_workspace(ell, n)), dtype=torch.uint8, device=self.dev)
+        self.gidx = [torch.tensor(lay.global_of_local(q), device=self.dev) for q in range(lay.P)]
 
     # 1. sketch of the local slab
     def sketch(self, A, m, ell, seed, omega, gloc):
@@ -268,54 +313,52 @@ class GpuOps:
                                          Bl.data_ptr(), ell, ws.data_ptr(), ws.numel(), self._s()), "sketch")
         return Bl
 
+    def pad_slab(self, Bn, lay, achieved):
+        if Bn.data_ptr() == self.slab.data_ptr():
+            return self.slab          # the sample update wrote straight into the slab
+        nb = min(Bn.shape[0], self.slab.shape[0])
+        if nb:
+            self.slab[:nb].copy_(Bn[:nb])
+        return self.slab
+
     def _assemble(self, parts, lay, ell, p0):
-        """Columns of the all-gathered slabs (each padded to n_local_max) into
-        global order for positions >= p0."""
-        n = lay.n
-        out = torch.empty((max(n - p0, 1), ell), dtype=torch.float64, device=self.dev)
+        """Columns of the all-gathered slabs into the replicated sample at their
+        global positions; the sample for positions >= p0 is Bglob[p0:]."""
         for q, part in enumerate(parts):
-            g = lay.global_of_local(q)
-            g = g[g >= p0]
-            if g.size:
-                self._chk(self.L.sqr_copy_columns(part.data_ptr(), ell, ell, None, out.data_ptr(), ell,
-                                                  self._idx(g - p0).data_ptr(), g.size, self._s()), "assemble")
-        return out
+            s = lay.first_local_at_or_after(q, p0)
+            cnt = lay.n_local(q) - s
+            if cnt > 0:
+                self._chk(self.L.sqr_copy_columns(part.data_ptr(), ell, ell, None, self.Bglob.data_ptr(), ell,
+                                                  self.gidx[q][s:].data_ptr(), cnt, self._s()), "assemble")
+        return self.Bglob[p0:]
 
     def assemble(self, parts, lay, ell):
         return self._assemble(parts, lay, ell, 0)
-
-    def pad_slab(self, Bn, lay, achieved):
-        nmax = max(lay.n_local(q) for q in range(lay.P))
-        out = torch.zeros((nmax, Bn.shape[1]), dtype=torch.float64, device=self.dev)
-        nb = min(Bn.shape[0], nmax)
-        if nb:
-            out[:nb].copy_(Bn[:nb])
-        return out
 
     def assemble_next(self, parts, lay, achieved, ell):
         return self._assemble(parts, lay, ell, achieved)
 
     # 2. replicated sample QRCP
     def sample_qrcp(self, B, ell, nt, bb, first):
-        from ._dev import status_new, status_read
-        Bf = torch.empty((max(nt, 1), ell), dtype=torch.float64, device=self.dev)
-        lperm = torch.empty(max(nt, 1), dtype=torch.int64, device=self.dev)
-        moves = torch.empty(4 * bb + 8, dtype=torch.int32, device=self.dev)
-        taus = torch.zeros(max(bb, 1), dtype=torch.float64, device=self.dev)
-        st = status_new(self.dev)
+        st = self.ctl[:72]
+        st.zero_()
         if not first:  # the sample floor of the first block (randomized.py:179-180)
             st[32:40].view(torch.float64).fill_(self._floor)
-        self._chk(self.L.sqr_sample_qrcp(B.data_ptr(), ell, ell, nt, bb, Bf.data_ptr(), ell, lperm.data_ptr(),
-                                         moves.data_ptr(), taus.data_ptr(), 1 if first else 0, st.data_ptr(),
-                                         self._s()), "sample_qrcp")
-        s = status_read(st)
+        moves = self.ctl[128:].view(torch.int32)
+        self._chk(self.L.sqr_sample_qrcp_ws(B.data_ptr(), ell, ell, nt, bb, self.Bf.data_ptr(), ell,
+                                            self.lperm.data_ptr(), moves.data_ptr(), self.staus.data_ptr(),
+                                            1 if first else 0, st.data_ptr(), self.sws.data_ptr(), self.sws.numel(),
+                                            self._s()), "sample_qrcp")
+        h = self.ctl.cpu().numpy()        # one D2H: status + moves
+        s = np.frombuffer(h[:72].tobytes(), dtype=self.lib.STATUS_DTYPE)[0]
         if first:
             self._floor = float(s["floor_sq"])
         stop = bool(s["stop"])
         reason = {2: "sample_floor", 3: "sample_rank"}.get(int(s["reason"]), "none")
         nm = int(s["nmoves"])
-        mv = moves[:2 * nm].view(nm, 2).cpu().numpy().astype(np.int64)
-        return _Sample(stop, reason, int(s["sample_achieved"]), mv, Bf, st)
+        mv = h[128:128 + 8 * nm].view(np.int32).reshape(nm, 2).astype(np.int64)
+        self._keep.clear()
+        return _Sample(stop, reason, int(s["sample_achieved"]), mv, self.Bf[:max(nt, 1)], st)
 
     # 3. point-to-point column moves
     def move_columns(self, A, ps, pd, lay, comm):
@@ -323,41 +366,56 @@ class GpuOps:
         ld = A.shape[1]
         osrc, odst = lay.owner(ps), lay.owner(pd)
         lsrc, ldst = lay.local_index(ps), lay.local_index(pd)
-        sends, recv_shapes = {}, {}
-        # pack every outgoing / locally moved source first (reads before writes)
         mine = np.nonzero(osrc == r)[0]
+        loc = np.nonzero(odst[mine] == r)[0] if mine.size else np.zeros(0, np.int64)
+        peers_out = sorted(set(odst[mine].tolist()) - {r})
+        peers_in = sorted(set(osrc[odst == r].tolist()) - {r})
+        # one upload for every index list of this block
+        pieces = [lsrc[mine], loc, ldst[mine[loc]]]
+        sel_out = {q: np.nonzero(odst[mine] == q)[0] for q in peers_out}
+        idx_in = {q: np.nonzero((odst == r) & (osrc == q))[0] for q in peers_in}
+        pieces += [sel_out[q] for q in peers_out] + [ldst[idx_in[q]] for q in peers_in]
+        offs = np.cumsum([0] + [p.size for p in pieces])
+        dev_idx = self._idx(np.concatenate(pieces) if offs[-1] else np.zeros(1, np.int64))
+
+        def view(i):
+            return dev_idx[offs[i]:offs[i + 1]]
+
+        sends, recv_shapes = {}, {}
         packed = None
         if mine.size:
             packed = torch.empty((mine.size, ld), dtype=torch.float64, device=self.dev)
-            self._chk(self.L.sqr_copy_columns(A.data_ptr(), ld, ld, self._idx(lsrc[mine]).data_ptr(),
-                                              packed.data_ptr(), ld, None, mine.size, self._s()), "pack")
-            for q in set(odst[mine].tolist()) - {r}:
-                sel = np.nonzero(odst[mine] == q)[0]
-                sends[q] = packed[self._idx(sel)]
-        for q in set(osrc[odst == r].tolist()) - {r}:
-            recv_shapes[q] = (int(np.count_nonzero((odst == r) & (osrc == q))), ld)
+            self._chk(self.L.sqr_copy_columns(A.data_ptr(), ld, ld, view(0).data_ptr(), packed.data_ptr(), ld, None,
+                                              mine.size, self._s()), "pack")
+            for i, q in enumerate(peers_out):
+                sends[q] = packed.index_select(0, view(3 + i))
+        for q in peers_in:
+            recv_shapes[q] = (int(idx_in[q].size), ld)
         recvs = comm.exchange(sends, recv_shapes, A)
         # unpack: local moves then received columns, in move order per source
-        if mine.size:
-            loc = np.nonzero(odst[mine] == r)[0]
-            if loc.size:
-                self._chk(self.L.sqr_copy_columns(packed.data_ptr(), ld, ld, self._idx(loc).data_ptr(), A.data_ptr(),
-                                                  ld, self._idx(ldst[mine[loc]]).data_ptr(), loc.size, self._s()),
-                          "unpack")
-        for q, buf in recvs.items():
-            idx = np.nonzero((odst == r) & (osrc == q))[0]
+        if loc.size:
+            self._chk(self.L.sqr_copy_columns(packed.data_ptr(), ld, ld, view(1).data_ptr(), A.data_ptr(), ld,
+                                              view(2).data_ptr(), loc.size, self._s()), "unpack")
+        for i, q in enumerate(peers_in):
+            buf = recvs[q]
             self._chk(self.L.sqr_copy_columns(buf.data_ptr(), ld, ld, None, A.data_ptr(), ld,
-                                              self._idx(ldst[idx]).data_ptr(), idx.size, self._s()), "unpack")
+                                              view(3 + len(peers_out) + i).data_ptr(), buf.shape[0], self._s()),
+                      "unpack")
 
     # 4. panel on the owner + broadcast
+    def _panel_views(self, mr, bb):
+        y = bb * mr
+        Y = self.pbuf[:y].view(bb, mr)
+        taus = self.pbuf[y:y + bb]
+        R11 = self.pbuf[y + bb:y + bb + bb * bb].view(bb, bb)
+        st = self.pbuf[y + bb + bb * bb:y + bb + bb * bb + 9].view(torch.uint8)
+        return Y, taus, R11, st, self.pbuf[:y + bb + bb * bb + 9], self.pbuf[y:y + bb + bb * bb + 9]
+
     def panel(self, A, lc, i0, m, w, bb, is_owner):
-        from ._dev import status_new
         mr = m - i0
-        Y = torch.zeros((bb, mr), dtype=torch.float64, device=self.dev)
-        taus = torch.zeros(bb, dtype=torch.float64, device=self.dev)
-        R11 = torch.zeros((bb, bb), dtype=torch.float64, device=self.dev)
-        st = status_new(self.dev)
+        Y, taus, R11, st, rec, tail = self._panel_views(mr, bb)
         if is_owner:
+            rec.zero_()
             ld = A.shape[1]
             Pp = A.data_ptr() + 8 * (lc * ld + i0)
             ws = self._ws(self.L.sqr_block_workspace(mr, 0, bb))
@@ -367,15 +425,13 @@ class GpuOps:
         return _Panel(0, Y, taus, None, R11, None, st)
 
     def broadcast_panel(self, pan, owner, comm, mr, bb):
-        meta = pan.st[:24].view(torch.int32)  # stop, reason, achieved, nblocks, sample_achieved, bhat
-        comm.broadcast(meta, owner)
-        comm.broadcast(pan.Y, owner)
-        comm.broadcast(pan.taus, owner)
-        comm.broadcast(pan.R11, owner)
-        mh = meta.cpu().numpy()
-        pan.bhat = 0 if mh[0] else int(mh[5])
-        pan.taus_host = pan.taus.cpu().numpy()
-        R = pan.R11.cpu().numpy().T[:pan.bhat, :pan.bhat]  # (bb, bb) storage is column-major
+        _, _, _, _, rec, tail = self._panel_views(mr, bb)
+        comm.broadcast(rec, owner)           # one message: Y, taus, R11, status
+        h = tail.cpu().numpy()               # one D2H: taus, R11, status
+        meta = h[bb + bb * bb:].view(np.int32)
+        pan.bhat = 0 if meta[0] else int(meta[5])
+        pan.taus_host = h[:bb].copy()
+        R = h[bb:bb + bb * bb].reshape(bb, bb).T[:pan.bhat, :pan.bhat]  # (bb, bb) storage is column-major
         pan.R11_host = np.triu(R)
         return pan
 
@@ -385,33 +441,34 @@ class GpuOps:
         ncols = A.shape[0] - t0
         bb = pan.Y.shape[0]
         mr = m - i0
-        T = torch.empty((bb, bb), dtype=torch.float64, device=self.dev)
+        T = self.T.view(-1)[:bb * bb].view(bb, bb)
         ws = self._ws(self.L.sqr_block_workspace(mr, max(ncols, 0), bb))
         self._chk(self.L.sqr_apply_block_update(A.data_ptr() + 8 * (t0 * ld + i0), ld, mr, max(ncols, 0), bb,
                                                 pan.Y.data_ptr(), mr, pan.taus.data_ptr(), T.data_ptr(), bb,
                                                 ws.data_ptr(), ws.numel(), self._s()), "block_update")
         pan.T = T
 
-    # 6. sample update of my columns
+    # 6. sample update of my columns, written straight into the all-gather slab
     def sample_update_local(self, samp, A, s0, rel, i0, bb, pan):
         ell = samp.Bf.shape[1]
         nloc = len(rel)
-        Bn = torch.empty((max(nloc, 1), ell), dtype=torch.float64, device=self.dev)
         if nloc == 0:
-            return Bn[:0]
+            return self.slab[:0]
         # Bf_loc = [S11 | Bf[:, rel]] and R_loc = [R11 | R12 of my columns]
-        Bfl = torch.empty((bb + nloc, ell), dtype=torch.float64, device=self.dev)
+        Bfl = self.Bfl[:bb + nloc]
         Bfl[:bb].copy_(samp.Bf[:bb])
-        self._chk(self.L.sqr_copy_columns(samp.Bf.data_ptr(), ell, ell, self._idx(rel).data_ptr(),
+        rel_d = self._idx(rel)
+        self._chk(self.L.sqr_copy_columns(samp.Bf.data_ptr(), ell, ell, rel_d.data_ptr(),
                                           Bfl.data_ptr() + 8 * bb * ell, ell, None, nloc, self._s()), "gather S")
-        Rl = torch.empty((bb + nloc, bb), dtype=torch.float64, device=self.dev)
+        Rl = self.Rl.view(-1)[:(bb + nloc) * bb].view(bb + nloc, bb)
         Rl[:bb].copy_(pan.R11)
         ld = A.shape[1]
         self._chk(self.L.sqr_copy_columns(A.data_ptr() + 8 * (s0 * ld + i0), ld, bb, None, Rl.data_ptr() + 8 * bb * bb,
                                           bb, None, nloc, self._s()), "gather R12")
-        self._chk(self.L.sqr_sample_update(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, Bn.data_ptr(), ell,
-                                           samp.st.data_ptr(), self._s()), "sample_update")
-        return Bn[:nloc]
+        self._chk(self.L.sqr_sample_update_b(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, bb,
+                                             self.slab.data_ptr(), ell, samp.st.data_ptr(), self.mbuf.data_ptr(),
+                                             self._s()), "sample_update")
+        return self.slab[:nloc]
 
 
 # ----------------------------------------------------------------- bench
@@ -428,6 +485,32 @@ def local_giid(m: int, n: int, b: int, seed: int, lay: BlockCyclic, r: int, devi
                        torch.cuda.current_stream(device).cuda_stream)
         j += w
     return A
+
+
+class _OpsTimer:
+    """SQR_DIST_TRACE=1: wraps every ops call with a device synchronisation and
+    accumulates wall time per method (diagnostics only; perturbs timing)."""
+
+    def __init__(self, ops, dev):
+        import time
+        self._ops, self._dev, self._t, self._time = ops, dev, {}, time
+
+    def __getattr__(self, name):
+        f = getattr(self._ops, name)
+        if not callable(f):
+            return f
+
+        def wrapped(*a, **k):
+            torch.cuda.synchronize(self._dev)
+            t0 = self._time.perf_counter()
+            out = f(*a, **k)
+            torch.cuda.synchronize(self._dev)
+            self._t[name] = self._t.get(name, 0.0) + self._time.perf_counter() - t0
+            return out
+        return wrapped
+
+    def report(self):
+        return {k: round(v * 1e3, 1) for k, v in sorted(self._t.items(), key=lambda kv: -kv[1])}
 
 
 def bench_main(args, bench):
@@ -454,6 +537,10 @@ def bench_main(args, bench):
     lay = BlockCyclic(n, b, comm.size)
     A0 = local_giid(m, n, b, 5, lay, comm.rank, dev)
     ops = GpuOps(dev)
+    tracer = None
+    if os.environ.get("SQR_DIST_TRACE"):
+        tracer = _OpsTimer(ops, dev)
+        ops = tracer
     torch.cuda.synchronize()
 
     def step(A_src):
@@ -520,7 +607,11 @@ def bench_main(args, bench):
                              "unit": "TFLOP/s", "frac": (ach_tf / bench.PEAK_FP64_TFLOPS) if ach_tf else None,
                              "traffic": None, "peak_source": bench.PEAK_SOURCE, "rank": 0},
                 "cpu_baseline": None, "e2e": e2e, "gpu_launches": int(launches),
-                "clocks": clocks}
+                "clocks": clocks,
+                "phases": {t: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
+                           for t, v in prof.items() if v[1]}}
+        if tracer is not None:
+            line["host_trace_ms"] = tracer.report()
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
