@@ -178,6 +178,53 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------- our arm
+def _event_ms(fn, reps=3):
+    import torch
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.median(ts))
+
+
+def secondary_metrics(G, A, dev):
+    """The other two parts of the headline metric, device-timed with the input
+    resident (median of 3 after 1 warm-up): TRQRCP at n = 32768 (k = 3328 ~ n/10,
+    SURVEY.md §8(d)) on the C5 matrix, and TUXV time-to-rank-k on BASELINE
+    configs[3] (C4: 20000^2 rank-100 signal + 1e-6 noise, k = 100, b = 32)."""
+    import torch
+    out = {}
+    ms = _event_ms(lambda: G.trqrcp(A, 3328, b=128, p=8, seed=0))
+    out["trqrcp_n32768_k3328"] = {"ms": ms, "algorithmic_gflop": 8187.0, "gflops": 8187e3 / ms,
+                                  "workload": "trqrcp(A_C5, k=3328, b=128, p=8, seed=0)"}
+    n = 20000
+    G1 = G.device_giid(n, 100, 41, device=dev)
+    G2 = G.device_giid(n, 100, 42, device=dev)
+    S = G1 @ G2.T
+    S /= torch.linalg.norm(S)
+    A4 = S + 1e-6 * G.device_giid(n, n, 43, device=dev)
+    del S, G1, G2
+    res = {}
+
+    def run():
+        res["r"] = G.tuxv(A4, 100, b=32, p=8, seed=0)
+    ms = _event_ms(run)
+    err = float(torch.linalg.norm(A4 - res["r"].reconstruct_device()) / torch.linalg.norm(A4))
+    out["tuxv_c4_time_to_rank_k"] = {"ms": ms, "algorithmic_gflop": 195.3, "gflops": 195.3e3 / ms,
+                                     "rel_error": err,
+                                     "workload": "tuxv(A_C4 20000x20000, k=100, b=32, p=8, seed=0); U, X, V "
+                                                 "(compact WY) and sigma_est on the device"}
+    del A4, res
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     ws, rank, local = dist_env()
@@ -276,6 +323,7 @@ def run_ours(args):
 
     phases = {t: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
               for t, v in prof.items() if v[1]}
+    secondary = None if args.no_secondary else secondary_metrics(G, A, dev)
     line = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
@@ -291,6 +339,7 @@ def run_ours(args):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
         "phases": phases,
+        "secondary": secondary,
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -310,6 +359,7 @@ def main():
                     help="run the multi-GPU (block-cyclic, NCCL) driver even at world size 1 (testing)")
     ap.add_argument("--cpu-sample-n", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the TRQRCP / TUXV secondary timings")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -233,6 +233,8 @@ int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, 
                   int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s);
 int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s);
 int iota(int64_t* p, int64_t n, cudaStream_t s);
+int zero_columns(double* W, int64_t ld, int64_t rows, int64_t ncols, const int32_t* lim, const int32_t* gate,
+                 cudaStream_t s);
 int copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* sidx, double* dst, int64_t ldd,
                  const int64_t* didx, int64_t n, cudaStream_t s);
 int copy_upper(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t n, const int32_t* gate,

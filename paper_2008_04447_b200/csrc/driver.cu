@@ -59,10 +59,10 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.lperm = c.take<int64_t>(n);
   w.moves = c.take<int32_t>(4 * b + 8);
   w.stau = c.take<double>(b);
-  w.Ypan = c.take<double>(m * b);
+  w.Ypan = c.take<double>(m * 2 * b);  // [Y_P | Y_J] of a merged pair (PairedSweep)
   w.Gm = c.take<double>(b * b);
-  w.Wt = c.take<double>(b * (n + b));
-  w.W = c.take<double>(b * n);
+  w.Wt = c.take<double>(b * (n + 2 * b));
+  w.W = c.take<double>(2 * b * n);      // [W_P ; W_J], ld 2b
   w.OmT = (need_omega || resample) ? c.take<double>(m * ell) : nullptr;
   w.pscr = c.take<double>(PanelScratch::doubles(b));
   w.snap = c.take<int32_t>(8);
@@ -136,6 +136,77 @@ int trailing_update(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, 
   rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, Wt, ldw, 0.0, nullptr, 0, W, ldw, gws, kGemmWsBytes, s, d2);
   if (rc || skip_pass2) return rc;
   return gemm_nn(mr, nt, bb, 1.0, Y, ldy, W, ldw, 1.0, P, lda, P, lda, s, d3);
+}
+
+// Paired second sweep.  The reference applies every block reflection to the
+// trailing matrix in two sweeps (randomized.py:203-207): Y^T C (long K =
+// m - i0, ~93% of the fp64 tensor pipe) and C -= Y W (K = b = 128, ~84%:
+// the short-K rank-b update is prologue/epilogue heavy).  Blocks are paired
+// (P = 2q, J = 2q + 1) and P's second sweep is merged into J's, so the bulk
+// rank update runs once per pair with K = 2b (33.5 vs 31.1 TFLOP/s on the C5
+// shape, tools/nn_k_probe.py).  Arithmetic per column is unchanged:
+//   P: [G|Wt] = Y_P^T [Y_P|C];  W_P = -T_P^T Wt;  only the R12 rows
+//      C[0:b] += Y_P[0:b] W_P are applied (the sample update needs them);
+//   J: sample QRCP on the updated sample; moves act on C and W_P alike;
+//      the J panel columns get P's update (C_pan += Y_P W_P, then those W_P
+//      columns are zeroed); panel;
+//      [Y_J^T Y_P | G | Wt] = Y_J^T [Y_P | Y_J | C]  (one sweep, C lacking P),
+//      Wt += (Y_J^T Y_P) W_P  (so Wt = Y_J^T (C + Y_P W_P) exactly as if P had
+//      been applied), W_J = -T_J^T Wt, and finally
+//      C[b:] += [Y_P | Y_J] [W_P ; W_J]  with K = 2b.
+// Rows of Y are global rows offset by the pair's i0; Y_J sits in columns
+// [b, 2b) of Ycat with its first b rows zero.
+int trailing_first(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, const double* Ycat, int64_t ldy,
+                   const double* taus, double* T, int64_t ldt, double* GWt, int64_t ldw, double* Wcat,
+                   int64_t ldwc, sqr_status* st, double* gws, cudaStream_t s) {
+  GemmDyn d1{&st->stop, &st->bhat, kShiftB};
+  d1.pre = Ycat;
+  d1.ldpre = ldy;
+  d1.npre = (int)bb;
+  int rc = gemm_tn(bb, bb + nt, mr, 1.0, Ycat, ldy, P, lda, 0.0, nullptr, 0, GWt, ldw, gws, kGemmWsBytes, s, d1);
+  if (rc) return rc;
+  if ((rc = build_t(GWt, ldw, taus, bb, T, ldt, &st->stop, s))) return rc;
+  if (nt <= 1) return SQR_OK;
+  // W_P (relative to column bhat_P = b: to i0_J), then the R12 rows only
+  rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, GWt + bb * ldw, ldw, 0.0, nullptr, 0, Wcat, ldwc, gws, kGemmWsBytes, s,
+               GemmDyn{&st->stop, &st->bhat, 0});
+  if (rc) return rc;
+  return gemm_nn(bb, nt, bb, 1.0, Ycat, ldy, Wcat, ldwc, 1.0, P, lda, P, lda, s,
+                 GemmDyn{&st->stop, &st->bhat, kShiftD});
+}
+
+// J's update of the panel columns by the pending P, before J's panel (the
+// columns [0, sample_achieved) only; their W_P columns are then retired).
+int pending_panel_update(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t b, const double* Ycat,
+                         int64_t ldy, double* Wcat, int64_t ldwc, sqr_status* st, cudaStream_t s) {
+  GemmDyn d{&st->stop, nullptr, 0};
+  d.limit = &st->sample_achieved;
+  int rc = gemm_nn(mr, bb, b, 1.0, Ycat + b, ldy, Wcat, ldwc, 1.0, P, lda, P, lda, s, d);
+  if (rc) return rc;
+  return zero_columns(Wcat, ldwc, b, bb, &st->sample_achieved, &st->stop, s);
+}
+
+int trailing_second(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, int64_t b, const double* Ycat,
+                    int64_t ldy, const double* taus, double* T, int64_t ldt, double* GWt, int64_t ldw,
+                    double* Wcat, int64_t ldwc, sqr_status* st, double* gws, cudaStream_t s) {
+  const double* Yj = Ycat + b * ldy + b;  // rows from i0_J
+  GemmDyn d1{&st->stop, &st->bhat, kShiftB};
+  d1.pre = Ycat + b;  // [Y_P | Y_J] rows from i0_J
+  d1.ldpre = ldy;
+  d1.npre = (int)(b + bb);
+  int rc = gemm_tn(bb, b + bb + nt, mr, 1.0, Yj, ldy, P, lda, 0.0, nullptr, 0, GWt, ldw, gws, kGemmWsBytes, s, d1);
+  if (rc) return rc;
+  if ((rc = build_t(GWt + b * ldw, ldw, taus, bb, T, ldt, &st->stop, s))) return rc;
+  if (nt <= 1) return SQR_OK;
+  double* Wt = GWt + (b + bb) * ldw;
+  rc = gemm_nn(bb, nt, b, 1.0, GWt, ldw, Wcat, ldwc, 1.0, Wt, ldw, Wt, ldw, s,
+               GemmDyn{&st->stop, &st->bhat, kShiftB});
+  if (rc) return rc;
+  rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, Wt, ldw, 0.0, nullptr, 0, Wcat + b, ldwc, gws, kGemmWsBytes, s,
+               GemmDyn{&st->stop, &st->bhat, kShiftD});
+  if (rc) return rc;
+  return gemm_nn(mr, nt, b + bb, 1.0, Ycat + b, ldy, Wcat, ldwc, 1.0, P, lda, P, lda, s,
+                 GemmDyn{&st->stop, &st->bhat, kShiftB | kShiftD});
 }
 
 // Lookahead schedule of one block's second sweep (randomized.py:207-221):
@@ -294,18 +365,28 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
   double* Bn = w.Bnext;
   Lookahead la;
   if (!resample && (rc = la.init())) return rc;
+  static const bool no_pair = getenv("SQR_NO_PAIRED_SWEEP") != nullptr;
+  const bool pair = !resample && !la.on && !no_pair;
+  if (pair) SQR_CUDA(cudaMemset2DAsync(w.Ypan + b * m, m * 8, 0, b * 8, b, s));  // Y_J's zero top rows
   for (int64_t J = 0; J < nblk; ++J) {
     const int64_t i0 = J * b, bb = std::min(b, k - i0), nt = n - i0, mr = m - i0;
     double* P = A + i0 + i0 * lda;
     double* TJ = T + J * b * b;
+    const bool second = pair && (J & 1);                      // merges the pending block J-1
+    const bool first = pair && !(J & 1) && J + 1 < nblk;      // second sweep deferred to J+1
+    double* Yj = second ? w.Ypan + b * m + b : w.Ypan;         // ld m, rows from i0
     if ((J == 0 || !la.on) &&
         (rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
                           w.sample_bytes, s)))
       return rc;
     if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
+    if (second) {
+      if ((rc = apply_moves(w.W, 2 * b, b, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
+      if ((rc = pending_panel_update(P, lda, mr, bb, b, w.Ypan, m, w.W, 2 * b, st, s))) return rc;
+    }
     {
       PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
-      if ((rc = panel_factor(P, lda, mr, bb, -1, w.Ypan, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
+      if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
         return rc;
     }
     if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
@@ -330,8 +411,13 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       SQR_CUDA(cudaStreamWaitEvent(s, la.join, 0));
       continue;
     }
-    if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s)))
-      return rc;
+    if (first)
+      rc = trailing_first(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s);
+    else if (second)
+      rc = trailing_second(P, lda, mr, nt, bb, b, w.Ypan, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s);
+    else
+      rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s);
+    if (rc) return rc;
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
     if (J + 1 < nblk) {
       const int64_t a1 = i0 + bb;  // achieved if the block completed

@@ -309,6 +309,16 @@ __global__ void copy_columns_kernel(const double* src, int64_t lds, int64_t rows
   }
 }
 
+// W[0:rows, c] = 0 for c < min(ncols, *lim) (gated on *gate): retires the
+// columns of a deferred block update that were already applied in place.
+__global__ void zero_columns_kernel(double* W, int64_t ld, int rows, int ncols, const int32_t* lim,
+                                    const int32_t* gate) {
+  if (gate && *gate) return;
+  const int nc = lim ? min(ncols, *lim) : ncols;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * nc; e += gridDim.x * blockDim.x)
+    W[(int64_t)(e / rows) * ld + e % rows] = 0.0;
+}
+
 __global__ void iota_kernel(int64_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = i;
@@ -400,6 +410,16 @@ int copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* si
   dim3 grid((unsigned)std::min<int64_t>(cdiv(rows, 256), 64), (unsigned)std::min<int64_t>(n, 4096));
   copy_columns_kernel<<<grid, 256, 0, s>>>(src, lds, rows, sidx, dst, ldd, didx, n);
   SQR_LAUNCH("copy_columns_kernel");
+  return SQR_OK;
+}
+
+int zero_columns(double* W, int64_t ld, int64_t rows, int64_t ncols, const int32_t* lim, const int32_t* gate,
+                 cudaStream_t s) {
+  if (rows <= 0 || ncols <= 0) return SQR_OK;
+  ProfScope ps(kTagMisc, s);
+  zero_columns_kernel<<<(unsigned)std::min<int64_t>(cdiv(rows * ncols, 256), 512), 256, 0, s>>>(
+      W, ld, (int)rows, (int)ncols, lim, gate);
+  SQR_LAUNCH("zero_columns_kernel");
   return SQR_OK;
 }
 
