@@ -997,8 +997,10 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
         if (lane == 0) SQR_TRACE(a.trace, 8 * j + 6);
         __syncwarp();
         winner(j + 1);
+        if (a.trace && g == 0 && tid == 0) a.trace[8 * j + 7] = gtimer();  // winner + reflector done
       } else {
         smem_update(j, 32);
+        if (a.trace && g == 0 && tid == 32) a.trace[8 * j + 5] = gtimer();  // deferred update done
       }
       __syncthreads();
       SQR_TRACE(a.trace, 8 * j + 4);

@@ -14,6 +14,7 @@ dev = torch.device("cuda", 0)
 only = sys.argv[1] if len(sys.argv) > 1 else "all"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 m = n = 32768
+NTS = int(os.environ.get("SQR_PROBE_NT", n))  # sample width for the sample_qrcp probe
 b, ell = 128, 136
 
 
@@ -64,7 +65,7 @@ st = status_new(dev)
 
 def sample():
     st.zero_()
-    _lib.check(L.sqr_sample_qrcp(B.ptr, B.ld, ell, n, b, Bf.ptr, Bf.ld, lperm.data_ptr(), moves.data_ptr(),
+    _lib.check(L.sqr_sample_qrcp(B.ptr, B.ld, ell, NTS, b, Bf.ptr, Bf.ld, lperm.data_ptr(), moves.data_ptr(),
                                  taus.data_ptr(), 1, st.data_ptr(), s))
 
 
