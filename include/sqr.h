@@ -92,6 +92,13 @@ int sqr_gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, 
 int sqr_gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
                 const double* Y, int64_t ldy, double beta, const double* E, int64_t lde,
                 double* D, int64_t ldd, void* stream);
+/* Same with a caller workspace: skinny products with long K (TUXV's A V_k,
+ * randomized.py:384) split K across CTAs when the output tiles cannot fill
+ * the GPU; partials are summed in a fixed order (deterministic).  Needs up to
+ * 16 * M * N doubles; less workspace means fewer splits. */
+int sqr_gemm_nn_ws(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+                   const double* Y, int64_t ldy, double beta, const double* E, int64_t lde,
+                   double* D, int64_t ldd, double* workspace, int64_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------- sample QRCP (K2, K12)
  * Halted pivoted QR of the l x nt sample B (sketch.py:97-119 -> reference.py
@@ -202,6 +209,11 @@ int sqr_apply_wy(const double* Y, int64_t ldy, const double* T, int64_t ldt, int
  * where each rank owns a subset of the columns. */
 int64_t sqr_block_workspace(int64_t m, int64_t ncols, int64_t b);
 /* dst[:, dst_idx[j]] = src[:, src_idx[j]], j < n, rows [0, rows); NULL index = identity. */
+/* Input contract (validation.py:21-37): dst = src (m x n, column-major; dst
+ * may be NULL for a check only) and *nonfinite += #NaN/Inf entries, in one
+ * read of src.  *nonfinite is a device counter the caller zeroes. */
+int sqr_copy_check(const double* src, int64_t lds, int64_t m, int64_t n, double* dst, int64_t ldd,
+                   unsigned long long* nonfinite, void* stream);
 int sqr_copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* src_idx, double* dst,
                      int64_t ldd, const int64_t* dst_idx, int64_t n, void* stream);
 /* Panel QR of an mr x w panel (w <= 128), leaves + compact-WY updates; st->bhat/stop. */

@@ -91,10 +91,49 @@ def upload(A, device, copy: bool = True) -> ColMajor:
     return out
 
 
+def _copy_check(src_ptr: int, lds: int, m: int, n: int, dst: "ColMajor | None", device) -> int:
+    """libsqr copy_check_kernel: optional copy + non-finite count in one read."""
+    cnt = torch.zeros(1, dtype=torch.int64, device=device)
+    _lib.check(_lib.lib().sqr_copy_check(src_ptr, lds, m, n, dst.ptr if dst is not None else None,
+                                         dst.ld if dst is not None else 0, cnt.data_ptr(), stream_handle()),
+               "sqr_copy_check")
+    return int(cnt.item())
+
+
+def _device_colmajor(A, device) -> int | None:
+    """Leading dimension if A is an fp64 CUDA tensor on `device` in column-major
+    layout (stride (1, ld)), else None."""
+    if (isinstance(A, torch.Tensor) and A.is_cuda and A.device == torch.device(device) and A.dtype == torch.float64
+            and A.dim() == 2 and A.shape[0] > 0 and A.shape[1] > 0 and A.stride(0) == 1
+            and A.stride(1) >= A.shape[0]):
+        return int(A.stride(1))
+    return None
+
+
+def load_checked(A, device, copy: bool = True, check: bool = True) -> ColMajor:
+    """The input contract of validation.check_matrix (validation.py:21-37) on
+    the device: 2-D, finite, copied into fresh column-major storage (or, with
+    copy=False and a column-major fp64 device input, wrapped read-only).  A
+    column-major device input is copied and scanned in ONE pass."""
+    lds = _device_colmajor(A, device)
+    if lds is not None:
+        m, n = A.shape
+        if copy:
+            M = ColMajor.empty(m, n, device)
+        else:
+            M = ColMajor(A.as_strided((n, m), (lds, 1)), m, n, lds)
+        bad = _copy_check(A.data_ptr(), lds, m, n, M if copy else None, device) if (copy or check) else 0
+    else:
+        M = upload(A, device)
+        bad = _copy_check(M.ptr, M.ld, M.m, M.n, None, device) if (check and M.m and M.n) else 0
+    if bad:
+        raise ValueError(f"A contains {bad} non-finite entries")
+    return M
+
+
 def check_finite(M: ColMajor, name: str = "A") -> None:
     if M.m and M.n:
-        v = M.view()
-        bad = int((~torch.isfinite(v)).sum().item())
+        bad = _copy_check(M.ptr, M.ld, M.m, M.n, None, M.t.device)
         if bad:
             raise ValueError(f"{name} contains {bad} non-finite entries")
 

@@ -36,6 +36,8 @@ SIGNATURES = {
                             c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_gemm_nn": (c_int, [c_i64, c_i64, c_i64, c_dbl, c_ptr, c_i64, c_ptr, c_i64, c_dbl, c_ptr, c_i64,
                             c_ptr, c_i64, c_ptr]),
+    "sqr_gemm_nn_ws": (c_int, [c_i64, c_i64, c_i64, c_dbl, c_ptr, c_i64, c_ptr, c_i64, c_dbl, c_ptr, c_i64,
+                               c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_sample_qrcp": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_int,
                                 c_ptr, c_ptr]),
     "sqr_sample_qrcp_workspace": (c_i64, [c_i64, c_i64]),
@@ -62,6 +64,7 @@ SIGNATURES = {
     "sqr_apply_wy": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_i64, c_int, c_ptr, c_i64,
                              c_ptr]),
     "sqr_block_workspace": (c_i64, [c_i64, c_i64, c_i64]),
+    "sqr_copy_check": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
     "sqr_copy_columns": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_panel_factor": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_int, c_ptr, c_ptr, c_i64,
                                  c_ptr]),

@@ -208,7 +208,7 @@ int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int6
             int64_t ws_bytes, cudaStream_t s, GemmDyn dyn);
 int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx, const double* Y,
             int64_t ldy, double beta, const double* E, int64_t lde, double* D, int64_t ldd, cudaStream_t s,
-            GemmDyn dyn);
+            GemmDyn dyn, double* ws = nullptr, int64_t ws_bytes = 0);
 int64_t sample_qrcp_workspace(int64_t ell, int64_t nt);
 int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf, int64_t ldbf,
                 int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st, void* ws,

@@ -319,6 +319,22 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// gemm_nn split-K reduction: D(m, n) = alpha * sum_z part[z](m, n) + beta * E(m, n).
+__global__ void __launch_bounds__(256)
+    nn_splitk_reduce_kernel(int M, int N, int nsplit, double alpha, const double* __restrict__ part, double beta,
+                            const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
+  if (dyn.stop && *dyn.stop) return;
+  const int64_t total = (int64_t)M * N;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int m = (int)(e % M), n = (int)(e / M);
+    double s = 0.0;
+    for (int z = 0; z < nsplit; ++z) s += __ldcg(part + z * total + e);
+    double v = alpha * s;
+    if (beta != 0.0) v = fma(beta, E[(int64_t)n * lde + m], v);
+    D[(int64_t)n * ldd + m] = v;
+  }
+}
+
 // ---------------------------------------------------------------- gemm_nn
 // CTA tile 64 m x 128 n; 4 warps = 2 (m) x 2 (n); warp tile 32 m x 64 n.
 // beta * E is read in the epilogue in two halves (32 values per thread in
@@ -442,7 +458,7 @@ template <int VEC, int BNT>
 __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
     gemm_nn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
                    const double* __restrict__ Y, int64_t ldy, double beta, const double* E,
-                   int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
+                   int64_t lde, double* D, int64_t ldd, GemmDyn dyn, int kchunk, double* part) {
   using Cfg = NnCfg<VEC, BNT>;
   constexpr int NJ = Cfg::NJ;
     extern __shared__ __align__(16) double smem[];
@@ -462,7 +478,13 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;
   const int wm = (warp & 1) * 32, wn = (warp >> 1) * (Cfg::BN / 2);
-  const int nk = (int)cdiv(K, kBK);
+  // split-K (blockIdx.z): this CTA's K range [kbeg, kend); X and Y are
+  // advanced so the loaders see a K-range starting at 0
+  const int kbeg = blockIdx.z * kchunk;
+  K = min(K, kbeg + kchunk) - kbeg;
+  X += (int64_t)kbeg * ldx;
+  Y += kbeg;
+  const int nk = K > 0 ? (int)cdiv(K, kBK) : 0;
   double acc[2][NJ][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -517,6 +539,27 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
     }
   }
   cp_async_wait<0>();
+
+  if (part != nullptr) {
+    // split-K: raw partial tile to part[z] (column-major M x N); the reduce
+    // kernel sums the splits in index order (bitwise deterministic)
+    double* mine = part + (int64_t)blockIdx.z * M * N;
+#pragma unroll
+    for (int mi = 0; mi < 2; ++mi)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int m = m0 + wm + mi * 16 + g + h * 8;
+        if (m >= M) continue;
+#pragma unroll
+        for (int nj = 0; nj < NJ; ++nj)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int n = n0 + wn + nj * 8 + 2 * t + e;
+            if (n < N) __stcg(mine + (int64_t)n * M + m, acc[mi][nj][h * 2 + e]);
+          }
+      }
+    return;
+  }
 
   // Epilogue in 4 row chunks (mi, h); the beta*E loads of chunk c+1 are issued
   // before the stores of chunk c (E and D may alias in place, so the compiler
@@ -629,7 +672,7 @@ int dispatch_tn_vec(int M, int N, int K, double alpha, const double* X, int64_t 
 template <int VEC>
 int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* Y,
               int64_t ldy, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
-              GemmDyn dyn, cudaStream_t s) {
+              GemmDyn dyn, cudaStream_t s, double* ws, int64_t ws_bytes) {
   using Cfg = NnCfg<VEC, SQR_NN_BN>;
   static bool configured = false;
   if (!configured) {
@@ -637,11 +680,36 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
                                   Cfg::SMEM));
     configured = true;
   }
-  dim3 grid((unsigned)cdiv(M, Cfg::BM), (unsigned)cdiv(N, Cfg::BN));
+  const int64_t tiles = cdiv(M, Cfg::BM) * cdiv(N, Cfg::BN);
+  // Split K when the tiles fill less than ~3 waves of resident CTAs and K is
+  // long (skinny products such as TUXV's A V_k): splits of >= 1024 K, chosen
+  // to minimise the padded waves; needs a caller workspace (static shapes
+  // only: no dynamic shift / limit).
+  int nsplit = 1;
+  const int64_t slots = (int64_t)SQR_NN_CTAS * sm_count();
+  if (ws != nullptr && dyn.shift == nullptr && dyn.limit == nullptr && K >= 2048 && tiles < 3 * slots) {
+    double best = (double)cdiv(tiles, slots);
+    for (int sp = 2; sp <= 16 && (int64_t)K / sp >= 1024; ++sp) {
+      if ((int64_t)sp * M * N * 8 > ws_bytes) break;
+      const double cost = (double)cdiv(tiles * sp, slots) / sp + 0.03;
+      if (cost < best - 1e-9) {
+        best = cost;
+        nsplit = sp;
+      }
+    }
+  }
+  const int kchunk = nsplit > 1 ? (int)rup(cdiv(K, nsplit), kBK) : std::max(K, 1);
+  nsplit = nsplit > 1 ? (int)cdiv(K, kchunk) : 1;
+  dim3 grid((unsigned)cdiv(M, Cfg::BM), (unsigned)cdiv(N, Cfg::BN), (unsigned)nsplit);
   ProfScope ps(kTagGemmNn, s);
   gemm_nn_kernel<VEC, SQR_NN_BN><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde,
-                                                                  D, ldd, dyn);
+                                                                  D, ldd, dyn, kchunk, nsplit > 1 ? ws : nullptr);
   SQR_LAUNCH("gemm_nn_kernel");
+  if (nsplit > 1) {
+    const int blocks = (int)std::min<int64_t>(cdiv((int64_t)M * N, 256), (int64_t)sm_count() * 8);
+    nn_splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, nsplit, alpha, ws, beta, E, lde, D, ldd, dyn);
+    SQR_LAUNCH("nn_splitk_reduce_kernel");
+  }
   return SQR_OK;
 }
 
@@ -667,13 +735,14 @@ int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int6
 
 int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
             const double* Y, int64_t ldy, double beta, const double* E, int64_t lde, double* D,
-            int64_t ldd, cudaStream_t s, GemmDyn dyn) {
+            int64_t ldd, cudaStream_t s, GemmDyn dyn, double* ws, int64_t ws_bytes) {
   if (M <= 0 || N <= 0) return SQR_OK;
   if (beta != 0.0 && E == nullptr) E = D;
   const bool v2 = aligned16(X) && aligned16(Y) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
                   (beta == 0.0 || (aligned16(E) && lde % 2 == 0));
-  if (v2) return launch_nn<2>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s);
-  return launch_nn<1>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s);
+  if (v2)
+    return launch_nn<2>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s, ws, ws_bytes);
+  return launch_nn<1>((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, dyn, s, ws, ws_bytes);
 }
 
 int64_t gemm_tn_workspace(int64_t N, int64_t /*K*/) {
@@ -696,4 +765,11 @@ extern "C" int sqr_gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const 
                            double* D, int64_t ldd, void* stream) {
   return sqr::gemm_nn(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd,
                       static_cast<cudaStream_t>(stream), sqr::GemmDyn{});
+}
+
+extern "C" int sqr_gemm_nn_ws(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
+                              const double* Y, int64_t ldy, double beta, const double* E, int64_t lde,
+                              double* D, int64_t ldd, double* workspace, int64_t workspace_bytes, void* stream) {
+  return sqr::gemm_nn(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, static_cast<cudaStream_t>(stream),
+                      sqr::GemmDyn{}, workspace, workspace_bytes);
 }

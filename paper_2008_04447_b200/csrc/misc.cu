@@ -319,6 +319,32 @@ __global__ void zero_columns_kernel(double* W, int64_t ld, int rows, int ncols, 
     W[(int64_t)(e / rows) * ld + e % rows] = 0.0;
 }
 
+// dst = src (m x n, column-major; dst may be NULL) and *nonfinite += the
+// number of NaN / Inf entries: the input contract's copy + finite scan
+// (validation.py:21-37) in one read of A.  Warp-aggregated atomics.
+__global__ void copy_check_kernel(const double* __restrict__ src, int64_t lds, int64_t m, int64_t n,
+                                  double* __restrict__ dst, int64_t ldd, unsigned long long* nonfinite) {
+  unsigned bad = 0;
+  const int64_t rows_per = (int64_t)blockDim.x * 2;
+  const int64_t rchunks = (m + rows_per - 1) / rows_per;
+  for (int64_t w = blockIdx.x; w < rchunks * n; w += gridDim.x) {
+    const int64_t c = w / rchunks, r0 = (w % rchunks) * rows_per;
+    const double* s = src + c * lds + r0;
+    double* d = dst ? dst + c * ldd + r0 : nullptr;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t r = threadIdx.x + u * (int64_t)blockDim.x;
+      if (r0 + r < m) {
+        const double v = __ldcs(s + r);
+        bad += isfinite(v) ? 0u : 1u;
+        if (d) __stcs(d + r, v);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nonfinite, (unsigned long long)bad);
+}
+
 __global__ void iota_kernel(int64_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = i;
@@ -475,6 +501,22 @@ extern "C" int sqr_sample_update_b(const double* Bf, int64_t ldbf, int64_t ell, 
     return SQR_EINVAL;
   }
   return sqr::sample_update(Bf, ldbf, ell, R, ldr, nt, b, Bnext, ldbn, st, mbuf, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sqr_copy_check(const double* src, int64_t lds, int64_t m, int64_t n, double* dst, int64_t ldd,
+                              unsigned long long* nonfinite, void* stream) {
+  if (m <= 0 || n <= 0) return SQR_OK;
+  if (lds < m || (dst != nullptr && ldd < m) || nonfinite == nullptr) {
+    sqr::set_error("sqr_copy_check: bad leading dimension or NULL counter");
+    return SQR_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t work = sqr::cdiv(m, 512) * n;
+  const int blocks = (int)std::min<int64_t>(work, (int64_t)sqr::sm_count() * 16);
+  sqr::ProfScope ps(sqr::kTagMisc, s);
+  sqr::copy_check_kernel<<<blocks, 256, 0, s>>>(src, lds, m, n, dst, ldd, nonfinite);
+  SQR_LAUNCH("copy_check_kernel");
+  return SQR_OK;
 }
 
 extern "C" int64_t sqr_launch_count(void) { return sqr::g_launches.load(); }

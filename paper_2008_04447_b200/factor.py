@@ -21,7 +21,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._dev import ColMajor, Workspace, check_finite, ptr, require_cuda, status_new, status_read, stream_handle, upload
+from ._dev import (ColMajor, Workspace, check_finite, load_checked, ptr, require_cuda, status_new, status_read,
+                   stream_handle, upload)
 from .counters import (CommCounters, qr_blocked_counters, qrcp_blas2_counters, qrcp_blocked_counters,
                        rqrcp_counters, trqrcp_counters)
 from .rng import host_omega
@@ -57,10 +58,9 @@ def invert_permutation(perm: np.ndarray) -> np.ndarray:
     return inv
 
 
-def _load(A, device=None) -> tuple[ColMajor, bool]:
+def _load(A, device=None, copy: bool = True, check: bool = True) -> tuple[ColMajor, bool]:
     dev = require_cuda(device if device is not None else (A.device if isinstance(A, torch.Tensor) and A.is_cuda else None))
-    M = upload(A, dev)
-    check_finite(M)
+    M = load_checked(A, dev, copy=copy, check=check)
     return M, not isinstance(A, torch.Tensor)
 
 
@@ -193,8 +193,10 @@ def gemm_tn(X: ColMajor, C: ColMajor, alpha: float = 1.0) -> ColMajor:
 def gemm_nn(X: ColMajor, Y: ColMajor, alpha: float = 1.0) -> ColMajor:
     M, N, K = X.m, Y.n, X.n
     D = ColMajor.empty(M, N, Y.t.device)
-    _lib.check(_lib.lib().sqr_gemm_nn(M, N, K, alpha, X.ptr, X.ld, Y.ptr, Y.ld, 0.0, None, 0, D.ptr, D.ld,
-                                      stream_handle()), "sqr_gemm_nn")
+    ws = _ws(16 * M * N * 8, Y.t.device) if K >= 2048 else None  # split-K scratch for skinny products
+    _lib.check(_lib.lib().sqr_gemm_nn_ws(M, N, K, alpha, X.ptr, X.ld, Y.ptr, Y.ld, 0.0, None, 0, D.ptr, D.ld,
+                                         ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
+                                         stream_handle()), "sqr_gemm_nn")
     return D
 
 
@@ -545,6 +547,9 @@ def _qr_blocked_dev(M: ColMajor, k: int, b: int) -> PivotedFactorization:
     pf = PivotedFactorization(m, n, None, None, None, k, qr_blocked_counters(m, n, k, b))
     pf._Rd = _upper_rows(M, k)
     pf._permd = torch.arange(n, device=dev)
+    # all k reflectors as ONE compact-WY block (what _compose_all of the
+    # per-block list gives, householder.py:94-104): one masked copy + T from G
+    pf._composed_fn = lambda: _packed_blocks(M, taus, None, k, [(0, k)], m)[0]
     if bk == b:
         pf._blocks_fn = lambda: _packed_blocks(M, taus, Tb, bk, widths, m)
     else:  # reference blocking with b > 128: same reflectors, regrouped
@@ -766,13 +771,15 @@ def trqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, allow_large_k: boo
 def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refine_sigma: bool = False,
          allow_large_k: bool = False, omega=None) -> TuxvResult:
     """TRQRCP + QLP flip-flop passes (randomized.py:353-406)."""
-    M, _ = _load(A)
-    m, n = M.m, M.n
     if j_max < 1:
         raise ValueError("j_max must be >= 1")
+    # trqrcp validates A and factors its own copy; A itself is then only read
+    # (A V_k), so a column-major device input is used in place
+    tf = trqrcp(A, k, b=b, p=p, seed=seed, allow_large_k=allow_large_k, omega=omega)
+    M, _ = _load(A, copy=False, check=False)
+    m, n = M.m, M.n
     dev = M.t.device
-    Aorig = M  # trqrcp factors its own copy
-    tf = trqrcp(M.view(), k, b=b, p=p, seed=seed, allow_large_k=allow_large_k, omega=omega)
+    Aorig = M
     kh = tf.achieved_rank
     cnt = tf.counters
     if kh == 0:
@@ -785,7 +792,9 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     Z0t.view().copy_(Rd[:, inv].T)
     vf = _qr_blocked_dev(Z0t, kh, b)
     cnt.merge(vf.counters)
-    v_blocks, u_blocks = vf.blocks, []
+    # the flip-flop passes use each factor as one composed block (QLP: U, V
+    # of the result are the compositions, randomized.py:344-350, 396-406)
+    v_blocks, u_blocks = [vf._composed_fn()], []
     X = vf.R_device(dev)[:kh, :kh].T.contiguous()
     for j in range(1, j_max + 1):
         if j % 2 == 1:
@@ -795,7 +804,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
             cnt.add_blas3(m, n, kh)
             uf = _qr_blocked_dev(Z, kh, b)
             cnt.merge(uf.counters)
-            u_blocks = uf.blocks
+            u_blocks = [uf._composed_fn()]
             X = uf.R_device(dev)[:kh, :kh].contiguous()
         else:
             Uk = _q_columns_dev(u_blocks, m, kh, dev)
@@ -806,7 +815,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
             cnt.add_blas3(kh, m, n)
             vf = _qr_blocked_dev(Z, kh, b)
             cnt.merge(vf.counters)
-            v_blocks = vf.blocks
+            v_blocks = [vf._composed_fn()]
             X = vf.R_device(dev)[:kh, :kh].T.contiguous()
     sig = torch.abs(torch.diagonal(X))
     if refine_sigma:

@@ -193,3 +193,32 @@ def test_rqrcp_streams_r_to_host(m, n, k, b):
     assert np.array_equal(got.perm, ref.perm)
     assert np.array_equal(got.R, ref.R)
     assert np.all(np.tril(out[: got.achieved_rank], -1) == 0.0)
+
+
+def test_device_inputs_checked_and_untouched():
+    """Column-major CUDA inputs go through the fused copy + finite scan
+    (sqr_copy_check); tuxv reads A in place without modifying it; non-finite
+    entries raise ValueError like validation.check_matrix."""
+    A = gauss(300, 200, 4)
+    Ad = torch.from_numpy(np.ascontiguousarray(A.T)).cuda().T          # (m, n), stride (1, m)
+    before = Ad.clone()
+    pf = G.rqrcp(Ad, 100, b=16, p=8, omega="host")
+    ref = O.rqrcp(A, 100, b=16, p=8, seed=0)
+    assert np.array_equal(pf.perm, ref.perm)
+    res = G.tuxv(Ad, 12, b=8, p=8, seed=1, omega="host")
+    xref = O.tuxv(A, 12, b=8, p=8, seed=1)
+    assert np.abs(res.reconstruct() - xref.reconstruct()).max() <= 1e-9 * np.abs(A).max()
+    assert torch.equal(Ad, before)
+    Cd = torch.from_numpy(A.copy()).cuda()                             # C-ordered: torch copy path
+    assert np.array_equal(G.rqrcp(Cd, 100, b=16, p=8, omega="host").perm, ref.perm)
+    for bad in (np.nan, np.inf, -np.inf):
+        B = Ad.clone()
+        B[7, 11] = bad
+        with pytest.raises(ValueError, match="non-finite"):
+            G.rqrcp(B, 10, b=8, p=4)
+        with pytest.raises(ValueError, match="non-finite"):
+            G.tuxv(B, 10, b=8, p=4)
+        Bc = Cd.clone()
+        Bc[3, 5] = bad
+        with pytest.raises(ValueError, match="non-finite"):
+            G.trqrcp(Bc, 10, b=8, p=4)

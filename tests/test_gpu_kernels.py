@@ -225,3 +225,24 @@ def test_panel_factor_zero_column(mr, w, zc):
     assert np.all(Yg[:, zc:] == 0.0) and np.all(tg[zc:] == 0.0)
     if zc == 0:
         assert int(s["stop"]) == 1 and int(s["reason"]) == 4
+
+
+@pytest.mark.parametrize("M,N,K,off", [(20000, 100, 20000, 0), (3000, 40, 9000, 1), (777, 130, 4100, 0)])
+def test_gemm_nn_split_k(M, N, K, off):
+    """sqr_gemm_nn_ws: skinny long-K products split K across CTAs (TUXV's
+    A V_k); the fixed-order reduction is bitwise reproducible."""
+    rng = np.random.default_rng(M + 7 * N + K)
+    X = rng.standard_normal((M + off, K))
+    Y = rng.standard_normal((K + off, N))
+    E = rng.standard_normal((M, N))
+    Xd, Yd, Ed = upload(X, DEV), upload(Y, DEV), upload(E, DEV)
+    w = ws(16 * M * N * 8)
+    outs = []
+    for _ in range(2):
+        D = ColMajor.empty(M, N, DEV)
+        _lib.check(L.sqr_gemm_nn_ws(M, N, K, 0.5, Xd.col_ptr(off, 0), Xd.ld, Yd.col_ptr(off, 0), Yd.ld, -1.0, Ed.ptr,
+                                    Ed.ld, D.ptr, D.ld, w.data_ptr(), w.numel(), stream_handle()))
+        outs.append(D)
+    want = 0.5 * X[off:] @ Y[off:] - E
+    assert relerr(outs[0].numpy(), want) <= 1e-13
+    assert torch.equal(outs[0].view(), outs[1].view())
