@@ -41,6 +41,10 @@ constexpr int kStages = 3;
 #define SQR_NN_CTAS 4
 #endif
 constexpr int kStagesNN = SQR_NN_STAGES;
+#ifndef SQR_NN_GROUP
+#define SQR_NN_GROUP 16
+#endif
+constexpr int kNnGroup = SQR_NN_GROUP;  // M-tiles per raster group (gemm_nn)
 
 // ---------------------------------------------------------------- gemm_tn
 // Computed as D^T(N x M) = C^T(N x K) X(K x M): MMA rows = n, MMA cols = i.
@@ -473,7 +477,22 @@ __global__ void __launch_bounds__(kThreads, SQR_NN_CTAS)
     }
   }
   if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
-  const int m0 = blockIdx.x * Cfg::BM, n0 = blockIdx.y * Cfg::BN;
+  // Grouped raster: CTAs in launch order walk groups of kNnGroup M-tiles
+  // down all N-tiles, so the ~600 co-resident CTAs touch ~16 M-panels of X
+  // and ~37 N-panels of Y instead of every X panel (a 67 MB X at K = 2b
+  // would otherwise be re-fetched from DRAM by every wave).
+  int mt, nt_;
+  {
+    const int tm = gridDim.x, tn = gridDim.y;
+    const int lin = blockIdx.y * tm + blockIdx.x;
+    const int per = kNnGroup * tn;
+    const int first = (lin / per) * kNnGroup;
+    const int gsz = min(tm - first, kNnGroup);
+    const int r = lin % per;
+    mt = first + r % gsz;
+    nt_ = r / gsz;
+  }
+  const int m0 = mt * Cfg::BM, n0 = nt_ * Cfg::BN;
   if (n0 >= N) return;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t = lane & 3;

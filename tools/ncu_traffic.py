@@ -16,10 +16,13 @@ B = 128
 
 
 def algorithmic_bytes():
-    """C5 streaming bytes per kernel class: pass 1 reads the trailing matrix once
-    (Y^T C), pass 2 reads and writes it (C -= Y W); the sketch reads A once."""
+    """C5 streaming bytes per kernel class: every block's first sweep reads its
+    trailing matrix once (Y^T C); the second sweep runs once per block PAIR
+    (driver.cu trailing_second, K = 2b) and reads + writes the second block's
+    trailing matrix; the sketch reads A once."""
     c = sum((M - B * j) * (N - B * (j + 1)) * 8 for j in range(N // B))
-    return {"gemm_tn": c + M * N * 8, "gemm_nn": 2 * c}
+    c2 = sum((M - B * j) * (N - B * (j + 1)) * 8 for j in range(1, N // B, 2))
+    return {"gemm_tn": c + M * N * 8, "gemm_nn": 2 * c2}
 
 
 def main(src, dst):
