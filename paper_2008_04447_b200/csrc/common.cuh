@@ -229,9 +229,13 @@ int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
              int transpose, const int32_t* gate, cudaStream_t s);
 int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm, const int32_t* moves,
                 const sqr_status* st, int64_t max_moves, cudaStream_t s);
+int su_prep(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, int64_t bmax, double* mbuf,
+            sqr_status* st, int32_t* guard, cudaStream_t s);
 int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
-                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s);
-int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s);
+                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s,
+                  bool prepped = false);
+int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s,
+                 const int32_t* guard = nullptr);
 int iota(int64_t* p, int64_t n, cudaStream_t s);
 int zero_columns(double* W, int64_t ld, int64_t rows, int64_t ncols, const int32_t* lim, const int32_t* gate,
                  cudaStream_t s);

@@ -39,6 +39,7 @@ struct RqrcpWs {
   int64_t* lperm;
   int32_t* moves;
   int32_t* snap;  // {stop .. bhat} of the block whose bulk update is in flight
+  int32_t* guard; // R11 guard verdict of the early sample-update prep (EarlyPrep)
   void *sample, *panel;
   int64_t sample_bytes, panel_bytes;
   int64_t total;
@@ -66,6 +67,7 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.OmT = (need_omega || resample) ? c.take<double>(m * ell) : nullptr;
   w.pscr = c.take<double>(PanelScratch::doubles(b));
   w.snap = c.take<int32_t>(8);
+  w.guard = c.take<int32_t>(8);
   w.total = c.off + 256;
   return w;
 }
@@ -244,6 +246,44 @@ struct Lookahead {
   }
 };
 
+// M = S11 R11^-1 and the R11 guard of the sample update (sketch.py:132-149,
+// randomized.py:217-219) depend only on the block's factored sample and its
+// R11, both final right after the panel: they run on a high-priority side
+// stream concurrently with the trailing update (16 CTAs next to the GEMM)
+// instead of on the critical path between the update and the next sample
+// QRCP.  The guard verdict goes to a separate word that finish_block folds
+// into st->stop after the update, as the reference orders it.
+struct EarlyPrep {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~EarlyPrep() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
+  }
+  int init() {
+    int lo = 0, hi = 0;
+    SQR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SQR_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+    SQR_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    SQR_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    return SQR_OK;
+  }
+  int launch(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, int64_t bb, double* mbuf,
+             sqr_status* st, int32_t* guard, cudaStream_t s) {
+    SQR_CUDA(cudaEventRecord(fork, s));
+    SQR_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    const int rc = su_prep(Bf, ldbf, R, ldr, bb, mbuf, st, guard, side);
+    if (rc) return rc;
+    SQR_CUDA(cudaEventRecord(join, side));
+    return SQR_OK;
+  }
+  int wait(cudaStream_t s) {
+    SQR_CUDA(cudaStreamWaitEvent(s, join, 0));
+    return SQR_OK;
+  }
+};
+
 int pass2_split(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, const double* Y, int64_t ldy,
                 const double* W, int64_t ldw, sqr_status* st, int32_t* snap, cudaStream_t s, cudaEvent_t fork) {
   SQR_CUDA(cudaMemcpyAsync(snap, st, 6 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
@@ -367,6 +407,10 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
   if (!resample && (rc = la.init())) return rc;
   static const bool no_pair = getenv("SQR_NO_PAIRED_SWEEP") != nullptr;
   const bool pair = !resample && !la.on && !no_pair;
+  static const bool no_early = getenv("SQR_NO_EARLY_PREP") != nullptr;
+  EarlyPrep ep;
+  const bool early = !resample && !la.on && !no_early;
+  if (early && (rc = ep.init())) return rc;
   if (pair) SQR_CUDA(cudaMemset2DAsync(w.Ypan + b * m, m * 8, 0, b * 8, b, s));  // Y_J's zero top rows
   for (int64_t J = 0; J < nblk; ++J) {
     const int64_t i0 = J * b, bb = std::min(b, k - i0), nt = n - i0, mr = m - i0;
@@ -390,6 +434,8 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
         return rc;
     }
     if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
+    const bool prep = early && J + 1 < nblk && nt - bb > 0;
+    if (prep && (rc = ep.launch(w.Bf, ell, P, lda, bb, w.Gm, st, w.guard, s))) return rc;
     if (la.on) {
       // Second sweep split around the side stream (see Lookahead).
       if ((rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s,
@@ -418,7 +464,8 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     else
       rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s);
     if (rc) return rc;
-    if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s))) return rc;
+    if (prep && (rc = ep.wait(s))) return rc;
+    if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s, prep ? w.guard : nullptr))) return rc;
     if (J + 1 < nblk) {
       const int64_t a1 = i0 + bb;  // achieved if the block completed
       if (resample) {
@@ -429,7 +476,7 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
           return rc;
         stream_pos += (uint64_t)(ell * (m - a1));
       } else {
-        if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, bb, Bn, ell, st, w.Gm, s))) return rc;
+        if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, bb, Bn, ell, st, w.Gm, s, prep))) return rc;
       }
       std::swap(Bc, Bn);
     }

@@ -174,7 +174,7 @@ constexpr int kSuThreads = 256;
 constexpr int kSuRows = kSuThreads / 32;
 __global__ void __launch_bounds__(kSuThreads, 1)
     su_prep_kernel(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, double* Mout, int64_t ldm,
-                   int bmax, sqr_status* st) {
+                   int bmax, sqr_status* st, int32_t* guard) {
   extern __shared__ __align__(16) double Rs[];  // R11 transposed: Rs[l * P + c] = R(l, c), P odd
   __shared__ double rdiag[128];
   __shared__ double wmin[kSuRows];
@@ -212,8 +212,13 @@ __global__ void __launch_bounds__(kSuThreads, 1)
   const double d0 = bh > 0 ? fabs(rdiag[0]) : 0.0;
   dmin = fmin(dmin, d0);
   const bool ok = (bh > 0) && (dmin > 0x1p-52 * d0);
+  // With a guard word (su_prep launched early on a side stream, concurrent
+  // with the trailing update that reads st->stop) the verdict is only
+  // recorded; finish_block folds it into st->stop after the update, in the
+  // reference's order (randomized.py:212-219).
+  if (guard != nullptr && blockIdx.x == 0 && tid == 0) *guard = ok ? 0 : 1;
   if (!ok) {
-    if (blockIdx.x == 0 && tid == 0) {
+    if (guard == nullptr && blockIdx.x == 0 && tid == 0) {
       st->stop = 1;
       st->reason = SQR_STOP_R11_SINGULAR;
     }
@@ -266,7 +271,8 @@ __global__ void copy_s22_kernel(const double* Bf, int64_t ldbf, int ell, int nt,
 }
 
 // ----------------------------------------------------------- bookkeeping
-__global__ void finish_block_kernel(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n) {
+__global__ void finish_block_kernel(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n,
+                                    const int32_t* guard) {
   if (st->stop) return;
   const int bhat = st->bhat;
   const int achieved = i0 + bhat;
@@ -282,6 +288,9 @@ __global__ void finish_block_kernel(sqr_status* st, int32_t* widths, int i0, int
   } else if (n - achieved == 0) {
     st->stop = 1;
     st->reason = SQR_STOP_NO_TRAILING;
+  } else if (guard != nullptr && *guard) {
+    st->stop = 1;
+    st->reason = SQR_STOP_R11_SINGULAR;
   }
 }
 
@@ -379,9 +388,8 @@ int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm
   return SQR_OK;
 }
 
-int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
-                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s) {
-  if (nt <= 0) return SQR_OK;
+int su_prep(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, int64_t bmax, double* mbuf,
+            sqr_status* st, int32_t* guard, cudaStream_t s) {
   if (bmax > 128) {
     set_error("sample_update: block size %lld > 128", (long long)bmax);
     return SQR_EINVAL;
@@ -392,11 +400,23 @@ int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, 
     SQR_CUDA(cudaFuncSetAttribute(su_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     configured = smem;
   }
-  {
-    ProfScope ps(kTagSampleUpd, s);
-    su_prep_kernel<<<(unsigned)cdiv(bmax, (int64_t)kSuRows), kSuThreads, smem, s>>>(Bf, ldbf, R, ldr, mbuf, bmax,
-                                                                                  (int)bmax, st);
-    SQR_LAUNCH("su_prep_kernel");
+  // The early (guard-word) launch overlaps the trailing update on a side
+  // stream: it is not event-timed (its span would mostly be queueing).
+  if (guard == nullptr) prof_begin(kTagSampleUpd, s);
+  su_prep_kernel<<<(unsigned)cdiv(bmax, (int64_t)kSuRows), kSuThreads, smem, s>>>(Bf, ldbf, R, ldr, mbuf, bmax,
+                                                                                (int)bmax, st, guard);
+  if (guard == nullptr) prof_end(kTagSampleUpd, s);
+  SQR_LAUNCH("su_prep_kernel");
+  return SQR_OK;
+}
+
+int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
+                  int64_t bmax, double* Bn, int64_t ldbn, sqr_status* st, double* mbuf, cudaStream_t s,
+                  bool prepped) {
+  if (nt <= 0) return SQR_OK;
+  if (!prepped) {
+    const int rc = su_prep(Bf, ldbf, R, ldr, bmax, mbuf, st, nullptr, s);
+    if (rc) return rc;
   }
   // B_top = S12 - M R12 with the block size read on the device (== bmax
   // whenever the loop continues: a short block stops the factorization).
@@ -412,9 +432,10 @@ int sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double* R, 
   return SQR_OK;
 }
 
-int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s) {
+int finish_block(sqr_status* st, int32_t* widths, int i0, int bb, int k, int n, cudaStream_t s,
+                 const int32_t* guard) {
   ProfScope ps(kTagMisc, s);
-  finish_block_kernel<<<1, 1, 0, s>>>(st, widths, i0, bb, k, n);
+  finish_block_kernel<<<1, 1, 0, s>>>(st, widths, i0, bb, k, n, guard);
   SQR_LAUNCH("finish_block_kernel");
   return SQR_OK;
 }
