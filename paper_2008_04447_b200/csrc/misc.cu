@@ -159,6 +159,40 @@ __global__ void apply_moves_kernel(double* X, int64_t ld, int64_t rows, int64_t 
   }
 }
 
+// Register-staged variant for <= 256 moves: warp w of a 256-thread CTA owns
+// moves w, w+8, ..., w+248 of the CTA's 32 rows (one row per lane), issues
+// all of its <= 32 source loads before any store (every read of the CTA's
+// rows precedes every write after the barrier), then stores.  No shared
+// memory, ~8 CTAs/SM, so one wave covers m = 32768 rows with a single DRAM
+// round trip per CTA.
+__global__ void __launch_bounds__(256) apply_moves_reg_kernel(double* X, int64_t ld, int64_t rows, int64_t col0,
+                                                              int64_t* perm, const int32_t* moves,
+                                                              const sqr_status* st) {
+  if (st->stop) return;
+  const int nm = st->nmoves;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t r = (int64_t)blockIdx.x * 32 + lane;
+  const bool live = r < rows;
+  double v[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int mv = warp + 8 * i;
+    v[i] = (mv < nm && live) ? __ldcs(X + (col0 + moves[2 * mv + 1]) * ld + r) : 0.0;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int mv = warp + 8 * i;
+    if (mv < nm && live) __stcs(X + (col0 + moves[2 * mv]) * ld + r, v[i]);
+  }
+  if (perm != nullptr && blockIdx.x == 0) {
+    __shared__ int64_t pb[256];
+    for (int mv = threadIdx.x; mv < nm; mv += blockDim.x) pb[mv] = perm[col0 + moves[2 * mv + 1]];
+    __syncthreads();
+    for (int mv = threadIdx.x; mv < nm; mv += blockDim.x) perm[col0 + moves[2 * mv]] = pb[mv];
+  }
+}
+
 // ------------------------------------------------------------ sample update
 // B_next = [S12 - S11 R11^{-1} R12 ; S22]  (sketch.py:132-149).
 // su_prep (one CTA): the R11 diagonal guard (randomized.py:133-135) and
@@ -375,6 +409,13 @@ int gaussian(double* out, int64_t ld, int64_t rows, int64_t cols, uint64_t seed,
 int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm, const int32_t* moves,
                 const sqr_status* st, int64_t max_moves, cudaStream_t s) {
   if (rows <= 0 && perm == nullptr) return SQR_OK;
+  if (max_moves <= 256) {
+    const int blocks = (int)std::max<int64_t>(1, cdiv(rows, 32));
+    ProfScope ps(kTagMoves, s);
+    apply_moves_reg_kernel<<<blocks, 256, 0, s>>>(X, ld, rows, col0, perm, moves, st);
+    SQR_LAUNCH("apply_moves_reg_kernel");
+    return SQR_OK;
+  }
   const int64_t smem = std::max<int64_t>(max_moves, 1) * kMoveRows * 8;
   static int64_t configured = 0;
   if (smem > 48 * 1024 && smem > configured) {
