@@ -86,6 +86,37 @@ class BlockCyclic:
         return int(np.searchsorted(self.global_of_local(r), p))
 
 
+@dataclass
+class MovePlan:
+    """Rank r's share of one block's column moves (dst <- src, global
+    positions), in move order:
+      pack      local indices of the sources this rank owns (read first);
+      local     (packed row, local destination) pairs staying on this rank;
+      send[q]   packed rows going to peer q;
+      recv[q]   local destinations of the columns arriving from peer q.
+    Every source is packed before any destination is written, so the moves
+    act as one simultaneous permutation (randomized.py:194-195)."""
+
+    pack: np.ndarray
+    local_rows: np.ndarray
+    local_dst: np.ndarray
+    send: dict
+    recv: dict
+
+
+def move_plan(ps, pd, lay: BlockCyclic, r: int) -> MovePlan:
+    ps, pd = np.asarray(ps), np.asarray(pd)
+    osrc, odst = lay.owner(ps), lay.owner(pd)
+    lsrc, ldst = lay.local_index(ps), lay.local_index(pd)
+    mine = np.nonzero(osrc == r)[0]
+    loc = np.nonzero(odst[mine] == r)[0]
+    send = {int(q): np.nonzero(odst[mine] == q)[0] for q in sorted(set(odst[mine].tolist()) - {r})}
+    recv = {}
+    for q in sorted(set(osrc[odst == r].tolist()) - {r}):
+        recv[int(q)] = ldst[np.nonzero((odst == r) & (osrc == q))[0]]
+    return MovePlan(lsrc[mine], loc, ldst[mine[loc]], send, recv)
+
+
 # -------------------------------------------------------------------- comm
 class TorchComm:
     """torch.distributed with the process group's backend (NCCL on GPUs, gloo
@@ -362,19 +393,12 @@ class GpuOps:
 
     # 3. point-to-point column moves
     def move_columns(self, A, ps, pd, lay, comm):
-        r = comm.rank
         ld = A.shape[1]
-        osrc, odst = lay.owner(ps), lay.owner(pd)
-        lsrc, ldst = lay.local_index(ps), lay.local_index(pd)
-        mine = np.nonzero(osrc == r)[0]
-        loc = np.nonzero(odst[mine] == r)[0] if mine.size else np.zeros(0, np.int64)
-        peers_out = sorted(set(odst[mine].tolist()) - {r})
-        peers_in = sorted(set(osrc[odst == r].tolist()) - {r})
+        plan = move_plan(ps, pd, lay, comm.rank)
+        peers_out, peers_in = list(plan.send), list(plan.recv)
         # one upload for every index list of this block
-        pieces = [lsrc[mine], loc, ldst[mine[loc]]]
-        sel_out = {q: np.nonzero(odst[mine] == q)[0] for q in peers_out}
-        idx_in = {q: np.nonzero((odst == r) & (osrc == q))[0] for q in peers_in}
-        pieces += [sel_out[q] for q in peers_out] + [ldst[idx_in[q]] for q in peers_in]
+        pieces = ([plan.pack, plan.local_rows, plan.local_dst] + [plan.send[q] for q in peers_out]
+                  + [plan.recv[q] for q in peers_in])
         offs = np.cumsum([0] + [p.size for p in pieces])
         dev_idx = self._idx(np.concatenate(pieces) if offs[-1] else np.zeros(1, np.int64))
 
@@ -383,19 +407,19 @@ class GpuOps:
 
         sends, recv_shapes = {}, {}
         packed = None
-        if mine.size:
-            packed = torch.empty((mine.size, ld), dtype=torch.float64, device=self.dev)
+        if plan.pack.size:
+            packed = torch.empty((plan.pack.size, ld), dtype=torch.float64, device=self.dev)
             self._chk(self.L.sqr_copy_columns(A.data_ptr(), ld, ld, view(0).data_ptr(), packed.data_ptr(), ld, None,
-                                              mine.size, self._s()), "pack")
+                                              plan.pack.size, self._s()), "pack")
             for i, q in enumerate(peers_out):
                 sends[q] = packed.index_select(0, view(3 + i))
         for q in peers_in:
-            recv_shapes[q] = (int(idx_in[q].size), ld)
+            recv_shapes[q] = (int(plan.recv[q].size), ld)
         recvs = comm.exchange(sends, recv_shapes, A)
         # unpack: local moves then received columns, in move order per source
-        if loc.size:
+        if plan.local_rows.size:
             self._chk(self.L.sqr_copy_columns(packed.data_ptr(), ld, ld, view(1).data_ptr(), A.data_ptr(), ld,
-                                              view(2).data_ptr(), loc.size, self._s()), "unpack")
+                                              view(2).data_ptr(), plan.local_rows.size, self._s()), "unpack")
         for i, q in enumerate(peers_in):
             buf = recvs[q]
             self._chk(self.L.sqr_copy_columns(buf.data_ptr(), ld, ld, None, A.data_ptr(), ld,

@@ -5,7 +5,7 @@ import numpy as np
 import torch
 
 from oracle import port as O
-from paper_2008_04447_b200.distributed import _Panel, _Sample
+from paper_2008_04447_b200.distributed import _Panel, _Sample, move_plan
 
 
 class NumpyOps:
@@ -59,24 +59,16 @@ class NumpyOps:
         return _Sample(False, "none", st.achieved, moves, torch.from_numpy(np.ascontiguousarray(st.B.T)), st)
 
     def move_columns(self, A, ps, pd, lay, comm):
-        r = comm.rank
-        osrc, odst = lay.owner(ps), lay.owner(pd)
-        lsrc, ldst = lay.local_index(ps), lay.local_index(pd)
-        mine = np.nonzero(osrc == r)[0]
-        packed = A[torch.as_tensor(lsrc[mine])].clone() if mine.size else None
-        sends, shapes = {}, {}
-        for q in set(odst[mine].tolist()) - {r}:
-            sends[q] = packed[torch.as_tensor(np.nonzero(odst[mine] == q)[0])]
-        for q in set(osrc[odst == r].tolist()) - {r}:
-            shapes[q] = (int(np.count_nonzero((odst == r) & (osrc == q))), A.shape[1])
+        # the same plan GpuOps executes (distributed.move_plan)
+        plan = move_plan(ps, pd, lay, comm.rank)
+        packed = A[torch.as_tensor(plan.pack)].clone() if plan.pack.size else None
+        sends = {q: packed[torch.as_tensor(rows)] for q, rows in plan.send.items()}
+        shapes = {q: (int(dst.size), A.shape[1]) for q, dst in plan.recv.items()}
         recvs = comm.exchange(sends, shapes, A)
-        if mine.size:
-            loc = np.nonzero(odst[mine] == r)[0]
-            if loc.size:
-                A[torch.as_tensor(ldst[mine[loc]])] = packed[torch.as_tensor(loc)]
+        if plan.local_rows.size:
+            A[torch.as_tensor(plan.local_dst)] = packed[torch.as_tensor(plan.local_rows)]
         for q, buf in recvs.items():
-            idx = np.nonzero((odst == r) & (osrc == q))[0]
-            A[torch.as_tensor(ldst[idx])] = buf
+            A[torch.as_tensor(plan.recv[q])] = buf
 
     def panel(self, A, lc, i0, m, w, bb, is_owner):
         mr = m - i0

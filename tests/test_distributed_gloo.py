@@ -83,3 +83,36 @@ def test_layout_roundtrip():
             assert np.all(lay.owner(g) == r)
             assert np.array_equal(lay.local_index(g), np.arange(g.size))
         assert sum(lay.n_local(r) for r in range(P)) == n
+
+
+def test_move_plan_is_a_simultaneous_permutation():
+    """distributed.move_plan (used by both backends) applied rank by rank equals
+    the single-process column permutation, for random move sets."""
+    from paper_2008_04447_b200.distributed import BlockCyclic, move_plan
+    rng = np.random.default_rng(3)
+    for n, b, P in [(64, 8, 3), (100, 16, 4), (40, 4, 2)]:
+        lay = BlockCyclic(n, b, P)
+        for _ in range(20):
+            i0 = int(rng.integers(0, n - b))
+            k = int(rng.integers(1, b + 1))
+            # a block-style permutation: positions i0..i0+k receive k distinct sources
+            src = rng.choice(np.arange(i0, n), size=k, replace=False)
+            perm = np.arange(n)
+            for j, s in enumerate(src):
+                perm[[i0 + j, s]] = perm[[s, i0 + j]]
+            changed = np.nonzero(perm != np.arange(n))[0]
+            pd, ps = changed, perm[changed]
+            cols = np.arange(n, dtype=np.float64) * 10.0
+            want = cols[perm]
+            local = [cols[lay.global_of_local(r)].copy() for r in range(P)]
+            plans = [move_plan(ps, pd, lay, r) for r in range(P)]
+            packed = [local[r][p.pack].copy() for r, p in enumerate(plans)]
+            new = [x.copy() for x in local]
+            for r, p in enumerate(plans):
+                new[r][p.local_dst] = packed[r][p.local_rows]
+                for q, dst in p.recv.items():
+                    new[r][dst] = packed[q][plans[q].send[r]]
+            got = np.empty(n)
+            for r in range(P):
+                got[lay.global_of_local(r)] = new[r]
+            assert np.array_equal(got, want)
