@@ -12,6 +12,7 @@ from .factor import (PivotedFactorization, ReflectorBlock, TruncatedFactorizatio
                      apply_blocks_qt, blocks_q_columns, invert_permutation, qr_blocked, qrcp_blas2, qrcp_blocked,
                      rqrcp, rsrqrcp, ssrqrcp, trqrcp, tuxv, wy_compose)
 from .rng import NormalStream, device_giid, giid, normals
+from . import callers  # noqa: E402  (quality / estimators callers of the hot path)
 
 __all__ = [
     "CommCounters", "PivotedFactorization", "ReflectorBlock", "TruncatedFactorization", "TuxvResult",
