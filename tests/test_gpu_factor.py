@@ -222,3 +222,33 @@ def test_device_inputs_checked_and_untouched():
         Bc[3, 5] = bad
         with pytest.raises(ValueError, match="non-finite"):
             G.trqrcp(Bc, 10, b=8, p=4)
+
+
+def lowrank(m, n, r, seed, noise=0.0):
+    rng = np.random.default_rng(seed)
+    A = rng.standard_normal((m, r)) @ rng.standard_normal((r, n))
+    if noise:
+        A += noise * rng.standard_normal((m, n))
+    return np.asfortranarray(A)
+
+
+# Early exits landing on the first (P, second sweep deferred) or the second
+# (J, merged sweep) block of a pair: the paired second sweep must reproduce the
+# reference's loop exits, R rows and counters exactly (driver.cu trailing_first /
+# pending_panel_update / trailing_second).
+@pytest.mark.parametrize("m,n,k,b,r,noise,seed", [
+    (200, 180, 180, 16, 53, 0.0, 1),    # rank ends inside block 3 (a J block)
+    (200, 180, 180, 16, 39, 0.0, 2),    # rank ends inside block 2 (a P block)
+    (200, 180, 180, 16, 48, 0.0, 3),    # rank = 3 full blocks: sample floor at block 3
+    (200, 180, 180, 16, 64, 0.0, 4),    # rank = 4 full blocks: exit after a complete pair
+    (150, 170, 150, 16, 150, 0.0, 5),   # full rank, odd block count (10 blocks of 16, last 6 wide)
+    (300, 130, 130, 12, 130, 0.0, 6),   # 11 blocks: the last one unpaired
+    (120, 200, 100, 8, 60, 1e-13, 7),   # noise floor reached mid-pair
+])
+def test_paired_sweep_early_exits(m, n, k, b, r, noise, seed):
+    A = lowrank(m, n, r, seed, noise)
+    pf = G.rqrcp(A, k, b=b, p=8, seed=seed, omega="host")
+    ref = O.rqrcp(A, k, b=b, p=8, seed=seed)
+    check_against(pf, ref, A)
+    if pf.achieved_rank:
+        assert pf.rel_residual(A) <= 1e-12 * max(1.0, np.linalg.norm(A) / max(ref.r_diag[0], 1e-300))
