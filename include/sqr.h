@@ -214,6 +214,10 @@ int64_t sqr_block_workspace(int64_t m, int64_t ncols, int64_t b);
  * read of src.  *nonfinite is a device counter the caller zeroes. */
 int sqr_copy_check(const double* src, int64_t lds, int64_t m, int64_t n, double* dst, int64_t ldd,
                    unsigned long long* nonfinite, void* stream);
+/* Same for a ROW-major src (element (r, c) at src[r * lds + c], lds >= n, e.g. a
+ * C-ordered torch tensor) into column-major dst (tiled transpose). */
+int sqr_copy_check_t(const double* src, int64_t lds, int64_t m, int64_t n, double* dst, int64_t ldd,
+                     unsigned long long* nonfinite, void* stream);
 int sqr_copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* src_idx, double* dst,
                      int64_t ldd, const int64_t* dst_idx, int64_t n, void* stream);
 /* Panel QR of an mr x w panel (w <= 128), leaves + compact-WY updates; st->bhat/stop. */

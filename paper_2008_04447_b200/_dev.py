@@ -110,13 +110,31 @@ def _device_colmajor(A, device) -> int | None:
     return None
 
 
+def _device_rowmajor(A, device) -> int | None:
+    """Row stride if A is an fp64 CUDA tensor on `device` in row-major layout."""
+    if (isinstance(A, torch.Tensor) and A.is_cuda and A.device == torch.device(device) and A.dtype == torch.float64
+            and A.dim() == 2 and A.shape[0] > 0 and A.shape[1] > 0 and A.stride(1) == 1
+            and A.stride(0) >= A.shape[1]):
+        return int(A.stride(0))
+    return None
+
+
 def load_checked(A, device, copy: bool = True, check: bool = True) -> ColMajor:
     """The input contract of validation.check_matrix (validation.py:21-37) on
     the device: 2-D, finite, copied into fresh column-major storage (or, with
     copy=False and a column-major fp64 device input, wrapped read-only).  A
     column-major device input is copied and scanned in ONE pass."""
     lds = _device_colmajor(A, device)
-    if lds is not None:
+    rls = _device_rowmajor(A, device) if lds is None else None
+    if rls is not None:
+        # C-ordered device input: tiled transpose + scan in one pass
+        m, n = A.shape
+        M = ColMajor.empty(m, n, device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=device)
+        _lib.check(_lib.lib().sqr_copy_check_t(A.data_ptr(), rls, m, n, M.ptr, M.ld, cnt.data_ptr(), stream_handle()),
+                   "sqr_copy_check_t")
+        bad = int(cnt.item()) if check else 0
+    elif lds is not None:
         m, n = A.shape
         if copy:
             M = ColMajor.empty(m, n, device)

@@ -65,6 +65,7 @@ SIGNATURES = {
                              c_ptr]),
     "sqr_block_workspace": (c_i64, [c_i64, c_i64, c_i64]),
     "sqr_copy_check": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
+    "sqr_copy_check_t": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
     "sqr_copy_columns": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_panel_factor": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_int, c_ptr, c_ptr, c_i64,
                                  c_ptr]),

@@ -388,6 +388,40 @@ __global__ void copy_check_kernel(const double* __restrict__ src, int64_t lds, i
   if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nonfinite, (unsigned long long)bad);
 }
 
+// Row-major source (element (r, c) at src[r * lds + c]) into column-major
+// dst, + the non-finite count: 32 x 32 tiles through padded shared memory so
+// both the reads (along c) and the writes (along r) are coalesced.
+__global__ void __launch_bounds__(256) copy_check_t_kernel(const double* __restrict__ src, int64_t lds, int64_t m,
+                                                           int64_t n, double* __restrict__ dst, int64_t ldd,
+                                                           unsigned long long* nonfinite) {
+  __shared__ double tile[32][33];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8 threads
+  const int64_t tiles_c = (n + 31) / 32, tiles = ((m + 31) / 32) * tiles_c;
+  unsigned bad = 0;
+  for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+    const int64_t r0 = (t / tiles_c) * 32, c0 = (t % tiles_c) * 32;
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      const int64_t r = r0 + ty + i, c = c0 + tx;
+      double v = 0.0;
+      if (r < m && c < n) {
+        v = __ldcs(src + r * lds + c);
+        bad += isfinite(v) ? 0u : 1u;
+      }
+      tile[ty + i][tx] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 32; i += 8) {
+      const int64_t c = c0 + ty + i, r = r0 + tx;
+      if (r < m && c < n) __stcs(dst + c * ldd + r, tile[tx][ty + i]);
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(nonfinite, (unsigned long long)bad);
+}
+
 __global__ void iota_kernel(int64_t* p, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = i;
@@ -578,6 +612,22 @@ extern "C" int sqr_copy_check(const double* src, int64_t lds, int64_t m, int64_t
   sqr::ProfScope ps(sqr::kTagMisc, s);
   sqr::copy_check_kernel<<<blocks, 256, 0, s>>>(src, lds, m, n, dst, ldd, nonfinite);
   SQR_LAUNCH("copy_check_kernel");
+  return SQR_OK;
+}
+
+extern "C" int sqr_copy_check_t(const double* src, int64_t lds, int64_t m, int64_t n, double* dst, int64_t ldd,
+                                unsigned long long* nonfinite, void* stream) {
+  if (m <= 0 || n <= 0) return SQR_OK;
+  if (lds < n || dst == nullptr || ldd < m || nonfinite == nullptr) {
+    sqr::set_error("sqr_copy_check_t: bad leading dimension or NULL argument");
+    return SQR_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int64_t tiles = sqr::cdiv(m, 32) * sqr::cdiv(n, 32);
+  const int blocks = (int)std::min<int64_t>(tiles, (int64_t)sqr::sm_count() * 8);
+  sqr::ProfScope ps(sqr::kTagMisc, s);
+  sqr::copy_check_t_kernel<<<blocks, 256, 0, s>>>(src, lds, m, n, dst, ldd, nonfinite);
+  SQR_LAUNCH("copy_check_t_kernel");
   return SQR_OK;
 }
 

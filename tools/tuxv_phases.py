@@ -14,7 +14,7 @@ dev = torch.device("cuda", 0)
 n = int(os.environ.get("N", "20000"))
 G1 = G.device_giid(n, 100, 41, device=dev)
 G2 = G.device_giid(n, 100, 42, device=dev)
-S = G1 @ G2.T
+S = (G2 @ G1.T).T  # column-major (Fortran) like the reference's arrays
 S /= torch.linalg.norm(S)
 A = S + 1e-6 * G.device_giid(n, n, 43, device=dev)
 del S
