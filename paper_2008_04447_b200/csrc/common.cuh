@@ -3,12 +3,19 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/sqr.h"
 
 namespace sqr {
 
 constexpr int kWarp = 32;
+
+// Debug / A-B switches: set, non-empty and not "0".
+inline bool env_flag(const char* name) {
+  const char* e = getenv(name);
+  return e != nullptr && *e != '\0' && !(e[0] == '0' && e[1] == '\0');
+}
 
 // ----------------------------------------------------------------- error state
 void set_error(const char* fmt, ...);

@@ -81,7 +81,7 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
 int panel_factor(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t wstat, double* Y, int64_t ldy,
                  double* taus, int stop_at_zero, sqr_status* st, void* pws, int64_t pwsb, const PanelScratch& sc,
                  double* gws, cudaStream_t s) {
-  static const bool no_block = getenv("SQR_NO_BLOCKPANEL") != nullptr;
+  static const bool no_block = env_flag("SQR_NO_BLOCKPANEL");
   if (!no_block && mr <= panel_block_max_rows() && bb <= 128)
     return panel_block(P, lda, mr, wstat, bb, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s);
   int rc;
@@ -405,9 +405,9 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
   double* Bn = w.Bnext;
   Lookahead la;
   if (!resample && (rc = la.init())) return rc;
-  static const bool no_pair = getenv("SQR_NO_PAIRED_SWEEP") != nullptr;
+  static const bool no_pair = env_flag("SQR_NO_PAIRED_SWEEP");
   const bool pair = !resample && !la.on && !no_pair;
-  static const bool no_early = getenv("SQR_NO_EARLY_PREP") != nullptr;
+  static const bool no_early = env_flag("SQR_NO_EARLY_PREP");
   EarlyPrep ep;
   const bool early = !resample && !la.on && !no_early;
   if (early && (rc = ep.init())) return rc;

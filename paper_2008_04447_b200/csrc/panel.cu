@@ -546,7 +546,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   }
   const int sms = sm_count();
   const int64_t mrl0 = mr - c0;
-  if (wmax <= kLW && mrl0 <= (int64_t)std::min(sms, 148) * kLThreads * 2 && getenv("SQR_NO_LEAF") == nullptr) {
+  if (wmax <= kLW && mrl0 <= (int64_t)std::min(sms, 148) * kLThreads * 2 && !env_flag("SQR_NO_LEAF")) {
     // register-resident leaf kernel: one (or two) rows per thread
     const int rpt = mrl0 <= (int64_t)std::min(sms, 148) * kLThreads ? 1 : 2;
     const int G = (int)cdiv(mrl0, (int64_t)kLThreads * rpt);

@@ -18,6 +18,8 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace sqr {
@@ -676,6 +678,7 @@ __global__ void __launch_bounds__(kSqThreads, 1) sample_qrcp_kernel(SampleArgs a
 // sample_qrcp_kernel.
 constexpr int kRT = 256;
 constexpr int kRR = 48;  // register rows
+constexpr int kMaxEllCl = 144;  // sample rows supported by the cluster variant
 
 // shared-memory pair load the compiler may not CSE (keeps 64 y values from
 // staying live across the dot and the update loops)
@@ -709,8 +712,18 @@ __device__ __forceinline__ void add_move(const RegArgs& a, int dst, int src) {
   a.moves[2 * slot + 1] = src;
 }
 
+// CL = true: the whole grid is ONE thread-block cluster (<= 16 CTAs, n_t <=
+// 4096): the per-step candidate exchange goes through distributed shared
+// memory (each CTA's record and candidate column stay in its own shared
+// memory, readers map them with map_shared_rank) and the grid barrier is
+// the hardware cluster barrier (arrive.release / wait.acquire), instead of
+// L2 records, a fence and an atomic counter.
+template <bool CL>
 __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   extern __shared__ __align__(16) double sm[];
+  __shared__ __align__(16) double2 crec_s[2][16];    // CL: every CTA's candidate record (pushed), per parity
+  __shared__ __align__(16) double ccol_s[2][kMaxEllCl];  // CL: my candidate column per step parity
+  __shared__ double xs_s[2];                         // CL: my (sum, max) of the initial norms
   const int ell = a.ell, RS = a.RS;
   const int YP = ((max(ell, RS + kRR) + 1) | 1) + 1;  // even pitch of a reflector buffer
   double* cs = sm;                                     // [RS][kRT]
@@ -728,7 +741,8 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   __shared__ Bcast bc_s;
   if (a.st->stop) return;
   GridBarrier gb;
-  gb.init(a.bar);
+  if (!CL) gb.init(a.bar);
+  namespace cg = cooperative_groups;
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int col = g * kRT + tid;
@@ -774,15 +788,29 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     if (tid == 0) {
       for (int i = 1; i < (kRT >> 5); ++i) mx = fmax(mx, sred[i]);
       mx = fmax(mx, sred[0]);
-      a.psum[g] = s;
-      a.pmax[g] = mx;
+      if (CL) {
+        xs_s[0] = s;
+        xs_s[1] = mx;
+      } else {
+        a.psum[g] = s;
+        a.pmax[g] = mx;
+      }
     }
   }
-  gb.sync();
   double total = 0.0, gmax = 0.0;
-  for (int i = 0; i < G; ++i) {
-    total += __ldcg(a.psum + i);
-    gmax = fmax(gmax, __ldcg(a.pmax + i));
+  if (CL) {
+    cg::this_cluster().sync();
+    for (int i = 0; i < G; ++i) {
+      const double* rx = cg::this_cluster().map_shared_rank(xs_s, i);
+      total += rx[0];
+      gmax = fmax(gmax, rx[1]);
+    }
+  } else {
+    gb.sync();
+    for (int i = 0; i < G; ++i) {
+      total += __ldcg(a.psum + i);
+      gmax = fmax(gmax, __ldcg(a.pmax + i));
+    }
   }
   const double fro = sqrt(total);
   const double rank_floor_sq = (kRankFloor * fro) * (kRankFloor * fro);
@@ -794,6 +822,7 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       a.st->reason = SQR_STOP_SAMPLE_FLOOR;
       a.st->sample_achieved = 0;
     }
+    if (CL) cg::this_cluster().sync();  // peers may still be reading my xs_s
     return;
   }
   if (g == 0 && tid == 0 && a.first) a.st->floor_sq = sample_floor;
@@ -814,9 +843,17 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     int l = lane < (kRT >> 5) ? wl_s[lane] : -1;
     warp_argmax(v, p, l);
     const int par = jn & 1;
-    if (tid == 0) a.cand[par * G + g] = make_double2(v, __longlong_as_double((long long)p));
+    if (CL) {
+      // push my record into every peer's shared memory (lane q -> CTA q):
+      // after the cluster barrier each reader finds all records locally
+      if (warp == 0 && lane < G)
+        *cg::this_cluster().map_shared_rank(&crec_s[par][g], lane) =
+            make_double2(v, __longlong_as_double((long long)p));
+    } else if (tid == 0) {
+      a.cand[par * G + g] = make_double2(v, __longlong_as_double((long long)p));
+    }
     if (l >= 0 && warp == (l >> 5)) {
-      double* dst = a.ccol + ((size_t)par * G + g) * ell;
+      double* dst = CL ? ccol_s[par] : a.ccol + ((size_t)par * G + g) * ell;
       if (tid == l) {
 #pragma unroll
         for (int q = 0; q < kRR; q += 2) *reinterpret_cast<double2*>(stg + q) = make_double2(xr[q], xr[q + 1]);
@@ -839,7 +876,11 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
         const int i = lane + 32 * k;
-        rec[k] = i < G ? __ldcg(a.cand + par * G + i) : make_double2(-1.0, __longlong_as_double((long long)INT_MAX));
+        if (CL)
+          rec[k] = i < G ? crec_s[par][i] : make_double2(-1.0, __longlong_as_double((long long)INT_MAX));
+        else
+          rec[k] = i < G ? __ldcg(a.cand + par * G + i)
+                         : make_double2(-1.0, __longlong_as_double((long long)INT_MAX));
       }
 #pragma unroll
       for (int k = 0; k < 5; ++k) {
@@ -857,11 +898,12 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     double s1 = 0.0, nrm = 0.0, beta = 0.0, tau = 0.0, y0 = 1.0;
     const bool go = bv > rank_floor_sq;  // reference.py:123-124
     if (go) {
-      const double* u = a.ccol + ((size_t)par * G + bl) * ell + jn;
+      const double* u = CL ? cg::this_cluster().map_shared_rank(ccol_s[par], bl) + jn
+                           : a.ccol + ((size_t)par * G + bl) * ell + jn;
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = lane + 32 * i;
-        x[i] = r < len ? __ldcg(u + r) : 0.0;
+        x[i] = r < len ? (CL ? u[r] : __ldcg(u + r)) : 0.0;
       }
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i)
@@ -893,6 +935,17 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   // (wcol, y), by threads [t0, kRT): rows outer, columns inner (coalesced)
   auto smem_update = [&](int jd, int t0) {
     const double* yp = ybuf(jd & 1);
+    if (t0 == 32) {
+      // warps 1..7 (224 threads): thread t owns column t (its w in a
+      // register) for all rows, and rows jd + w' + 7k of column 224 + lane
+      // of the last 32 columns: 8/7 of a column per thread, 2 shared loads
+      // + 1 store per cell (no per-cell w reload)
+      const int t = tid - 32, lw = t >> 5;
+      const double wc = wcol[t], wx = wcol[224 + lane];
+      for (int r = jd; r < RS; ++r) cs[r * kRT + t] = fma(-yp[r], wc, cs[r * kRT + t]);
+      for (int r = jd + lw; r < RS; r += 7) cs[r * kRT + 224 + lane] = fma(-yp[r], wx, cs[r * kRT + 224 + lane]);
+      return;
+    }
     const int nthr = kRT - t0;
     const int ncell = (RS - jd) * kRT;
     for (int e = tid - t0; e < ncell; e += nthr) {
@@ -902,7 +955,10 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   };
 
   publish(0);
-  gb.sync();
+  if (CL)
+    cg::this_cluster().sync();
+  else
+    gb.sync();
   if (warp == 0) winner(0);
   __syncthreads();
 
@@ -990,10 +1046,18 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     if (j + 1 < a.bb) {
       publish(j + 1);
       SQR_TRACE(a.trace, 8 * j + 2);
-      gb.arrive();
+      if (CL) {
+        __syncthreads();  // publish read the candidate's shared-memory rows
+        asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      } else {
+        gb.arrive();
+      }
       SQR_TRACE(a.trace, 8 * j + 3);
       if (warp == 0) {
-        if (lane == 0) gb.wait_lane0();
+        if (CL)
+          asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+        else if (lane == 0)
+          gb.wait_lane0();
         if (lane == 0) SQR_TRACE(a.trace, 8 * j + 6);
         __syncwarp();
         winner(j + 1);
@@ -1001,6 +1065,7 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       } else {
         smem_update(j, 32);
         if (a.trace && g == 0 && tid == 32) a.trace[8 * j + 5] = gtimer();  // deferred update done
+        if (CL) asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
       }
       __syncthreads();
       SQR_TRACE(a.trace, 8 * j + 4);
@@ -1011,6 +1076,7 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     }
   }
   __syncthreads();
+  if (CL) cg::this_cluster().sync();  // no CTA leaves while a peer may read its records
   // remaining columns go to their final positions
   if (pos >= 0) {
     double* dst = a.Bf + (int64_t)pos * a.ldbf;
@@ -1039,6 +1105,42 @@ struct SampleWorkspace {
   }
 };
 
+// Largest cluster the register sample kernel can be launched with (16 with
+// the non-portable opt-in where the GPCs allow it, else 8), probed once.
+int cluster_max() {
+  static int cmax = -1;
+  if (cmax >= 0) return cmax;
+  cmax = 0;
+  const int smem = (int)(((int64_t)(144 - kRR) * kRT + 2 * 152 + 2 + kRT) * 8);
+  if (cudaFuncSetAttribute(sample_qrcp_reg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    return cmax;
+  }
+  cudaFuncSetAttribute(sample_qrcp_reg_kernel<true>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaGetLastError();
+  for (int c : {16, 8}) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(c);
+    cfg.blockDim = dim3(kRT);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = c;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, sample_qrcp_reg_kernel<true>, &cfg) == cudaSuccess && n > 0) {
+      cmax = c;
+      break;
+    }
+    cudaGetLastError();
+  }
+  return cmax;
+}
+
 int64_t sample_qrcp_workspace(int64_t ell, int64_t nt) { return SampleWorkspace::bytes(ell, nt); }
 
 int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf,
@@ -1054,7 +1156,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     return SQR_EINVAL;
   }
   const int sms = sm_count();
-  static const bool no_reg = getenv("SQR_NO_REGSAMPLE") != nullptr;
+  static const bool no_reg = env_flag("SQR_NO_REGSAMPLE");
   if (!no_reg && ell <= 144 && nt <= (int64_t)std::min(sms, 148) * kRT) {
     RegArgs a{};
     a.B = B;
@@ -1084,16 +1186,43 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     const int G = (int)std::max<int64_t>(1, cdiv(nt, (int64_t)kRT));
     const int YP = (int)(((std::max<int64_t>(ell, a.RS + kRR) + 1) | 1) + 1);
     const int smem = (int)(((int64_t)a.RS * kRT + 2 * YP + 2 + kRT) * 8);
-    static int configured = 0;
+    static int configured = 0, configured_cl = 0;
     if (smem > configured) {
-      SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    smem));
       configured = smem;
+    }
+    // One cluster when the sample fits 16 CTAs (the hardware cluster
+    // barrier and DSMEM exchange; measured per-step cost in DESIGN.md).
+    static const bool no_cl = env_flag("SQR_NO_CLUSTER_SAMPLE");
+    if (!no_cl && G <= cluster_max() && ell <= kMaxEllCl) {
+      if (smem > configured_cl) {
+        SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      smem));
+        configured_cl = smem;
+      }
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(G);
+      cfg.blockDim = dim3(kRT);
+      cfg.dynamicSmemBytes = (size_t)smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = G;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      ProfScope ps(kTagSample, s);
+      count_launch();
+      SQR_CUDA(cudaLaunchKernelEx(&cfg, sample_qrcp_reg_kernel<true>, a));
+      return SQR_OK;
     }
     void* args[] = {&a};
     SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
     ProfScope ps(kTagSample, s);
     count_launch();
-    SQR_CUDA(cudaLaunchCooperativeKernel((const void*)sample_qrcp_reg_kernel, dim3(G), dim3(kRT), args,
+    SQR_CUDA(cudaLaunchCooperativeKernel((const void*)sample_qrcp_reg_kernel<false>, dim3(G), dim3(kRT), args,
                                          (size_t)smem, s));
     return SQR_OK;
   }
