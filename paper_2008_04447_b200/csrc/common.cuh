@@ -116,28 +116,35 @@ struct GridBarrier {
   // Split phases: arrive() publishes this CTA's prior writes; wait() (any
   // one warp may call it, the caller's thread 0 polls) returns once every
   // CTA has arrived.  sync() = arrive + wait.
+  // red.release is cumulative over the CTA's writes ordered before it by
+  // the bar.sync (one MEMBAR.GPU in SASS; an explicit fence.acq_rel in front
+  // of it only adds a second one), and the acquire poll (LDG.STRONG.GPU +
+  // L1 invalidate, no MEMBAR) synchronises with every arrival through the
+  // counter's release sequence.  SQR_GB_FENCE builds the fenced variant.
   __device__ void arrive() {
     __syncthreads();
     target += nblocks;
     if (threadIdx.x == 0) {
+#ifdef SQR_GB_FENCE
       asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+#endif
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
     }
   }
   __device__ void wait_lane0() {  // call from lane 0 of one warp
-    while ((int)(ld_relaxed_u32(ctr) - target) < 0) {
+    while ((int)(ld_acquire_u32(ctr) - target) < 0) {
     }
-    asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
   }
   __device__ void sync() {
     __syncthreads();
     target += nblocks;
     if (threadIdx.x == 0) {
+#ifdef SQR_GB_FENCE
       asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
+#endif
       asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(ctr) : "memory");
-      while ((int)(ld_relaxed_u32(ctr) - target) < 0) {
+      while ((int)(ld_acquire_u32(ctr) - target) < 0) {
       }
-      asm volatile("fence.acq_rel.gpu;\n" ::: "memory");
     }
     __syncthreads();
   }
