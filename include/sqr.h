@@ -105,7 +105,7 @@ int sqr_gemm_nn_ws(int64_t M, int64_t N, int64_t K, double alpha, const double* 
  * _qrcp_core:107-150) on a persistent cooperative kernel.  Writes the
  * factored sample in pivoted order to Bf (l x nt, ldbf), the local
  * permutation lperm[pos] = source column (int64, nt), the list of moved
- * positions moves[2*i] = dst, moves[2*i+1] = src (int32, <= 2*bb pairs) and
+ * positions moves[2*i] = dst, moves[2*i+1] = src (int32, <= 2*bb pairs; dst = -1 marks an unused slot) and
  * st->sample_achieved / st->nmoves.  first != 0 also sets st->floor_sq from
  * this sample (randomized.py:179-180).  Skipped when st->stop is set. */
 int sqr_sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb,

@@ -137,7 +137,7 @@ __global__ void apply_moves_kernel(double* X, int64_t ld, int64_t rows, int64_t 
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int m = m0 + u * nw;
-      v[u] = (m < nm && r < rows) ? __ldcs(X + (col0 + moves[2 * m + 1]) * ld + r) : 0.0;
+      v[u] = (m < nm && r < rows && moves[2 * m] >= 0) ? __ldcs(X + (col0 + moves[2 * m + 1]) * ld + r) : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -148,14 +148,16 @@ __global__ void apply_moves_kernel(double* X, int64_t ld, int64_t rows, int64_t 
   __syncthreads();
   for (int m = warp; m < nm; m += nw) {
     const int dst = moves[2 * m];
-    if (r < rows) X[(col0 + dst) * ld + r] = buf[m * kMoveRows + lane];
+    if (r < rows && dst >= 0) X[(col0 + dst) * ld + r] = buf[m * kMoveRows + lane];
   }
   if (perm != nullptr && blockIdx.x == 0) {
     __syncthreads();
     int64_t* pb = reinterpret_cast<int64_t*>(buf);
-    for (int m = threadIdx.x; m < nm; m += blockDim.x) pb[m] = perm[col0 + moves[2 * m + 1]];
+    for (int m = threadIdx.x; m < nm; m += blockDim.x)
+      if (moves[2 * m] >= 0) pb[m] = perm[col0 + moves[2 * m + 1]];
     __syncthreads();
-    for (int m = threadIdx.x; m < nm; m += blockDim.x) perm[col0 + moves[2 * m]] = pb[m];
+    for (int m = threadIdx.x; m < nm; m += blockDim.x)
+      if (moves[2 * m] >= 0) perm[col0 + moves[2 * m]] = pb[m];
   }
 }
 
@@ -177,19 +179,21 @@ __global__ void __launch_bounds__(256) apply_moves_reg_kernel(double* X, int64_t
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const int mv = warp + 8 * i;
-    v[i] = (mv < nm && live) ? __ldcs(X + (col0 + moves[2 * mv + 1]) * ld + r) : 0.0;
+    v[i] = (mv < nm && live && moves[2 * mv] >= 0) ? __ldcs(X + (col0 + moves[2 * mv + 1]) * ld + r) : 0.0;
   }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
     const int mv = warp + 8 * i;
-    if (mv < nm && live) __stcs(X + (col0 + moves[2 * mv]) * ld + r, v[i]);
+    if (mv < nm && live && moves[2 * mv] >= 0) __stcs(X + (col0 + moves[2 * mv]) * ld + r, v[i]);
   }
   if (perm != nullptr && blockIdx.x == 0) {
     __shared__ int64_t pb[256];
-    for (int mv = threadIdx.x; mv < nm; mv += blockDim.x) pb[mv] = perm[col0 + moves[2 * mv + 1]];
+    for (int mv = threadIdx.x; mv < nm; mv += blockDim.x)
+      if (moves[2 * mv] >= 0) pb[mv] = perm[col0 + moves[2 * mv + 1]];
     __syncthreads();
-    for (int mv = threadIdx.x; mv < nm; mv += blockDim.x) perm[col0 + moves[2 * mv]] = pb[mv];
+    for (int mv = threadIdx.x; mv < nm; mv += blockDim.x)
+      if (moves[2 * mv] >= 0) perm[col0 + moves[2 * mv]] = pb[mv];
   }
 }
 

@@ -748,7 +748,15 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   const int col = g * kRT + tid;
   const bool own = col < a.nt;
   auto ybuf = [&](int par) -> double* { return ybase + par * YP + yoff; };
-  if (g == 0 && tid == 0) a.st->nmoves = 0;
+  // Moves without atomics (an atomicAdd round trip in the pivot's CTA sat on
+  // the critical path of every step): slot j <- the pivot of step j, slot
+  // bb + j <- the column displaced at step j if that is where it ends; -1
+  // marks a no-op.  CTA 0 pre-fills 2*bb slots before the first barrier.
+  if (g == 0) {
+    for (int e = tid; e < 4 * a.bb; e += kRT) a.moves[e] = -1;
+    if (tid == 0) a.st->nmoves = 2 * a.bb;
+  }
+  int disp = -1;  // step at which my column was last displaced
   for (int e = tid; e < 2 * YP; e += kRT) ybase[e] = 0.0;  // zero rows beyond ell (ell < 64)
 
   // ---- load my column: rows [0, RS) to shared memory, [RS, ell) to registers
@@ -984,10 +992,18 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       bfj[j] = beta;
       for (int r = j + 1; r < ell; ++r) bfj[r] = yf[r];
       a.lperm[j] = col;
-      if (col != j) add_move(a, j, col);
+      if (col != j) {
+        a.moves[2 * j] = j;
+        a.moves[2 * j + 1] = col;
+      }
+      if (disp >= 0) a.moves[2 * (a.bb + disp)] = -1;  // superseded displacement
       pos = -1;
     } else if (pos >= 0) {
       const int pn = (pos == j) ? pc : pos;  // the column at position j moves to pc
+      if (pos == j) {
+        if (disp >= 0) a.moves[2 * (a.bb + disp)] = -1;
+        disp = j;
+      }
       pos = pn;
       double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
       {
@@ -1085,7 +1101,12 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     for (int q = 0; q < kRR; ++q)
       if (RS + q < ell) dst[RS + q] = xr[q];
     a.lperm[pos] = col;
-    if (pos != col) add_move(a, pos, col);
+    if (disp >= 0 && pos != col) {
+      a.moves[2 * (a.bb + disp)] = pos;
+      a.moves[2 * (a.bb + disp) + 1] = col;
+    } else if (disp >= 0) {
+      a.moves[2 * (a.bb + disp)] = -1;
+    }
   }
   if (g == 0 && tid == 0) {
     a.st->sample_achieved = achieved;

@@ -388,6 +388,7 @@ class GpuOps:
         reason = {2: "sample_floor", 3: "sample_rank"}.get(int(s["reason"]), "none")
         nm = int(s["nmoves"])
         mv = h[128:128 + 8 * nm].view(np.int32).reshape(nm, 2).astype(np.int64)
+        mv = mv[(mv[:, 0] >= 0) & (mv[:, 0] != mv[:, 1])]  # drop no-op slots (dst = -1) and self-moves
         self._keep.clear()
         return _Sample(stop, reason, int(s["sample_achieved"]), mv, self.Bf[:max(nt, 1)], st)
 

@@ -112,6 +112,8 @@ def test_sample_qrcp_matches_oracle(ell, nt, bb, seed):
     assert relerr(got[a:, a:], st_ref.S22) <= 1e-11
     assert relerr(taus.cpu().numpy()[:a], st_ref.u_block.tau) <= 1e-12
     mv = moves.cpu().numpy()[: 2 * int(s["nmoves"])].reshape(-1, 2)
+    mv = mv[mv[:, 0] >= 0]  # dst = -1 marks an unused slot
+    assert np.unique(mv[:, 0]).size == mv.shape[0] and np.unique(mv[:, 1]).size == mv.shape[0]
     lp = np.arange(nt)
     lp[mv[:, 0]] = mv[:, 1]
     assert np.array_equal(lp, st_ref.local_perm)
