@@ -757,6 +757,8 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     if (tid == 0) a.st->nmoves = 2 * a.bb;
   }
   int disp = -1;  // step at which my column was last displaced
+  int pj = -1;     // step at which my column became the pivot
+  double pbeta = 0.0;
   for (int e = tid; e < 2 * YP; e += kRT) ybase[e] = 0.0;  // zero rows beyond ell (ell < 64)
 
   // ---- load my column: rows [0, RS) to shared memory, [RS, ell) to registers
@@ -983,20 +985,12 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     cbl = -1;
     double wvv = 0.0;
     if (pos == pc) {
-      // the pivot: R part rows < j, beta, reflector tail -> Bf column j
-      double* bfj = a.Bf + (int64_t)j * a.ldbf;
-      for (int r = 0; r < min(j, RS); ++r) bfj[r] = cs[r * kRT + tid];
-#pragma unroll
-      for (int q = 0; q < kRR; ++q)
-        if (RS + q < j) bfj[RS + q] = xr[q];
-      bfj[j] = beta;
-      for (int r = j + 1; r < ell; ++r) bfj[r] = yf[r];
-      a.lperm[j] = col;
-      if (col != j) {
-        a.moves[2 * j] = j;
-        a.moves[2 * j + 1] = col;
-      }
-      if (disp >= 0) a.moves[2 * (a.bb + disp)] = -1;  // superseded displacement
+      // the pivot: its column is frozen from here on (w = 0 in every later
+      // update), so Bf column j (R part, beta, reflector tail u / (u_j -
+      // beta)) is written after the loop -- no global stores in the step
+      // that the grid barrier's release would have to wait for
+      pj = j;
+      pbeta = beta;
       pos = -1;
     } else if (pos >= 0) {
       const int pn = (pos == j) ? pc : pos;  // the column at position j moves to pc
@@ -1093,6 +1087,34 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   }
   __syncthreads();
   if (CL) cg::this_cluster().sync();  // no CTA leaves while a peer may read its records
+  if (pj >= 0) {
+    // pivot of step pj -> Bf column pj, exactly as the winner built it
+    // (y_r = u_r / y0 with y0 = u_pj - beta; y = 0 for a zero column)
+    double* bfj = a.Bf + (int64_t)pj * a.ldbf;
+    const double u0 = pj < RS ? cs[pj * kRT + tid] : [&] {
+      double v = 0.0;
+#pragma unroll
+      for (int q = 0; q < kRR; ++q)
+        if (RS + q == pj) v = xr[q];
+      return v;
+    }();
+    const double y0 = u0 - pbeta;
+    for (int r = 0; r < RS; ++r) {
+      const double u = cs[r * kRT + tid];
+      bfj[r] = r < pj ? u : (r == pj ? pbeta : (pbeta != 0.0 ? u / y0 : 0.0));
+    }
+#pragma unroll
+    for (int q = 0; q < kRR; ++q) {
+      const int r = RS + q;
+      if (r < ell) bfj[r] = r < pj ? xr[q] : (r == pj ? pbeta : (pbeta != 0.0 ? xr[q] / y0 : 0.0));
+    }
+    a.lperm[pj] = col;
+    if (col != pj) {
+      a.moves[2 * pj] = pj;
+      a.moves[2 * pj + 1] = col;
+    }
+    if (disp >= 0) a.moves[2 * (a.bb + disp)] = -1;  // superseded displacement
+  }
   // remaining columns go to their final positions
   if (pos >= 0) {
     double* dst = a.Bf + (int64_t)pos * a.ldbf;
