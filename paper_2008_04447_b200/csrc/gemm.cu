@@ -49,14 +49,24 @@ constexpr int kNnGroup = SQR_NN_GROUP;  // M-tiles per raster group (gemm_nn)
 // ---------------------------------------------------------------- gemm_tn
 // Computed as D^T(N x M) = C^T(N x K) X(K x M): MMA rows = n, MMA cols = i.
 // CTA tile: 64 n x MT i;  4 warps = 2 (n) x 2 (i);  warp tile 32 n x MT/2 i.
+#ifndef SQR_TN_BK
+#define SQR_TN_BK 16
+#endif
+#ifndef SQR_TN_STAGES
+#define SQR_TN_STAGES 3
+#endif
 template <int MT, int VEC>
 struct TnCfg {
   static constexpr int BN = 64;
   static constexpr int NI = MT / 16;  // n8 fragments per warp along i
-  static constexpr int A_ELEMS = BN * kPitchK;
-  static constexpr int B_ELEMS = MT * kPitchK;
+  // K per stage / ring depth (two CTAs per SM must fit: the 144-row tile keeps 16 x 3)
+  static constexpr int BK = MT <= 128 ? SQR_TN_BK : 16;
+  static constexpr int NST = MT <= 128 ? SQR_TN_STAGES : 3;
+  static constexpr int PK = BK + 4;   // pitch of a k-row (4 mod 16 doubles)
+  static constexpr int A_ELEMS = BN * PK;
+  static constexpr int B_ELEMS = MT * PK;
   static constexpr int STAGE = A_ELEMS + B_ELEMS;
-  static constexpr int SMEM = STAGE * kStages * 8;
+  static constexpr int SMEM = STAGE * NST * 8;
   static constexpr int ACC = 2 * NI * 4;
 };
 
@@ -65,7 +75,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
                                               int64_t ldx, const double* __restrict__ C, int64_t ldc,
                                               int M, int N, int n0, int k0, int kend, const GemmDyn& dyn) {
   using Cfg = TnCfg<MT, VEC>;
-  constexpr int CPR = kBK / VEC;  // chunks per row
+  constexpr int CPR = Cfg::BK / VEC;  // chunks per row
   const int tid = threadIdx.x;
 #pragma unroll 4
   for (int c = tid; c < Cfg::BN * CPR; c += kThreads) {
@@ -75,7 +85,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
     const double* src = !ok ? C
                             : (n < dyn.npre ? dyn.pre + (int64_t)n * dyn.ldpre + k
                                             : C + (int64_t)(n - dyn.npre) * ldc + k);
-    double* dst = sA + r * kPitchK + kc;
+    double* dst = sA + r * Cfg::PK + kc;
     if constexpr (VEC == 2) {
       const int sz = ok ? ((k + 1 < kend) ? 16 : 8) : 0;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
@@ -90,7 +100,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
     const int k = k0 + kc;
     const bool ok = (r < M) && (k < kend);
     const double* src = ok ? X + (int64_t)r * ldx + k : X;
-    double* dst = sB + r * kPitchK + kc;
+    double* dst = sB + r * Cfg::PK + kc;
     if constexpr (VEC == 2) {
       const int sz = ok ? ((k + 1 < kend) ? 16 : 8) : 0;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(dst)), "l"(src),
@@ -106,6 +116,7 @@ __device__ __forceinline__ void tn_load_stage(double* sA, double* sB, const doub
 // one add and one cp.async per 16-byte chunk.
 template <int MT>
 struct TnLoader2 {
+  static constexpr int kBK = TnCfg<MT, 2>::BK, kPitchK = TnCfg<MT, 2>::PK;
   static constexpr int CPR = kBK / 2;             // 16-byte chunks per k-row
   static constexpr int RSTEP = kThreads / CPR;    // rows covered per pass
   static constexpr int NA = 64 / RSTEP;
@@ -187,6 +198,7 @@ __global__ void __launch_bounds__(kThreads, 2)
   const int split = blockIdx.y, nsplit = gridDim.y;
   const int kbeg = split * kchunk;
   const int kend = min(K, kbeg + kchunk);
+  constexpr int kBK = Cfg::BK, kPitchK = Cfg::PK, kStages = Cfg::NST;
   const int nk = kend > kbeg ? (int)cdiv(kend - kbeg, kBK) : 0;
 
   double acc[2][Cfg::NI][4];
@@ -646,7 +658,7 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
       best = sp;
     }
   }
-  int kchunk = (int)rup(cdiv(K, best), kBK);
+  int kchunk = (int)rup(cdiv(K, best), Cfg::BK);
   int nsplit = (int)cdiv(K, kchunk);
   if (nsplit < 1) nsplit = 1;
   double* part = nullptr;
