@@ -208,11 +208,28 @@ def _apply_blocks(blocks, C: ColMajor, transpose: bool) -> ColMajor:
         if blk.width == 0:
             continue
         Yd, _, Td = blk.device_parts(dev)
+        if blk.width > MAX_ELL:
+            # composed blocks wider than the fused kernel's 144 (e.g. TUXV's U / V
+            # for k > 144): C -= Y op(T) (Y^T C) with the chunked DMMA GEMMs
+            if C.n == 0:
+                continue
+            Wt = gemm_tn(Yd, C)                          # j x n
+            Tm = Td if not transpose else _transpose(Td)
+            W = gemm_nn(Tm, Wt)                          # op(T) Y^T C
+            YW = gemm_nn(Yd, W)
+            C.view().sub_(YW.view())
+            continue
         ws = _ws(2 * blk.width * max(C.n, 1) * 8 + (200 << 20), dev)
         _lib.check(_lib.lib().sqr_apply_wy(Yd.ptr, Yd.ld, Td.ptr, Td.ld, Yd.m, blk.width, C.ptr, C.ld, C.n,
                                            1 if transpose else 0, ptr(ws), ws.numel(), stream_handle()),
                    "sqr_apply_wy")
     return C
+
+
+def _transpose(M: ColMajor) -> ColMajor:
+    out = ColMajor.empty(M.n, M.m, M.t.device)
+    out.view().copy_(M.view().T)
+    return out
 
 
 def _q_columns_dev(blocks, m: int, r: int, dev) -> ColMajor:
@@ -549,7 +566,8 @@ def _qr_blocked_dev(M: ColMajor, k: int, b: int) -> PivotedFactorization:
     pf._permd = torch.arange(n, device=dev)
     # all k reflectors as ONE compact-WY block (what _compose_all of the
     # per-block list gives, householder.py:94-104): one masked copy + T from G
-    pf._composed_fn = lambda: _packed_blocks(M, taus, None, k, [(0, k)], m)[0]
+    pf._composed_fn = (lambda: [_packed_blocks(M, taus, None, k, [(0, k)], m)[0]]) if k <= MAX_ELL \
+        else (lambda: pf.blocks)
     if bk == b:
         pf._blocks_fn = lambda: _packed_blocks(M, taus, Tb, bk, widths, m)
     else:  # reference blocking with b > 128: same reflectors, regrouped
@@ -794,7 +812,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     cnt.merge(vf.counters)
     # the flip-flop passes use each factor as one composed block (QLP: U, V
     # of the result are the compositions, randomized.py:344-350, 396-406)
-    v_blocks, u_blocks = [vf._composed_fn()], []
+    v_blocks, u_blocks = vf._composed_fn(), []
     X = vf.R_device(dev)[:kh, :kh].T.contiguous()
     for j in range(1, j_max + 1):
         if j % 2 == 1:
@@ -804,7 +822,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
             cnt.add_blas3(m, n, kh)
             uf = _qr_blocked_dev(Z, kh, b)
             cnt.merge(uf.counters)
-            u_blocks = [uf._composed_fn()]
+            u_blocks = uf._composed_fn()
             X = uf.R_device(dev)[:kh, :kh].contiguous()
         else:
             Uk = _q_columns_dev(u_blocks, m, kh, dev)
@@ -815,7 +833,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
             cnt.add_blas3(kh, m, n)
             vf = _qr_blocked_dev(Z, kh, b)
             cnt.merge(vf.counters)
-            v_blocks = [vf._composed_fn()]
+            v_blocks = vf._composed_fn()
             X = vf.R_device(dev)[:kh, :kh].T.contiguous()
     sig = torch.abs(torch.diagonal(X))
     if refine_sigma:

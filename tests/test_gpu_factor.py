@@ -252,3 +252,15 @@ def test_paired_sweep_early_exits(m, n, k, b, r, noise, seed):
     check_against(pf, ref, A)
     if pf.achieved_rank:
         assert pf.rel_residual(A) <= 1e-12 * max(1.0, np.linalg.norm(A) / max(ref.r_diag[0], 1e-300))
+
+
+def test_tuxv_wider_than_one_wy_kernel_block():
+    """k > 144: the QLP factors are composed blocks wider than the fused
+    apply kernel (factor._apply_blocks falls back to the chunked GEMMs)."""
+    A = lowrank(420, 380, 170, 9, noise=1e-3)
+    res = G.tuxv(A, 160, b=32, p=8, seed=4, omega="host", allow_large_k=True)
+    ref = O.tuxv(A, 160, b=32, p=8, seed=4, allow_large_k=True)
+    assert res.achieved_rank == ref.achieved_rank == 160
+    assert np.abs(res.reconstruct() - ref.reconstruct()).max() <= 1e-9 * np.abs(A).max()
+    U = res.u_columns()
+    assert np.abs(U.T @ U - np.eye(160)).max() <= 1e-12
