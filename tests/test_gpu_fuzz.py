@@ -95,3 +95,44 @@ def test_fuzz_rsrqrcp(i):
     pf = G.rsrqrcp(A, k, b=b, p=p, seed=seed)
     ref = O.rsrqrcp(A, k, b=b, p=p, seed=seed)
     check_fuzz(pf, ref, A)
+
+
+EDGE = [
+    # (m, n, k, b, p, rank)      what it reaches
+    (50, 40, 40, 1, 0, 40),      # b = 1, p = 0
+    (60, 50, 1, 16, 8, 50),      # k = 1
+    (30, 60, 30, 32, 8, 30),     # l >= m: the blocked-QRCP fallback
+    (200, 180, 180, 128, 16, 180),  # l = 144, the widest sample
+    (150, 40000, 150, 16, 8, 150),  # n_t > 148*256: the shared-memory sample kernel
+    (40000, 100, 100, 32, 8, 100),  # mr > 148*256: the leaf panel path
+    (80000, 70, 70, 64, 8, 70),     # mr > 2*148*256: the generic panel kernel
+    (300, 300, 300, 32, 8, 0),      # all-zero input
+]
+
+
+@pytest.mark.parametrize("case", EDGE, ids=lambda c: "x".join(map(str, c)))
+def test_edge_shapes(case):
+    m, n, k, b, p, r = case
+    rng = np.random.default_rng(m * 7 + n)
+    if r == 0:
+        A = np.zeros((m, n), order="F")
+    else:
+        A = np.asfortranarray(rng.standard_normal((m, r)) @ rng.standard_normal((r, n)) if r < min(m, n)
+                              else rng.standard_normal((m, n)))
+    pf = G.rqrcp(A, k, b=b, p=p, seed=5, omega="host")
+    ref = O.rqrcp(A, k, b=b, p=p, seed=5)
+    check_fuzz(pf, ref, A)
+    kt = max(1, min(k, min(m, n) // 2))
+    tf = G.trqrcp(A, kt, b=b, p=p, seed=5, omega="host")
+    tref = O.trqrcp(A, kt, b=b, p=p, seed=5)
+    check_fuzz(tf, tref, A)
+
+
+@pytest.mark.parametrize("j_max,refine", [(2, False), (3, True)])
+def test_tuxv_flip_flops(j_max, refine):
+    rng = np.random.default_rng(11)
+    A = np.asfortranarray(rng.standard_normal((300, 40)) @ np.diag(0.7 ** np.arange(40)) @ rng.standard_normal((40, 260)))
+    res = G.tuxv(A, 20, j_max=j_max, b=8, p=8, seed=2, refine_sigma=refine, omega="host")
+    ref = O.tuxv(A, 20, j_max=j_max, b=8, p=8, seed=2, refine_sigma=refine)
+    assert np.abs(res.reconstruct() - ref.reconstruct()).max() <= 1e-9 * np.abs(A).max()
+    np.testing.assert_allclose(np.abs(res.sigma_est), np.abs(ref.sigma_est), rtol=1e-10)
