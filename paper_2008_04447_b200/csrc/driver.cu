@@ -85,8 +85,11 @@ int panel_factor(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t wstat, 
   if (!no_block && mr <= panel_block_max_rows() && bb <= 128)
     return panel_block(P, lda, mr, wstat, bb, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s);
   int rc;
-  for (int64_t c0 = 0; c0 < bb; c0 += kLeaf) {
-    const int64_t lwe = std::min(kLeaf, bb - c0);
+  // 16-wide leaves when the panel needs 3-4 rows per thread (register file)
+  const int64_t rows1 = (int64_t)std::min(sm_count(), 148) * 256;
+  const int64_t leaf = (mr > 2 * rows1 && mr <= 4 * rows1) ? 16 : kLeaf;
+  for (int64_t c0 = 0; c0 < bb; c0 += leaf) {
+    const int64_t lwe = std::min(leaf, bb - c0);
     if ((rc = panel_qr(P, lda, mr, wstat, lwe, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s, c0))) return rc;
     const int64_t rest = bb - (c0 + lwe);
     if (rest <= 0 || mr - c0 <= 0) continue;

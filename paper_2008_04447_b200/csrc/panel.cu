@@ -360,12 +360,14 @@ constexpr int kLThreads = 256;
 constexpr int kLWarps = kLThreads / 32;
 constexpr int kLW = 32;
 
-template <int RPT>
+// LW = leaf width (32, or 16 for very tall panels where RPT = 3..4 rows per
+// thread must fit the register file).
+template <int RPT, int LW>
 __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
-  __shared__ double red[kLWarps][kLW];
-  __shared__ double vals[kLW];
-  __shared__ double rowv[kLW];
-  __shared__ double wv[kLW];
+  __shared__ double red[kLWarps][LW];
+  __shared__ double vals[LW];
+  __shared__ double rowv[LW];
+  __shared__ double wv[LW];
   if (a.st->stop) return;
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -386,34 +388,35 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
   GridBarrier gb;
   gb.init(a.bar);
   int rows[RPT];
-  double x[RPT][kLW];
+  double x[RPT][LW];
 #pragma unroll
   for (int i = 0; i < RPT; ++i) {
     rows[i] = g * kLThreads * RPT + i * kLThreads + tid;
 #pragma unroll
-    for (int c = 0; c < kLW; ++c)
+    for (int c = 0; c < LW; ++c)
       x[i][c] = (rows[i] < a.mr && c < w) ? a.P[(int64_t)c * a.ldp + rows[i]] : 0.0;
   }
   int bhat = w;
   SQR_TRACE(a.trace, 8 * 40 + 1);
 #pragma unroll
-  for (int t = 0; t < kLW; ++t) {
+  for (int t = 0; t < LW; ++t) {
     if (t >= w) break;
     const int par = t & 1;
     // ---- partials of step t over my rows > t: q[0] = |a|^2, q[v] = a . P_{t+v}
-    double q[kLW];
+    double q[LW];
 #pragma unroll
-    for (int v = 0; v < kLW; ++v) q[v] = 0.0;
+    for (int v = 0; v < LW; ++v) q[v] = 0.0;
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       const bool in = rows[i] > t;
       const double av = in ? x[i][t] : 0.0;
 #pragma unroll
-      for (int v = 0; v < kLW - t; ++v) q[v] = fma(av, x[i][t + v], q[v]);
+      for (int v = 0; v < LW - t; ++v) q[v] = fma(av, x[i][t + v], q[v]);
     }
-    // ---- warp transpose butterfly: lane l ends with the warp sum of value l
+    // ---- warp transpose butterfly: lane l ends with the warp sum of value
+    // l mod LW (for LW = 16 the two 16-lane halves are added at the end)
 #pragma unroll
-    for (int k = 16; k >= 1; k >>= 1) {
+    for (int k = LW / 2; k >= 1; k >>= 1) {
       const bool upper = (lane & k) != 0;
 #pragma unroll
       for (int i = 0; i < k; ++i) {
@@ -422,30 +425,31 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
         q[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
       }
     }
-    red[warp][lane] = q[0];
+    if (LW < 32) q[0] += __shfl_xor_sync(0xffffffffu, q[0], 16);
+    if (lane < LW) red[warp][lane] = q[0];
     __syncthreads();
-    if (tid < kLW - t) {
+    if (tid < LW - t) {
       double s = 0.0;
 #pragma unroll
       for (int wi = 0; wi < kLWarps; ++wi) s += red[wi][tid];
-      a.part[((size_t)par * (kLW + 1) + tid) * G + g] = s;
+      a.part[((size_t)par * (LW + 1) + tid) * G + g] = s;
     }
     // the owner of row t (CTA 0, thread t) publishes it
     if (g == 0 && tid == t) {
 #pragma unroll
-      for (int v = 0; v < kLW - t; ++v) a.rowt[par * (kLW + 1) + v] = x[0][t + v];
+      for (int v = 0; v < LW - t; ++v) a.rowt[par * (LW + 1) + v] = x[0][t + v];
     }
     SQR_TRACE(a.trace, 8 * t + 1);
     gb.sync();
     SQR_TRACE(a.trace, 8 * t + 2);
     {
-      const int L = min(kLW - t, w - t);
-      if (tid < L) rowv[tid] = __ldcg(a.rowt + par * (kLW + 1) + tid);
+      const int L = min(LW - t, w - t);
+      if (tid < L) rowv[tid] = __ldcg(a.rowt + par * (LW + 1) + tid);
       // 8 lanes per value (32 values x 8 = 256 threads), G/8 loads each in flight
       const int v = tid >> 3, qd = tid & 7;
       if (v < L) {
         double xr[kMaxG / 8];
-        const double* src = a.part + ((size_t)par * (kLW + 1) + v) * G;
+        const double* src = a.part + ((size_t)par * (LW + 1) + v) * G;
 #pragma unroll
         for (int i = 0; i < kMaxG / 8; ++i) {
           const int gi = qd + 8 * i;
@@ -475,7 +479,7 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
       y0 = at - beta;
       tau = 2.0 / (1.0 + sa / (y0 * y0));
     }
-    if (tid >= 1 && tid < min(kLW - t, w - t)) wv[tid] = tau * (rowv[tid] + vals[tid] / y0);
+    if (tid >= 1 && tid < min(LW - t, w - t)) wv[tid] = tau * (rowv[tid] + vals[tid] / y0);
     if (g == 0 && tid == 0) a.taus[t] = tau;
     __syncthreads();
     // ---- apply reflector t to my rows (row t keeps beta and its R entries)
@@ -485,11 +489,11 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
         const double yr = nrm != 0.0 ? x[i][t] / y0 : 0.0;
         x[i][t] = yr;
 #pragma unroll
-        for (int v = 1; v < kLW - t; ++v) x[i][t + v] = fma(-yr, wv[v], x[i][t + v]);
+        for (int v = 1; v < LW - t; ++v) x[i][t + v] = fma(-yr, wv[v], x[i][t + v]);
       } else if (rows[i] == t) {
         x[i][t] = beta;
 #pragma unroll
-        for (int v = 1; v < kLW - t; ++v) x[i][t + v] -= wv[v];
+        for (int v = 1; v < LW - t; ++v) x[i][t + v] -= wv[v];
       }
     }
     SQR_TRACE(a.trace, 8 * t + 4);
@@ -500,7 +504,7 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
     const int R = rows[i];
     if (R >= a.mr) continue;
 #pragma unroll
-    for (int c = 0; c < kLW; ++c) {
+    for (int c = 0; c < LW; ++c) {
       if (c < w) a.P[(int64_t)c * a.ldp + R] = x[i][c];
       if (c < a.wmax) {
         const double y = c < bhat ? (R > c ? x[i][c] : (R == c ? 1.0 : 0.0)) : 0.0;
@@ -546,9 +550,11 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   }
   const int sms = sm_count();
   const int64_t mrl0 = mr - c0;
-  if (wmax <= kLW && mrl0 <= (int64_t)std::min(sms, 148) * kLThreads * 2 && !env_flag("SQR_NO_LEAF")) {
-    // register-resident leaf kernel: one (or two) rows per thread
-    const int rpt = mrl0 <= (int64_t)std::min(sms, 148) * kLThreads ? 1 : 2;
+  const int64_t rows1 = (int64_t)std::min(sms, 148) * kLThreads;  // one row per thread
+  const bool narrow = wmax <= 16 && mrl0 > 2 * rows1 && mrl0 <= 4 * rows1;  // 16-wide leaves, 3-4 rows
+  if ((narrow || (wmax <= kLW && mrl0 <= 2 * rows1)) && !env_flag("SQR_NO_LEAF")) {
+    // register-resident leaf kernel: one to four rows per thread
+    const int rpt = (int)cdiv(mrl0, rows1);
     const int G = (int)cdiv(mrl0, (int64_t)kLThreads * rpt);
     PanelArgs a{};
     a.P = P;
@@ -573,7 +579,10 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
     SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
     ProfScope ps(kTagPanel, s);
     count_launch();
-    const void* fn = rpt == 1 ? (const void*)leaf_kernel<1> : (const void*)leaf_kernel<2>;
+    const void* fn = rpt == 1   ? (const void*)leaf_kernel<1, 32>
+                     : rpt == 2 ? (const void*)leaf_kernel<2, 32>
+                     : rpt == 3 ? (const void*)leaf_kernel<3, 16>
+                                : (const void*)leaf_kernel<4, 16>;
     SQR_CUDA(cudaLaunchCooperativeKernel(fn, dim3(G), dim3(kLThreads), args, 0, s));
     return SQR_OK;
   }
