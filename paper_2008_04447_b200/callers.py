@@ -71,29 +71,32 @@ def presort_columns(A):
     return np.asfortranarray(Ms.cpu().numpy()), order_h
 
 
+def _presorted_qr(A, k, b):
+    As, order = presort_columns(A)
+    pf = F.qr_blocked(As, k, b)
+    pf.perm = order
+    return pf
+
+
+# quality.py names -> device call (A, k, b, p, seed, omega, presort)
+_FACTORIZATIONS = {
+    "qrcp2": lambda A, k, b, p, s, om, ps: F.qrcp_blas2(A, k),
+    "qrcp3": lambda A, k, b, p, s, om, ps: F.qrcp_blocked(A, k, b),
+    "qr": lambda A, k, b, p, s, om, ps: _presorted_qr(A, k, b) if ps else F.qr_blocked(A, k, b),
+    "ssrqrcp": lambda A, k, b, p, s, om, ps: F.ssrqrcp(A, k, p=p, seed=s, omega=om),
+    "rqrcp": lambda A, k, b, p, s, om, ps: F.rqrcp(A, k, b=b, p=p, seed=s, omega=om),
+    "rsrqrcp": lambda A, k, b, p, s, om, ps: F.rsrqrcp(A, k, b=b, p=p, seed=s),
+    "trqrcp": lambda A, k, b, p, s, om, ps: F.trqrcp(A, k, b=b, p=p, seed=s, allow_large_k=True, omega=om),
+}
+
+
 def make_factorization(A, algorithm, k, b, p, seed, presort_qr: bool = False, omega=None):
-    """quality.py:96-117 (names: qrcp2 = BLAS-2 QRCP, qrcp3 = blocked QRCP,
-    qr = unpivoted blocked QR, optionally on norm-presorted columns)."""
-    if algorithm == "qrcp2":
-        return F.qrcp_blas2(A, k)
-    if algorithm == "qrcp3":
-        return F.qrcp_blocked(A, k, b)
-    if algorithm == "qr":
-        if presort_qr:
-            As, order = presort_columns(A)
-            pf = F.qr_blocked(As, k, b)
-            pf.perm = order
-            return pf
-        return F.qr_blocked(A, k, b)
-    if algorithm == "ssrqrcp":
-        return F.ssrqrcp(A, k, p=p, seed=seed, omega=omega)
-    if algorithm == "rqrcp":
-        return F.rqrcp(A, k, b=b, p=p, seed=seed, omega=omega)
-    if algorithm == "rsrqrcp":
-        return F.rsrqrcp(A, k, b=b, p=p, seed=seed)
-    if algorithm == "trqrcp":
-        return F.trqrcp(A, k, b=b, p=p, seed=seed, allow_large_k=True, omega=omega)
-    raise ValueError(f"unknown algorithm {algorithm!r}")
+    """quality.py:96-117 (qrcp2 = BLAS-2 QRCP, qrcp3 = blocked QRCP, qr =
+    unpivoted blocked QR, optionally on norm-presorted columns)."""
+    make = _FACTORIZATIONS.get(algorithm)
+    if make is None:
+        raise ValueError(f"unknown algorithm {algorithm!r}")
+    return make(A, k, b, p, seed, omega, presort_qr)
 
 
 def _device_matrix(A):
@@ -161,21 +164,48 @@ except ImportError:  # pragma: no cover
     BaseEstimator = TransformerMixin = object
     check_array = check_random_state = check_is_fitted = None
 
-# estimators.py:23-30
-_PIVOTED = {"qrcp": F.qrcp_blas2, "qrcp_blocked": F.qrcp_blocked, "ssrqrcp": F.ssrqrcp, "rqrcp": F.rqrcp,
-            "rsrqrcp": F.rsrqrcp, "trqrcp": F.trqrcp}
 
-
-def _resolve_seed(random_state) -> int:
-    """estimators.py:33-40: integers feed the counter-based stream directly."""
+def _seed_of(random_state) -> int:
+    """estimators.py:33-40: an integer feeds the counter-based stream as is
+    (masked to 64 bits); anything else draws one through sklearn."""
     if isinstance(random_state, numbers.Integral):
         return int(random_state) & 0xFFFFFFFFFFFFFFFF
-    rs = check_random_state(random_state)
-    return int(rs.randint(0, 2**63 - 1))
+    return int(check_random_state(random_state).randint(0, 2**63 - 1))
 
 
-class RandomizedPivotedQR(TransformerMixin, BaseEstimator):
-    """Column subset selection by randomized pivoted QR (estimators.py:43-126)."""
+# estimators.py:23-30 names -> device call (X, k, b, p, seed, omega); the QRCP
+# oracles ignore the seed, trqrcp is called with allow_large_k like the reference
+_SELECTORS = {
+    "qrcp": lambda X, k, b, p, s, om: F.qrcp_blas2(X, k),
+    "qrcp_blocked": lambda X, k, b, p, s, om: F.qrcp_blocked(X, k, b),
+    "ssrqrcp": lambda X, k, b, p, s, om: F.ssrqrcp(X, k, p=p, seed=s, omega=om),
+    "rqrcp": lambda X, k, b, p, s, om: F.rqrcp(X, k, b=b, p=p, seed=s, omega=om),
+    "rsrqrcp": lambda X, k, b, p, s, om: F.rsrqrcp(X, k, b=b, p=p, seed=s),
+    "trqrcp": lambda X, k, b, p, s, om: F.trqrcp(X, k, b=b, p=p, seed=s, allow_large_k=True, omega=om),
+}
+
+
+class _DeviceTransformer(TransformerMixin, BaseEstimator):
+    """Shared input handling of the two wrappers."""
+
+    def _fit_input(self, X):
+        X = check_array(X, dtype=np.float64, order="F")
+        k = int(self.rank)
+        if k < 1 or k > min(X.shape):
+            raise ValueError(f"rank must be in [1, min(m, n)], got {k}")
+        return X, k
+
+    def _new_input(self, X, attr):
+        check_is_fitted(self, attr)
+        X = check_array(X, dtype=np.float64)
+        if X.shape[1] != self.n_features_in_:
+            raise ValueError(f"X has {X.shape[1]} features, expected {self.n_features_in_}")
+        return X
+
+
+class RandomizedPivotedQR(_DeviceTransformer):
+    """Column subset selection by a pivoted factorization on the device
+    (estimators.py:43-126): `transform` keeps the rank_ leading pivot columns."""
 
     def __init__(self, rank=8, algorithm="rqrcp", block_size=32, padding=8, random_state=None, omega=None):
         self.rank = rank
@@ -187,44 +217,26 @@ class RandomizedPivotedQR(TransformerMixin, BaseEstimator):
 
     def fit(self, X, y=None):
         X = check_array(X, dtype=np.float64, order="F")
-        if self.algorithm not in _PIVOTED:
-            raise ValueError(f"algorithm must be one of {sorted(_PIVOTED)}, got {self.algorithm!r}")
-        k = int(self.rank)
-        if not 1 <= k <= min(X.shape):
-            raise ValueError(f"rank must be in [1, min(m, n)], got {k}")
-        seed = _resolve_seed(self.random_state)
-        b, p = int(self.block_size), int(self.padding)
-        if self.algorithm == "qrcp":
-            pf = F.qrcp_blas2(X, k)
-        elif self.algorithm == "qrcp_blocked":
-            pf = F.qrcp_blocked(X, k, b)
-        elif self.algorithm == "ssrqrcp":
-            pf = F.ssrqrcp(X, k, p=p, seed=seed, omega=self.omega)
-        elif self.algorithm == "trqrcp":
-            pf = F.trqrcp(X, k, b=b, p=p, seed=seed, allow_large_k=True, omega=self.omega)
-        elif self.algorithm == "rsrqrcp":
-            pf = F.rsrqrcp(X, k, b=b, p=p, seed=seed)
-        else:
-            pf = F.rqrcp(X, k, b=b, p=p, seed=seed, omega=self.omega)
+        select = _SELECTORS.get(self.algorithm)
+        if select is None:
+            raise ValueError(f"algorithm must be one of {sorted(_SELECTORS)}, got {self.algorithm!r}")
+        X, k = self._fit_input(X)
+        pf = select(X, k, int(self.block_size), int(self.padding), _seed_of(self.random_state), self.omega)
         self.factorization_ = pf
-        self.permutation_ = pf.perm.copy()
         self.rank_ = pf.achieved_rank
-        self.selected_columns_ = pf.perm[: self.rank_].copy()
-        self.r_diagonal_ = pf.r_diag.copy()
+        self.permutation_ = np.array(pf.perm, copy=True)
+        self.selected_columns_ = self.permutation_[: self.rank_].copy()
+        self.r_diagonal_ = np.array(pf.r_diag, copy=True)
         self.n_features_in_ = X.shape[1]
         return self
 
     def transform(self, X):
-        check_is_fitted(self, "selected_columns_")
-        X = check_array(X, dtype=np.float64)
-        if X.shape[1] != self.n_features_in_:
-            raise ValueError(f"X has {X.shape[1]} features, expected {self.n_features_in_}")
-        return X[:, self.selected_columns_]
+        return self._new_input(X, "selected_columns_")[:, self.selected_columns_]
 
 
-class TruncatedQLP(TransformerMixin, BaseEstimator):
-    """Truncated SVD approximation by flip-flop QLP on a sketched QR
-    (estimators.py:129-186); components_ = V^T of the TUXV factorization."""
+class TruncatedQLP(_DeviceTransformer):
+    """TruncatedSVD-like surface over TUXV (estimators.py:129-186):
+    components_ = V^T, singular_values_ = sigma_est, middle_ = X."""
 
     def __init__(self, rank=8, flip_flops=1, block_size=32, padding=8, refine_sigma=True, random_state=None,
                  omega=None):
@@ -241,30 +253,21 @@ class TruncatedQLP(TransformerMixin, BaseEstimator):
         return self
 
     def fit_transform(self, X, y=None):
-        X = check_array(X, dtype=np.float64, order="F")
-        k = int(self.rank)
-        if not 1 <= k <= min(X.shape):
-            raise ValueError(f"rank must be in [1, min(m, n)], got {k}")
-        res = F.tuxv(X, k, b=int(self.block_size), p=int(self.padding), seed=_resolve_seed(self.random_state),
-                     j_max=int(self.flip_flops), refine_sigma=bool(self.refine_sigma), allow_large_k=True,
+        X, k = self._fit_input(X)
+        res = F.tuxv(X, k, j_max=int(self.flip_flops), b=int(self.block_size), p=int(self.padding),
+                     seed=_seed_of(self.random_state), refine_sigma=bool(self.refine_sigma), allow_large_k=True,
                      omega=self.omega)
         V = res.v_columns()
-        self.result_ = res
-        self.rank_ = res.achieved_rank
+        self.result_, self.rank_ = res, res.achieved_rank
         self.components_ = np.ascontiguousarray(V.T)
-        self.singular_values_ = np.asarray(res.sigma_est).copy()
-        self.middle_ = np.asarray(res.X).copy()
+        self.singular_values_ = np.array(res.sigma_est, copy=True)
+        self.middle_ = np.array(res.X, copy=True)
         self.n_features_in_ = X.shape[1]
         return X @ V
 
     def transform(self, X):
-        check_is_fitted(self, "components_")
-        X = check_array(X, dtype=np.float64)
-        if X.shape[1] != self.n_features_in_:
-            raise ValueError(f"X has {X.shape[1]} features, expected {self.n_features_in_}")
-        return X @ self.components_.T
+        return self._new_input(X, "components_") @ self.components_.T
 
     def inverse_transform(self, X):
         check_is_fitted(self, "components_")
-        X = check_array(X, dtype=np.float64)
-        return X @ self.components_
+        return check_array(X, dtype=np.float64) @ self.components_
