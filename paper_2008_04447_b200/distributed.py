@@ -186,13 +186,50 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
                      lay, ell)
     achieved, nblocks, reason = 0, 0, "k_reached"
     first = True
+    # The panel's outcome (bhat, taus, R11) is read LAZILY: block J's trailing
+    # update and sample update run assuming a complete panel (bhat = bb), and
+    # its tail comes back with block J+1's sample-QRCP record in ONE host
+    # synchronisation per block.  A short / zero panel or a singular R11 then
+    # stops the loop exactly where the reference does (randomized.py:196-219):
+    # the speculative work past that point is discarded, and the panel columns
+    # left of a short panel's stop get the block update they miss.
+    pend = None
+
+    def settle(pd, tail, may_continue):
+        """Apply the reference's exits for the pending block; True = stop."""
+        nonlocal achieved, nblocks, reason
+        pi0, pbb, pan, lc_owner = pd
+        bhat, taus_host, R11_host = tail
+        if bhat == 0:  # randomized.py:197: no block, no update (ours used Y = 0: a no-op)
+            achieved, nblocks, reason = pi0, nblocks - 1, "panel_zero"
+            return True
+        taus[pi0:pi0 + bhat] = taus_host[:bhat]
+        if bhat < pbb:
+            # the short panel's remaining columns also take the block update
+            if lc_owner >= 0:
+                ops.block_update(A_local, lc_owner + bhat, pi0, m, pan, ncols=pbb - bhat)
+            achieved, reason = pi0 + bhat, "short_block"
+            return True
+        if not may_continue:
+            return True
+        d = np.abs(np.diag(R11_host))
+        if not (d.size > 0 and d.min() > _DIAG_FLOOR * d[0]):
+            reason = "r11_singular"
+            return True
+        return False
+
     while achieved < k:
         i0 = achieved
         bb = min(b, k - i0)
         nt = n - i0
         # ---- replicated sample QRCP (identical input -> identical pivots)
-        samp = ops.sample_qrcp(B, ell, nt, bb, first)
+        samp = ops.sample_qrcp(B, ell, nt, bb, first, pend[2] if pend else None)
         first = False
+        if pend is not None:
+            stop = settle(pend, samp.prev_tail, True)
+            pend = None
+            if stop:
+                break
         if samp.stop:
             reason = samp.reason
             break
@@ -209,35 +246,25 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         lc = int(lay.local_index(i0)) if owner == r else -1
         pan = ops.panel(A_local, lc, i0, m, samp.achieved, bb, owner == r)
         pan = ops.broadcast_panel(pan, owner, comm, m - i0, bb)
-        bhat = pan.bhat
-        if bhat == 0:
-            reason = "panel_zero"
-            break
-        taus[i0:i0 + bb] = pan.taus_host[:bb]
-        # ---- trailing update of my columns at global positions >= i0 + bhat
-        t0 = lay.first_local_at_or_after(r, i0 + bhat)
+        # ---- trailing update of my columns at global positions >= i0 + bb
+        t0 = lay.first_local_at_or_after(r, i0 + bb)
         ops.block_update(A_local, t0, i0, m, pan)
         nblocks += 1
-        achieved = i0 + bhat
-        ncols = n - achieved
-        if bhat < bb:
-            reason = "short_block"
-            break
+        achieved = i0 + bb
+        pend = (i0, bb, pan, lc)
         if achieved >= k:
             reason = "k_reached"
             break
-        if ncols == 0:
+        if n - achieved == 0:
             reason = "no_trailing"
-            break
-        d = np.abs(np.diag(pan.R11_host))
-        if not (d.size > 0 and d.min() > _DIAG_FLOOR * d[0]):
-            reason = "r11_singular"
             break
         # ---- sample update for my columns, all-gathered (sketch.py:132-149)
         s0 = lay.first_local_at_or_after(r, achieved)
         mine = gloc[s0:]
         Bn_loc = ops.sample_update_local(samp, A_local, s0, mine - i0, i0, bb, pan)
         B = ops.assemble_next(comm.all_gather(ops.pad_slab(Bn_loc, lay, achieved)), lay, achieved, ell)
+    if pend is not None:
+        settle(pend, ops.read_tail(pend[2]), False)
     counters = rqrcp_counters(m, n, b, ell, achieved, nblocks,
                               {"k_reached": 1, "short_block": 5, "no_trailing": 6}.get(reason, 0), False)
     return DistResult(achieved, nblocks, reason, perm, A_local, taus[:achieved], counters)
@@ -252,6 +279,7 @@ class _Sample:
     moves: np.ndarray
     Bf: object
     st: object
+    prev_tail: object = None  # (bhat, taus, R11) of the previous block's panel, read with this record
 
 
 @dataclass
@@ -263,6 +291,7 @@ class _Panel:
     R11: object          # (bb, bb) device
     R11_host: np.ndarray
     st: object
+    tail: object = None  # device [taus | R11 | status] record, parsed lazily
 
 
 class GpuOps:
@@ -326,6 +355,8 @@ class GpuOps:
         self.Rl = torch.zeros((b + max(nmax, 1), b), **f64)
         self.mbuf = torch.zeros(b * b, **f64)
         self.sws = torch.zeros(int(self.L.sqr_sample_qrcp_workspace(ell, n)), dtype=torch.uint8, device=self.dev)
+        self.h_ctl = torch.zeros(self.ctl.numel(), dtype=torch.uint8).pin_memory()
+        self.h_tail = torch.zeros(b + b * b + 9, dtype=torch.float64).pin_memory()
         self.gidx = [torch.tensor(lay.global_of_local(q), device=self.dev) for q in range(lay.P)]
 
     # 1. sketch of the local slab
@@ -370,7 +401,7 @@ class GpuOps:
         return self._assemble(parts, lay, ell, achieved)
 
     # 2. replicated sample QRCP
-    def sample_qrcp(self, B, ell, nt, bb, first):
+    def sample_qrcp(self, B, ell, nt, bb, first, pend_pan=None):
         st = self.ctl[:72]
         st.zero_()
         if not first:  # the sample floor of the first block (randomized.py:179-180)
@@ -380,7 +411,13 @@ class GpuOps:
                                             self.lperm.data_ptr(), moves.data_ptr(), self.staus.data_ptr(),
                                             1 if first else 0, st.data_ptr(), self.sws.data_ptr(), self.sws.numel(),
                                             self._s()), "sample_qrcp")
-        h = self.ctl.cpu().numpy()        # one D2H: status + moves
+        # one host synchronisation: status + moves, plus the previous panel's tail
+        self.h_ctl.copy_(self.ctl, non_blocking=True)
+        if pend_pan is not None:
+            self.h_tail[:pend_pan.tail.numel()].copy_(pend_pan.tail, non_blocking=True)
+        torch.cuda.current_stream(self.dev).synchronize()
+        h = self.h_ctl.numpy()
+        prev_tail = self._parse_tail(self.h_tail.numpy(), pend_pan.Y.shape[0]) if pend_pan is not None else None
         s = np.frombuffer(h[:72].tobytes(), dtype=self.lib.STATUS_DTYPE)[0]
         if first:
             self._floor = float(s["floor_sq"])
@@ -390,7 +427,9 @@ class GpuOps:
         mv = h[128:128 + 8 * nm].view(np.int32).reshape(nm, 2).astype(np.int64)
         mv = mv[(mv[:, 0] >= 0) & (mv[:, 0] != mv[:, 1])]  # drop no-op slots (dst = -1) and self-moves
         self._keep.clear()
-        return _Sample(stop, reason, int(s["sample_achieved"]), mv, self.Bf[:max(nt, 1)], st)
+        smp = _Sample(stop, reason, int(s["sample_achieved"]), mv, self.Bf[:max(nt, 1)], st)
+        smp.prev_tail = prev_tail
+        return smp
 
     # 3. point-to-point column moves
     def move_columns(self, A, ps, pd, lay, comm):
@@ -452,18 +491,24 @@ class GpuOps:
     def broadcast_panel(self, pan, owner, comm, mr, bb):
         _, _, _, _, rec, tail = self._panel_views(mr, bb)
         comm.broadcast(rec, owner)           # one message: Y, taus, R11, status
-        h = tail.cpu().numpy()               # one D2H: taus, R11, status
-        meta = h[bb + bb * bb:].view(np.int32)
-        pan.bhat = 0 if meta[0] else int(meta[5])
-        pan.taus_host = h[:bb].copy()
-        R = h[bb:bb + bb * bb].reshape(bb, bb).T[:pan.bhat, :pan.bhat]  # (bb, bb) storage is column-major
-        pan.R11_host = np.triu(R)
+        pan.tail = tail                      # read with the next block's sample record
         return pan
 
+    @staticmethod
+    def _parse_tail(h, bb):
+        """(bhat, taus, triu R11[:bhat, :bhat]) from a [taus | R11 | status] record."""
+        meta = h[bb + bb * bb:bb + bb * bb + 9].view(np.int32)
+        bhat = 0 if meta[0] else int(meta[5])
+        R = h[bb:bb + bb * bb].reshape(bb, bb).T[:bhat, :bhat]  # (bb, bb) storage is column-major
+        return bhat, h[:bb].copy(), np.triu(R)
+
+    def read_tail(self, pan):
+        return self._parse_tail(pan.tail.cpu().numpy(), pan.Y.shape[0])
+
     # 5. trailing update of my columns
-    def block_update(self, A, t0, i0, m, pan):
+    def block_update(self, A, t0, i0, m, pan, ncols=None):
         ld = A.shape[1]
-        ncols = A.shape[0] - t0
+        ncols = A.shape[0] - t0 if ncols is None else ncols
         bb = pan.Y.shape[0]
         mr = m - i0
         T = self.T.view(-1)[:bb * bb].view(bb, bb)

@@ -43,7 +43,12 @@ class NumpyOps:
     def assemble_next(self, parts, lay, achieved, ell):
         return self._assemble(parts, lay, ell, achieved)
 
-    def sample_qrcp(self, B, ell, nt, bb, first):
+    def sample_qrcp(self, B, ell, nt, bb, first, pend_pan=None):
+        smp = self._sample_qrcp(B, ell, nt, bb, first)
+        smp.prev_tail = self.read_tail(pend_pan) if pend_pan is not None else None
+        return smp
+
+    def _sample_qrcp(self, B, ell, nt, bb, first):
         Bm = B[:nt].numpy().T
         csq = np.einsum("ij,ij->j", Bm, Bm)
         if first:
@@ -98,18 +103,20 @@ class NumpyOps:
         comm.broadcast(pan.Y, owner)
         comm.broadcast(pan.taus, owner)
         comm.broadcast(pan.R11, owner)
-        mh = meta.numpy()
-        pan.bhat = 0 if mh[0] else int(mh[5])
-        pan.taus_host = pan.taus.numpy().copy()
-        pan.R11_host = np.triu(pan.R11.numpy().T[:pan.bhat, :pan.bhat])
+        pan.tail = meta
         return pan
 
-    def block_update(self, A, t0, i0, m, pan):
+    def read_tail(self, pan):
+        mh = pan.tail.numpy()
+        bhat = 0 if mh[0] else int(mh[5])
+        return bhat, pan.taus.numpy().copy(), np.triu(pan.R11.numpy().T[:bhat, :bhat])
+
+    def block_update(self, A, t0, i0, m, pan, ncols=None):
         Y = pan.Y.numpy().T
         tau = pan.taus.numpy()
         T = O.t_factor(Y, tau)
         pan.T = T
-        C = self.mat(A)[i0:m, t0:]
+        C = self.mat(A)[i0:m, t0:] if ncols is None else self.mat(A)[i0:m, t0:t0 + ncols]
         if C.shape[1]:
             W = T.T @ (Y.T @ C)
             C -= Y @ W
@@ -120,6 +127,10 @@ class NumpyOps:
             return torch.zeros((0, ell), dtype=torch.float64)
         Bf = samp.Bf.numpy().T
         R11 = np.triu(pan.R11.numpy().T)
+        if not O.r11_usable(R11):
+            # speculative block (short panel / singular R11, settled at the next
+            # sync): like the device guard, produce no sample
+            return torch.zeros((len(rel), ell), dtype=torch.float64)
         R12 = self.mat(A)[i0:i0 + bb, s0:s0 + len(rel)]
         X = O.back_solve(R11, R12)
         top = Bf[:bb, rel] - np.triu(Bf[:bb, :bb]) @ X

@@ -20,7 +20,17 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, m, n, k, b, p, seed, q):
+def _matrix(m, n, rr):
+    A = gauss(m, n, 17)
+    if rr > 0:  # rank-deficient: the sample floor stops the loop behind a pending block
+        A = np.asfortranarray(gauss(m, rr, 18) @ gauss(rr, n, 19))
+    elif rr < 0:  # -rr independent columns then exact zeros: a short panel (bhat < b) settles lazily
+        A = np.zeros((m, n), order="F")
+        A[:, :-rr] = gauss(m, -rr, 18)
+    return A
+
+
+def _worker(rank, world, port, m, n, k, b, p, seed, q, rr=0):
     import sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -29,7 +39,7 @@ def _worker(rank, world, port, m, n, k, b, p, seed, q):
     try:
         from dist_numpy_ops import NumpyOps
         from paper_2008_04447_b200.distributed import BlockCyclic, TorchComm, rqrcp_block_cyclic
-        A = gauss(m, n, 17)
+        A = _matrix(m, n, rr)
         lay = BlockCyclic(n, b, world)
         g = lay.global_of_local(rank)
         A_loc = torch.from_numpy(np.ascontiguousarray(A[:, g].T))
@@ -50,20 +60,22 @@ def _worker(rank, world, port, m, n, k, b, p, seed, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,m,n,k,b,p", [(2, 90, 70, 70, 8, 4), (3, 120, 100, 60, 16, 8), (2, 64, 80, 64, 8, 8)])
-def test_block_cyclic_matches_oracle(world, m, n, k, b, p):
+@pytest.mark.parametrize("world,m,n,k,b,p,rr", [(2, 90, 70, 70, 8, 4, 0), (3, 120, 100, 60, 16, 8, 0),
+                                                (2, 64, 80, 64, 8, 8, 0), (2, 90, 70, 70, 8, 4, 29),
+                                                (3, 100, 90, 90, 16, 4, 37), (2, 90, 70, 70, 8, 4, -29)])
+def test_block_cyclic_matches_oracle(world, m, n, k, b, p, rr):
     from oracle import port as O
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, k, b, p, 5, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, k, b, p, 5, q, rr)) for r in range(world)]
     for pr in procs:
         pr.start()
     achieved, perm, W, cnt, reason = q.get(timeout=240)
     for pr in procs:
         pr.join(timeout=60)
         assert pr.exitcode == 0
-    A = gauss(m, n, 17)
+    A = _matrix(m, n, rr)
     ref = O.rqrcp(A, k, b=b, p=p, seed=5)
     assert achieved == ref.achieved_rank
     assert np.array_equal(perm, ref.perm)
