@@ -151,6 +151,15 @@ int sqr_sample_update(const double* Bf, int64_t ldbf, int64_t ell, const double*
  * host (the multi-GPU orchestrator already knows b). */
 int sqr_sample_update_b(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
                         int64_t b, double* Bnext, int64_t ldbn, sqr_status* st, double* mbuf, void* stream);
+/* The same in two halves, so an orchestrator can run the prep (R11 guard +
+ * M = S11 R11^-1, sketch.py:132-149 / randomized.py:217-219) concurrently with
+ * the trailing update: prep reads S11 (first b columns of Bf) and R11 (ld ldr)
+ * and writes M (b*b) to mbuf; apply forms Bnext from M, R = [R11 | R12] and Bf. */
+int sqr_sample_update_prep(const double* Bf, int64_t ldbf, const double* R11, int64_t ldr, int64_t b,
+                           double* mbuf, sqr_status* st, void* stream);
+int sqr_sample_update_apply(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr, int64_t nt,
+                            int64_t b, double* Bnext, int64_t ldbn, sqr_status* st, const double* mbuf,
+                            void* stream);
 
 /* ------------------------------------------------------------- drivers
  * Full RQRCP (randomized.py:166-224, resample=0) / RSRQRCP (resample=1) on the

@@ -48,6 +48,9 @@ SIGNATURES = {
                              c_ptr]),
     "sqr_build_t": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_sample_update": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr]),
+    "sqr_sample_update_prep": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr]),
+    "sqr_sample_update_apply": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr,
+                                        c_ptr]),
     "sqr_sample_update_b": (c_int, [c_ptr, c_i64, c_i64, c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr,
                                     c_ptr]),
     "sqr_rqrcp_workspace": (c_i64, [c_i64, c_i64, c_i64, c_i64, c_i64]),

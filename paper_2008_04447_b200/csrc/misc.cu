@@ -635,6 +635,30 @@ extern "C" int sqr_copy_check_t(const double* src, int64_t lds, int64_t m, int64
   return SQR_OK;
 }
 
+// The two halves of sqr_sample_update_b for an orchestrator that overlaps the
+// prep with the trailing update: prep = R11 guard + M = S11 R11^-1 (b x b,
+// into mbuf; S11 = the first b columns of Bf, R11 at R with ld ldr), apply =
+// Bnext = [S12 - M R12 ; S22] (R = [R11 | R12], gated on st->stop).
+extern "C" int sqr_sample_update_prep(const double* Bf, int64_t ldbf, const double* R11, int64_t ldr, int64_t b,
+                                      double* mbuf, sqr_status* st, void* stream) {
+  if (b < 1 || mbuf == nullptr) {
+    sqr::set_error("sqr_sample_update_prep: need b >= 1 and a b*b scratch");
+    return SQR_EINVAL;
+  }
+  return sqr::su_prep(Bf, ldbf, R11, ldr, b, mbuf, st, nullptr, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" int sqr_sample_update_apply(const double* Bf, int64_t ldbf, int64_t ell, const double* R, int64_t ldr,
+                                       int64_t nt, int64_t b, double* Bnext, int64_t ldbn, sqr_status* st,
+                                       const double* mbuf, void* stream) {
+  if (b < 1 || b > ell || mbuf == nullptr) {
+    sqr::set_error("sqr_sample_update_apply: need 1 <= b <= ell and the prep's scratch");
+    return SQR_EINVAL;
+  }
+  return sqr::sample_update(Bf, ldbf, ell, R, ldr, nt, b, Bnext, ldbn, st, const_cast<double*>(mbuf),
+                            static_cast<cudaStream_t>(stream), true);
+}
+
 extern "C" int64_t sqr_launch_count(void) { return sqr::g_launches.load(); }
 
 extern "C" int sqr_profile_enable(int64_t max_launches) {

@@ -246,6 +246,8 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         lc = int(lay.local_index(i0)) if owner == r else -1
         pan = ops.panel(A_local, lc, i0, m, samp.achieved, bb, owner == r)
         pan = ops.broadcast_panel(pan, owner, comm, m - i0, bb)
+        if hasattr(ops, "prep_sample_update"):  # overlaps the trailing update
+            ops.prep_sample_update(samp, pan, bb)
         # ---- trailing update of my columns at global positions >= i0 + bb
         t0 = lay.first_local_at_or_after(r, i0 + bb)
         ops.block_update(A_local, t0, i0, m, pan)
@@ -355,6 +357,8 @@ class GpuOps:
         self.Rl = torch.zeros((b + max(nmax, 1), b), **f64)
         self.mbuf = torch.zeros(b * b, **f64)
         self.sws = torch.zeros(int(self.L.sqr_sample_qrcp_workspace(ell, n)), dtype=torch.uint8, device=self.dev)
+        self.side = torch.cuda.Stream(self.dev, priority=-1)
+        self.prep_done = None
         self.h_ctl = torch.zeros(self.ctl.numel(), dtype=torch.uint8).pin_memory()
         self.h_tail = torch.zeros(b + b * b + 9, dtype=torch.float64).pin_memory()
         self.gidx = [torch.tensor(lay.global_of_local(q), device=self.dev) for q in range(lay.P)]
@@ -401,7 +405,13 @@ class GpuOps:
         return self._assemble(parts, lay, ell, achieved)
 
     # 2. replicated sample QRCP
+    def _join_prep(self):
+        if self.prep_done is not None:
+            torch.cuda.current_stream(self.dev).wait_event(self.prep_done)
+            self.prep_done = None
+
     def sample_qrcp(self, B, ell, nt, bb, first, pend_pan=None):
+        self._join_prep()  # the overlapped prep writes the status record zeroed below
         st = self.ctl[:72]
         st.zero_()
         if not first:  # the sample floor of the first block (randomized.py:179-180)
@@ -503,7 +513,21 @@ class GpuOps:
         return bhat, h[:bb].copy(), np.triu(R)
 
     def read_tail(self, pan):
+        self._join_prep()
         return self._parse_tail(pan.tail.cpu().numpy(), pan.Y.shape[0])
+
+    # 4b. sample-update prep (R11 guard, M = S11 R11^-1) on a high-priority side
+    #     stream while the trailing update runs (cf. driver.cu EarlyPrep)
+    def prep_sample_update(self, samp, pan, bb):
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.dev))
+        self.side.wait_event(ev)
+        ell = samp.Bf.shape[1]
+        self._chk(self.L.sqr_sample_update_prep(samp.Bf.data_ptr(), ell, pan.R11.data_ptr(), bb, bb,
+                                                self.mbuf.data_ptr(), samp.st.data_ptr(), self.side.cuda_stream),
+                  "sample_update_prep")
+        self.prep_done = torch.cuda.Event()
+        self.prep_done.record(self.side)
 
     # 5. trailing update of my columns
     def block_update(self, A, t0, i0, m, pan, ncols=None):
@@ -522,6 +546,10 @@ class GpuOps:
     def sample_update_local(self, samp, A, s0, rel, i0, bb, pan):
         ell = samp.Bf.shape[1]
         nloc = len(rel)
+        prepped = self.prep_done is not None
+        if prepped:  # the overlapped prep wrote mbuf and may have set samp.st->stop
+            torch.cuda.current_stream(self.dev).wait_event(self.prep_done)
+            self.prep_done = None
         if nloc == 0:
             return self.slab[:0]
         # Bf_loc = [S11 | Bf[:, rel]] and R_loc = [R11 | R12 of my columns]
@@ -535,9 +563,14 @@ class GpuOps:
         ld = A.shape[1]
         self._chk(self.L.sqr_copy_columns(A.data_ptr() + 8 * (s0 * ld + i0), ld, bb, None, Rl.data_ptr() + 8 * bb * bb,
                                           bb, None, nloc, self._s()), "gather R12")
-        self._chk(self.L.sqr_sample_update_b(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, bb,
-                                             self.slab.data_ptr(), ell, samp.st.data_ptr(), self.mbuf.data_ptr(),
-                                             self._s()), "sample_update")
+        if prepped:  # M from the overlapped prep
+            self._chk(self.L.sqr_sample_update_apply(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, bb,
+                                                     self.slab.data_ptr(), ell, samp.st.data_ptr(),
+                                                     self.mbuf.data_ptr(), self._s()), "sample_update")
+        else:
+            self._chk(self.L.sqr_sample_update_b(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, bb,
+                                                 self.slab.data_ptr(), ell, samp.st.data_ptr(), self.mbuf.data_ptr(),
+                                                 self._s()), "sample_update")
         return self.slab[:nloc]
 
 
