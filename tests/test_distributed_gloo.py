@@ -62,7 +62,8 @@ def _worker(rank, world, port, m, n, k, b, p, seed, q, rr=0):
 
 @pytest.mark.parametrize("world,m,n,k,b,p,rr", [(2, 90, 70, 70, 8, 4, 0), (3, 120, 100, 60, 16, 8, 0),
                                                 (2, 64, 80, 64, 8, 8, 0), (2, 90, 70, 70, 8, 4, 29),
-                                                (3, 100, 90, 90, 16, 4, 37), (2, 90, 70, 70, 8, 4, -29)])
+                                                (3, 100, 90, 90, 16, 4, 37), (2, 90, 70, 70, 8, 4, -29),
+                                                (4, 130, 150, 120, 8, 8, 0)])
 def test_block_cyclic_matches_oracle(world, m, n, k, b, p, rr):
     from oracle import port as O
     ctx = mp.get_context("spawn")
