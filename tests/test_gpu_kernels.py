@@ -70,7 +70,7 @@ def test_gemm_tn(M, N, K, off):
 
 
 @pytest.mark.parametrize("M,N,K,off", [(1000, 1000, 32, 0), (4097, 300, 128, 0), (513, 77, 3, 1), (20000, 100, 20000, 0),
-                                       (100, 4000, 232, 1)])
+                                       (100, 4000, 232, 1), (128, 20000, 128, 0), (77, 19001, 256, 1)])
 def test_gemm_nn(M, N, K, off):
     rng = np.random.default_rng(M + N * K)
     X = rng.standard_normal((M + off, K))
