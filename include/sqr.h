@@ -237,6 +237,25 @@ int sqr_apply_block_update(double* C, int64_t ldc, int64_t mr, int64_t ncols, in
                            int64_t ldy, const double* taus, double* T, int64_t ldt, void* workspace,
                            int64_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------------ result assembly
+ * Bandwidth kernels that build the reference's result arrays on the device.
+ * dst (n x m, ld ldd) = src^T for src m x n (ld lds); upper != 0 keeps only
+ * src's upper trapezoid (r <= c) -- R = triu(work[:achieved, :]) as row-major
+ * rows (randomized.py:223, 338). */
+int sqr_transpose(const double* src, int64_t lds, int64_t m, int64_t n, double* dst, int64_t ldd,
+                  int upper, void* stream);
+/* Y (m x w, ldy) = the explicit unit-lower reflectors of packed columns
+ * [i0, i0+w) of W (ldw): the reference's Yfull, zeros above the block
+ * offset (randomized.py:199-201, reference.py:153-159). */
+int sqr_unpack_reflectors(const double* W, int64_t ldw, int64_t m, int64_t i0, int64_t w, double* Y,
+                          int64_t ldy, void* stream);
+/* gather: dst[i, j] = src[idx[i], j]; scatter: dst[idx[i], j] = src[i, j]
+ * (i < rows, j < cols, idx int64): TUXV's P^T V_k and Z0^T = (R P^T)^T
+ * (randomized.py:374, 384; validation.py:56-59). */
+int sqr_gather_rows(const double* src, int64_t lds, int64_t rows, int64_t cols, const int64_t* idx,
+                    double* dst, int64_t ldd, void* stream);
+int sqr_scatter_rows(const double* src, int64_t lds, int64_t rows, int64_t cols, const int64_t* idx,
+                     double* dst, int64_t ldd, void* stream);
 #ifdef __cplusplus
 }
 #endif

@@ -7,6 +7,9 @@ helpers raise.
 """
 from __future__ import annotations
 
+import contextlib
+import threading
+
 import numpy as np
 import torch
 
@@ -157,21 +160,57 @@ def check_finite(M: ColMajor, name: str = "A") -> None:
 
 
 class Workspace:
-    """Grow-only zero-initialised scratch per device (barrier / semaphore words
-    inside it are left at zero by every kernel that uses them)."""
+    """Grow-only zero-initialised scratch, one per (device, CUDA stream).
+
+    The reference promises "safe to call from multiple threads on disjoint
+    data".  Calls on different streams therefore get
+    different buffers (the cooperative kernels' grid-barrier words live in
+    them), and calls sharing a stream hold that stream's lock for the whole
+    enqueue (`lease`), so their kernels are stream-ordered one call after the
+    other.  A grown buffer is allocated on its stream; the old one is
+    released to torch's stream-ordered allocator when its last user drops
+    it, never while a call that holds it is still enqueueing.  Barrier /
+    semaphore words are left at zero by every kernel that uses them.
+    """
 
     _cache: dict = {}
+    _locks: dict = {}
+    _guard = threading.Lock()
+
+    @staticmethod
+    def _key(device):
+        dev = torch.device(device)
+        idx = dev.index if dev.index is not None else torch.cuda.current_device()
+        return (idx, torch.cuda.current_stream(idx).cuda_stream)
+
+    @classmethod
+    def _lock(cls, key) -> threading.RLock:
+        with cls._guard:
+            lk = cls._locks.get(key)
+            if lk is None:
+                lk = cls._locks[key] = threading.RLock()
+            return lk
 
     @classmethod
     def get(cls, nbytes: int, device) -> torch.Tensor:
-        key = (str(device),)
-        buf = cls._cache.get(key)
-        if buf is None or buf.numel() < nbytes:
-            cls._cache[key] = None
-            torch.cuda.synchronize(device)
-            buf = torch.zeros(int(nbytes) + 4096, dtype=torch.uint8, device=device)
-            cls._cache[key] = buf
-        return buf
+        """The current stream's buffer (>= nbytes).  Callers that enqueue
+        several launches on it should hold `lease` instead."""
+        key = cls._key(device)
+        with cls._lock(key):
+            buf = cls._cache.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.zeros(int(nbytes) + 4096, dtype=torch.uint8, device=torch.device("cuda", key[0]))
+                cls._cache[key] = buf
+            return buf
+
+    @classmethod
+    @contextlib.contextmanager
+    def lease(cls, nbytes: int, device):
+        """`with Workspace.lease(n, dev) as ws:` -- the buffer plus exclusive use
+        of it (per stream) until the block has enqueued its kernels."""
+        lk = cls._lock(cls._key(device))
+        with lk:
+            yield cls.get(nbytes, device)
 
 
 def status_new(device) -> torch.Tensor:

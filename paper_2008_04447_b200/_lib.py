@@ -74,6 +74,10 @@ SIGNATURES = {
                                  c_ptr]),
     "sqr_apply_block_update": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_ptr,
                                        c_i64, c_ptr]),
+    "sqr_transpose": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_int, c_ptr]),
+    "sqr_unpack_reflectors": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
+    "sqr_gather_rows": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
+    "sqr_scatter_rows": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
 }
 
 # struct sqr_status (include/sqr.h)

@@ -234,6 +234,14 @@ class RandomizedPivotedQR(_DeviceTransformer):
         return self._new_input(X, "selected_columns_")[:, self.selected_columns_]
 
 
+def _device_matmul(A, B) -> np.ndarray:
+    """A @ B on the device (libsqr DMMA GEMM), NumPy out: the estimator's
+    projections (estimators.py:157-186) stay off the host like every other
+    product of this package."""
+    dev = require_cuda()
+    return F.gemm_nn(upload(A, dev), upload(B, dev)).numpy()
+
+
 class TruncatedQLP(_DeviceTransformer):
     """TruncatedSVD-like surface over TUXV (estimators.py:129-186):
     components_ = V^T, singular_values_ = sigma_est, middle_ = X."""
@@ -263,11 +271,11 @@ class TruncatedQLP(_DeviceTransformer):
         self.singular_values_ = np.array(res.sigma_est, copy=True)
         self.middle_ = np.array(res.X, copy=True)
         self.n_features_in_ = X.shape[1]
-        return X @ V
+        return _device_matmul(X, V)
 
     def transform(self, X):
-        return self._new_input(X, "components_") @ self.components_.T
+        return _device_matmul(self._new_input(X, "components_"), self.components_.T)
 
     def inverse_transform(self, X):
         check_is_fitted(self, "components_")
-        return check_array(X, dtype=np.float64) @ self.components_
+        return _device_matmul(check_array(X, dtype=np.float64), self.components_)

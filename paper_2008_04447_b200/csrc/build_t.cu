@@ -133,11 +133,7 @@ int build_t_fast(const double* Gm, int64_t ldg, const double* taus, int64_t j, d
   }
   const int jp = j <= 16 ? 16 : j <= 32 ? 32 : j <= 64 ? 64 : 128;
   const int smem = (128 * kBtP + 64 * kBtXP) * 8;
-  static bool configured = false;
-  if (!configured) {
-    SQR_CUDA(cudaFuncSetAttribute(build_t_fast_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  if (int rc = smem_optin((const void*)build_t_fast_kernel, smem)) return rc;
   ProfScope ps(kTagBuildT, s);
   build_t_fast_kernel<<<1, kBtThreads, smem, s>>>(Gm, ldg, taus, (int)j, jp, T, ldt, gate);
   SQR_LAUNCH("build_t_fast_kernel");

@@ -22,6 +22,9 @@ void set_error(const char* fmt, ...);
 int check_cuda(cudaError_t e, const char* what);
 int sm_count();
 int max_smem_optin();
+// Dynamic shared-memory opt-in of `fn` on the CURRENT device (raised, never
+// lowered), once per (kernel, device); thread-safe (process-wide mutex).
+int smem_optin(const void* fn, int bytes);
 
 #define SQR_CUDA(call)                                              \
   do {                                                              \

@@ -312,10 +312,11 @@ extern "C" int64_t sqr_rqrcp_workspace(int64_t m, int64_t n, int64_t /*k*/, int6
 namespace sqr {
 namespace {
 // Streams the finished R columns to pinned host memory while later blocks run.
-// Column block [i0, i0+bb) never changes after its panel (later column moves
-// only touch columns >= the next block), so right after the panel its rows
-// above the block go out with one 2D copy and its diagonal block, with the
-// reflector tails zeroed, through a per-block staging slot.
+// Column block [i0, i0+bb) never changes after its block's trailing update
+// (later column moves only touch columns >= the next block), so right after
+// that update its rows above the block go out with one 2D copy and its
+// diagonal block, with the reflector tails zeroed, through a per-block
+// staging slot.
 struct RSink {
   double* host = nullptr;
   int64_t ldh = 0;
@@ -436,7 +437,6 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
         return rc;
     }
-    if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
     const bool prep = early && J + 1 < nblk && nt - bb > 0;
     if (prep && (rc = ep.launch(w.Bf, ell, P, lda, bb, w.Gm, st, w.guard, s))) return rc;
     if (la.on) {
@@ -446,6 +446,7 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
         return rc;
       if (nt > 1 && (rc = pass2_split(P, lda, mr, nt, bb, w.Ypan, m, w.W, b, st, w.snap, s, la.fork))) return rc;
       if (nt <= 1) SQR_CUDA(cudaEventRecord(la.fork, s));
+      if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
       cudaStream_t s2 = la.side;
       SQR_CUDA(cudaStreamWaitEvent(s2, la.fork, 0));
       if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s2))) return rc;
@@ -467,6 +468,10 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     else
       rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s);
     if (rc) return rc;
+    // R columns [i0, i0+bb) go out only now: a short panel (bhat < bb) leaves
+    // columns [i0+bhat, i0+bb) in the trailing matrix, whose R rows
+    // [i0, i0+bhat) the update above has just rewritten (randomized.py:203-213).
+    if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
     if (prep && (rc = ep.wait(s))) return rc;
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s, prep ? w.guard : nullptr))) return rc;
     if (J + 1 < nblk) {

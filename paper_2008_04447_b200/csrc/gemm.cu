@@ -636,12 +636,7 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
               int64_t ldc, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
               double* ws, int64_t ws_bytes, GemmDyn dyn, cudaStream_t s) {
   using Cfg = TnCfg<MT, VEC>;
-  static bool configured = false;
-  if (!configured) {
-    SQR_CUDA(cudaFuncSetAttribute(gemm_tn_kernel<MT, VEC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg::SMEM));
-    configured = true;
-  }
+  if (int rc = smem_optin((const void*)gemm_tn_kernel<MT, VEC>, Cfg::SMEM)) return rc;
   const int tiles = (int)cdiv(N, Cfg::BN);
   const int sms = 2 * sm_count();  // resident CTAs (2 per SM)
   // Pick the split count that minimises waves/split (i.e. the padded work),
@@ -705,12 +700,7 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
               int64_t ldy, double beta, const double* E, int64_t lde, double* D, int64_t ldd,
               GemmDyn dyn, cudaStream_t s, double* ws, int64_t ws_bytes) {
   using Cfg = NnCfg<VEC, SQR_NN_BN>;
-  static bool configured = false;
-  if (!configured) {
-    SQR_CUDA(cudaFuncSetAttribute(gemm_nn_kernel<VEC, SQR_NN_BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  Cfg::SMEM));
-    configured = true;
-  }
+  if (int rc = smem_optin((const void*)gemm_nn_kernel<VEC, SQR_NN_BN>, Cfg::SMEM)) return rc;
   const int64_t tiles = cdiv(M, Cfg::BM) * cdiv(N, Cfg::BN);
   // Split K when the tiles fill less than ~3 waves of resident CTAs and K is
   // long (skinny products such as TUXV's A V_k): splits of >= 1024 K, chosen

@@ -10,6 +10,7 @@
 #include <stdio.h>
 
 #include <atomic>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -46,15 +47,20 @@ struct Profiler {
   cudaEvent_t pending[kNumTags] = {};
 };
 Profiler g_prof;
+std::mutex g_prof_mu;  // bench-only instrumentation, but callable from any thread
 }  // namespace
 
 void prof_begin(int tag, cudaStream_t s) {
+  if (!g_prof.on) return;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   if (!g_prof.on || g_prof.used + 2 > g_prof.ev.size()) return;
   cudaEvent_t e = g_prof.ev[g_prof.used];
   cudaEventRecord(e, s);
   g_prof.pending[tag] = e;
 }
 void prof_end(int tag, cudaStream_t s) {
+  if (!g_prof.on) return;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
   if (!g_prof.on || g_prof.pending[tag] == nullptr || g_prof.used + 2 > g_prof.ev.size()) return;
   cudaEvent_t e = g_prof.ev[g_prof.used + 1];
   cudaEventRecord(e, s);
@@ -63,26 +69,50 @@ void prof_end(int tag, cudaStream_t s) {
   g_prof.pending[tag] = nullptr;
 }
 
+// Device attributes, cached per device (thread-safe: atomics, idempotent fill).
+namespace {
+constexpr int kMaxDev = 64;
+std::atomic<int> g_sms[kMaxDev], g_smem[kMaxDev];
+int cur_dev() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= kMaxDev ? 0 : dev;
+}
+}  // namespace
+
 int sm_count() {
-  static int n = 0;
+  const int dev = cur_dev();
+  int n = g_sms[dev].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
     if (n <= 0) n = 148;
+    g_sms[dev].store(n, std::memory_order_relaxed);
   }
   return n;
 }
 
 int max_smem_optin() {
-  static int n = 0;
+  const int dev = cur_dev();
+  int n = g_smem[dev].load(std::memory_order_relaxed);
   if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&n, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
     if (n <= 0) n = 227 * 1024;
+    g_smem[dev].store(n, std::memory_order_relaxed);
   }
   return n;
+}
+
+int smem_optin(const void* fn, int bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> done;
+  const int dev = cur_dev();
+  std::lock_guard<std::mutex> lock(mu);
+  int& cur = done[{fn, dev}];
+  if (bytes > cur) {
+    SQR_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    cur = bytes;
+  }
+  return SQR_OK;
 }
 
 namespace {
@@ -455,11 +485,7 @@ int apply_moves(double* X, int64_t ld, int64_t rows, int64_t col0, int64_t* perm
     return SQR_OK;
   }
   const int64_t smem = std::max<int64_t>(max_moves, 1) * kMoveRows * 8;
-  static int64_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    SQR_CUDA(cudaFuncSetAttribute(apply_moves_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  if (int rc = smem_optin((const void*)apply_moves_kernel, (int)smem)) return rc;
   const int blocks = (int)std::max<int64_t>(1, cdiv(rows, kMoveRows));
   ProfScope ps(kTagMoves, s);
   apply_moves_kernel<<<blocks, 256, smem, s>>>(X, ld, rows, col0, perm, moves, st);
@@ -474,11 +500,7 @@ int su_prep(const double* Bf, int64_t ldbf, const double* R, int64_t ldr, int64_
     return SQR_EINVAL;
   }
   const int64_t smem = (bmax | 1) * bmax * 8;
-  static int64_t configured = 0;
-  if (smem > 48 * 1024 && smem > configured) {
-    SQR_CUDA(cudaFuncSetAttribute(su_prep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = smem;
-  }
+  if (int rc = smem_optin((const void*)su_prep_kernel, (int)smem)) return rc;
   // The early (guard-word) launch overlaps the trailing update on a side
   // stream: it is not event-timed (its span would mostly be queueing).
   if (guard == nullptr) prof_begin(kTagSampleUpd, s);
@@ -663,6 +685,7 @@ extern "C" int64_t sqr_launch_count(void) { return sqr::g_launches.load(); }
 
 extern "C" int sqr_profile_enable(int64_t max_launches) {
   using sqr::g_prof;
+  std::lock_guard<std::mutex> lock(sqr::g_prof_mu);
   for (auto e : g_prof.ev) cudaEventDestroy(e);
   g_prof.ev.clear();
   g_prof.tags.clear();
@@ -680,6 +703,7 @@ extern "C" int sqr_profile_enable(int64_t max_launches) {
 // sqr_profile_enable; synchronises on the recorded events, then resets.
 extern "C" int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, int ntags) {
   using sqr::g_prof;
+  std::lock_guard<std::mutex> lock(sqr::g_prof_mu);
   for (int t = 0; t < ntags; ++t) {
     ms_per_tag[t] = 0.0;
     count_per_tag[t] = 0;

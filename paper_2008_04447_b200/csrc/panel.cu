@@ -640,11 +640,7 @@ int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double
   p += (int64_t)148 * 128 * wmax * 8;
   a.wred = reinterpret_cast<double*>(p);
   a.trace = g_trace_host_ptr;
-  static int configured = 0;
-  if (smem > configured) {
-    SQR_CUDA(cudaFuncSetAttribute(panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = (int)smem;
-  }
+  if (int rc = smem_optin((const void*)panel_kernel, (int)smem)) return rc;
   void* args[] = {&a};
   SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
   ProfScope ps(kTagPanel, s);

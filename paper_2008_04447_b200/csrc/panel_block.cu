@@ -508,11 +508,7 @@ int panel_block(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, dou
   a.mred = reinterpret_cast<double*>(p);
   a.trace = g_trace_host_ptr;
   const int smem = kSmemDoubles * 8;
-  static bool configured = false;
-  if (!configured) {
-    SQR_CUDA(cudaFuncSetAttribute(panel_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  if (int rc = smem_optin((const void*)panel_block_kernel, smem)) return rc;
   void* args[] = {&a};
   SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
   ProfScope ps(kTagPanel, s);

@@ -19,6 +19,8 @@
 #include <stdlib.h>
 
 #include <cooperative_groups.h>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -1150,10 +1152,23 @@ struct SampleWorkspace {
 
 // Largest cluster the register sample kernel can be launched with (16 with
 // the non-portable opt-in where the GPCs allow it, else 8), probed once.
+int cluster_max_probe();
 int cluster_max() {
-  static int cmax = -1;
-  if (cmax >= 0) return cmax;
-  cmax = 0;
+  // per device, probed once under a process-wide lock
+  static std::mutex mu;
+  static std::map<int, int> probed;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = probed.find(dev);
+  if (it != probed.end()) return it->second;
+  const int c = cluster_max_probe();
+  probed[dev] = c;
+  return c;
+}
+
+int cluster_max_probe() {
+  int cmax = 0;
   const int smem = (int)(((int64_t)(144 - kRR) * kRT + 2 * 152 + 2 + kRT) * 8);
   if (cudaFuncSetAttribute(sample_qrcp_reg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) !=
       cudaSuccess) {
@@ -1229,21 +1244,12 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     const int G = (int)std::max<int64_t>(1, cdiv(nt, (int64_t)kRT));
     const int YP = (int)(((std::max<int64_t>(ell, a.RS + kRR) + 1) | 1) + 1);
     const int smem = (int)(((int64_t)a.RS * kRT + 2 * YP + 2 + kRT) * 8);
-    static int configured = 0, configured_cl = 0;
-    if (smem > configured) {
-      SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    smem));
-      configured = smem;
-    }
+    if (int rc = smem_optin((const void*)sample_qrcp_reg_kernel<false>, smem)) return rc;
     // One cluster when the sample fits 16 CTAs (the hardware cluster
     // barrier and DSMEM exchange; measured per-step cost in DESIGN.md).
     static const bool no_cl = env_flag("SQR_NO_CLUSTER_SAMPLE");
     if (!no_cl && G <= cluster_max() && ell <= kMaxEllCl) {
-      if (smem > configured_cl) {
-        SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_reg_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      smem));
-        configured_cl = smem;
-      }
+      if (int rc = smem_optin((const void*)sample_qrcp_reg_kernel<true>, smem)) return rc;
       cudaLaunchConfig_t cfg{};
       cfg.gridDim = dim3(G);
       cfg.blockDim = dim3(kRT);
@@ -1317,12 +1323,7 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
   a.spill = reinterpret_cast<double*>(p);
   a.trace = g_trace_host_ptr;
 
-  static int configured_smem = 0;
-  if (smem > configured_smem) {
-    SQR_CUDA(cudaFuncSetAttribute(sample_qrcp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)smem));
-    configured_smem = (int)smem;
-  }
+  if (int rc = smem_optin((const void*)sample_qrcp_kernel, (int)smem)) return rc;
   void* args[] = {&a};
   SQR_CUDA(cudaMemsetAsync(a.bar, 0, 64, s));
   ProfScope ps(kTagSample, s);

@@ -17,6 +17,8 @@ reference), and ``omega=<array>`` feeds an explicit l x m matrix.
 """
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 import torch
 
@@ -64,8 +66,9 @@ def _load(A, device=None, copy: bool = True, check: bool = True) -> tuple[ColMaj
     return M, not isinstance(A, torch.Tensor)
 
 
-def _ws(nbytes, device) -> torch.Tensor:
-    return Workspace.get(nbytes, device)
+def _ws(nbytes, device):
+    """Exclusive use of the current stream's scratch while a call enqueues (_dev.Workspace)."""
+    return Workspace.lease(nbytes, device)
 
 
 # ------------------------------------------------------------ device blocks
@@ -150,9 +153,9 @@ def _build_t(Yd: ColMajor, taud: torch.Tensor) -> ColMajor:
     if j > MAX_ELL:
         return _compose_t_recursive(Yd, taud)
     T = ColMajor.empty(j, j, dev, zero=True)
-    ws = _ws(j * j * 8 + (200 << 20), dev)
-    _lib.check(_lib.lib().sqr_build_t(Yd.ptr, Yd.ld, Yd.m, j, ptr(taud), T.ptr, T.ld, ptr(ws), ws.numel(),
-                                      stream_handle()), "sqr_build_t")
+    with _ws(j * j * 8 + (200 << 20), dev) as ws:
+        _lib.check(_lib.lib().sqr_build_t(Yd.ptr, Yd.ld, Yd.m, j, ptr(taud), T.ptr, T.ld, ptr(ws), ws.numel(),
+                                          stream_handle()), "sqr_build_t")
     return T
 
 
@@ -181,22 +184,23 @@ def gemm_tn(X: ColMajor, C: ColMajor, alpha: float = 1.0) -> ColMajor:
     M, N, K = X.n, C.n, X.m
     dev = C.t.device
     D = ColMajor.empty(M, N, dev)
-    ws = _ws(200 << 20, dev)
-    for i0 in range(0, M, MAX_ELL):
-        mc = min(MAX_ELL, M - i0)
-        _lib.check(_lib.lib().sqr_gemm_tn(mc, N, K, alpha, X.col_ptr(0, i0), X.ld, C.ptr, C.ld, 0.0, None, 0,
-                                          D.col_ptr(i0, 0), D.ld, ptr(ws), ws.numel(), stream_handle()),
-                   "sqr_gemm_tn")
+    with _ws(200 << 20, dev) as ws:
+        for i0 in range(0, M, MAX_ELL):
+            mc = min(MAX_ELL, M - i0)
+            _lib.check(_lib.lib().sqr_gemm_tn(mc, N, K, alpha, X.col_ptr(0, i0), X.ld, C.ptr, C.ld, 0.0, None, 0,
+                                              D.col_ptr(i0, 0), D.ld, ptr(ws), ws.numel(), stream_handle()),
+                       "sqr_gemm_tn")
     return D
 
 
 def gemm_nn(X: ColMajor, Y: ColMajor, alpha: float = 1.0) -> ColMajor:
     M, N, K = X.m, Y.n, X.n
     D = ColMajor.empty(M, N, Y.t.device)
-    ws = _ws(16 * M * N * 8, Y.t.device) if K >= 2048 else None  # split-K scratch for skinny products
-    _lib.check(_lib.lib().sqr_gemm_nn_ws(M, N, K, alpha, X.ptr, X.ld, Y.ptr, Y.ld, 0.0, None, 0, D.ptr, D.ld,
-                                         ptr(ws) if ws is not None else None, ws.numel() if ws is not None else 0,
-                                         stream_handle()), "sqr_gemm_nn")
+    # split-K scratch for skinny products
+    with (_ws(16 * M * N * 8, Y.t.device) if K >= 2048 else contextlib.nullcontext()) as ws:
+        _lib.check(_lib.lib().sqr_gemm_nn_ws(M, N, K, alpha, X.ptr, X.ld, Y.ptr, Y.ld, 0.0, None, 0, D.ptr, D.ld,
+                                             ptr(ws) if ws is not None else None,
+                                             ws.numel() if ws is not None else 0, stream_handle()), "sqr_gemm_nn")
     return D
 
 
@@ -219,16 +223,18 @@ def _apply_blocks(blocks, C: ColMajor, transpose: bool) -> ColMajor:
             YW = gemm_nn(Yd, W)
             C.view().sub_(YW.view())
             continue
-        ws = _ws(2 * blk.width * max(C.n, 1) * 8 + (200 << 20), dev)
-        _lib.check(_lib.lib().sqr_apply_wy(Yd.ptr, Yd.ld, Td.ptr, Td.ld, Yd.m, blk.width, C.ptr, C.ld, C.n,
-                                           1 if transpose else 0, ptr(ws), ws.numel(), stream_handle()),
-                   "sqr_apply_wy")
+        with _ws(2 * blk.width * max(C.n, 1) * 8 + (200 << 20), dev) as ws:
+            _lib.check(_lib.lib().sqr_apply_wy(Yd.ptr, Yd.ld, Td.ptr, Td.ld, Yd.m, blk.width, C.ptr, C.ld, C.n,
+                                               1 if transpose else 0, ptr(ws), ws.numel(), stream_handle()),
+                       "sqr_apply_wy")
     return C
 
 
 def _transpose(M: ColMajor) -> ColMajor:
     out = ColMajor.empty(M.n, M.m, M.t.device)
-    out.view().copy_(M.view().T)
+    if M.m and M.n:
+        _lib.check(_lib.lib().sqr_transpose(M.ptr, M.ld, M.m, M.n, out.ptr, out.ld, 0, stream_handle()),
+                   "sqr_transpose")
     return out
 
 
@@ -480,17 +486,13 @@ def _packed_blocks(W: ColMajor, taus: torch.Tensor, Tbuf, b: int, widths, m: int
     LAPACK-packed work matrix: block J's reflector c sits in column i0+c."""
     dev = W.t.device
     out = []
-    rows = torch.arange(m, device=dev)
+    L = _lib.lib()
     for J, (i0, w) in enumerate(widths):
-        Y = ColMajor.empty(m, w, dev, zero=True)
-        cols = W.t[i0:i0 + w, :m]  # (w, m)
-        diag = (i0 + torch.arange(w, device=dev))[:, None]
-        below = rows[None, :] > diag
-        Y.t[:w, :m] = torch.where(below, cols, torch.zeros((), dtype=cols.dtype, device=dev))
-        Y.t[torch.arange(w, device=dev), (i0 + torch.arange(w, device=dev))] = 1.0
+        Y = ColMajor.empty(m, w, dev)
+        _lib.check(L.sqr_unpack_reflectors(W.ptr, W.ld, m, i0, w, Y.ptr, Y.ld, stream_handle()),
+                   "sqr_unpack_reflectors")
         if Tbuf is not None:
-            T = ColMajor.empty(w, w, dev)
-            T.view().copy_(Tbuf[J].view(b, b).T[:w, :w])
+            T = ColMajor(Tbuf[J].view(b, b)[:w], w, w, b)   # block J's T in place (ld b)
         else:
             T = _build_t(Y, taus[i0:i0 + w].contiguous())
         out.append(ReflectorBlock(offset=i0, _dev=(Y, taus[i0:i0 + w].clone(), T)))
@@ -498,8 +500,12 @@ def _packed_blocks(W: ColMajor, taus: torch.Tensor, Tbuf, b: int, widths, m: int
 
 
 def _upper_rows(W: ColMajor, rows: int) -> torch.Tensor:
-    """triu(W[:rows, :]) as a (rows, n) tensor."""
-    return torch.triu(W.view()[:rows, :]).contiguous()
+    """triu(W[:rows, :]) as a (rows, n) row-major tensor (sqr_transpose, upper)."""
+    out = torch.empty((rows, W.n), dtype=torch.float64, device=W.t.device)
+    if rows and W.n:
+        _lib.check(_lib.lib().sqr_transpose(W.ptr, W.ld, rows, W.n, out.data_ptr(), W.n, 1, stream_handle()),
+                   "sqr_transpose")
+    return out
 
 
 def _fallback_qrcp(M: ColMajor, k: int, b: int, numpy_out: bool, blas2: bool = False) -> PivotedFactorization:
@@ -557,9 +563,9 @@ def _qr_blocked_dev(M: ColMajor, k: int, b: int) -> PivotedFactorization:
     nblk = -(-k // bk)
     taus = torch.zeros(k, dtype=torch.float64, device=dev)
     Tb = torch.zeros((nblk, bk * bk), dtype=torch.float64, device=dev)
-    ws = _ws(L.sqr_qr_blocked_workspace(m, n, k, bk), dev)
-    _lib.check(L.sqr_qr_blocked(M.ptr, M.ld, m, n, k, bk, ptr(taus), ptr(Tb), ptr(ws), ws.numel(),
-                                stream_handle()), "sqr_qr_blocked")
+    with _ws(L.sqr_qr_blocked_workspace(m, n, k, bk), dev) as ws:
+        _lib.check(L.sqr_qr_blocked(M.ptr, M.ld, m, n, k, bk, ptr(taus), ptr(Tb), ptr(ws), ws.numel(),
+                                    stream_handle()), "sqr_qr_blocked")
     widths = [(i0, min(bk, k - i0)) for i0 in range(0, k, bk)]
     pf = PivotedFactorization(m, n, None, None, None, k, qr_blocked_counters(m, n, k, b))
     pf._Rd = _upper_rows(M, k)
@@ -640,20 +646,20 @@ def _randomized(A, k, b, p, seed, resample, omega=None, _status=None, out=None):
     Tb = torch.zeros((nblk, b * b), dtype=torch.float64, device=dev)
     st = status_new(dev)
     if out is None:
-        ws = _ws(L.sqr_rqrcp_workspace(m, n, k, b, p), dev)
-        _lib.check(L.sqr_rqrcp(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
-                               OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
-                               1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws), ws.numel(),
-                               stream_handle()), "sqr_rqrcp")
+        with _ws(L.sqr_rqrcp_workspace(m, n, k, b, p), dev) as ws:
+            _lib.check(L.sqr_rqrcp(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
+                                   OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
+                                   1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws),
+                                   ws.numel(), stream_handle()), "sqr_rqrcp")
     else:
         # R streamed to the host buffer block by block, overlapped with the later blocks
         out = _check_out(out, min(k, m), n)
-        ws = _ws(L.sqr_rqrcp_stream_r_workspace(m, n, k, b, p), dev)
-        _lib.check(L.sqr_rqrcp_stream_r(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
-                                        OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
-                                        1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws),
-                                        ws.numel(), out.ctypes.data, out.shape[0], stream_handle()),
-                   "sqr_rqrcp_stream_r")
+        with _ws(L.sqr_rqrcp_stream_r_workspace(m, n, k, b, p), dev) as ws:
+            _lib.check(L.sqr_rqrcp_stream_r(M.ptr, M.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
+                                            OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
+                                            1 if resample else 0, ptr(perm), ptr(taus), ptr(Tb), ptr(st), ptr(ws),
+                                            ws.numel(), out.ctypes.data, out.shape[0], stream_handle()),
+                       "sqr_rqrcp_stream_r")
     s = status_read(st)
     if _status is not None:
         _status.append(s)
@@ -744,6 +750,13 @@ def trqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, allow_large_k: boo
            omega=None, _status=None) -> TruncatedFactorization:
     """Truncated RQRCP without trailing update (randomized.py:250-341)."""
     M, _ = _load(A)
+    return _trqrcp_dev(M, k, b, p, seed, allow_large_k, omega, _status)
+
+
+def _trqrcp_dev(M: ColMajor, k, b, p, seed, allow_large_k=False, omega=None, _status=None):
+    """trqrcp on a validated device copy M, which the main path permutes in
+    place (the reference's `work`, randomized.py:278, 299); the result's
+    `_permuted_input` says whether it did."""
     m, n = M.m, M.n
     _check_block_args(m, n, k, b, p)
     if not allow_large_k and k > min(m, n) // 2:
@@ -767,11 +780,11 @@ def trqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, allow_large_k: boo
     taus = torch.zeros(k, dtype=torch.float64, device=dev)
     Tb = torch.zeros((nblk, b * b), dtype=torch.float64, device=dev)
     st = status_new(dev)
-    ws = _ws(L.sqr_trqrcp_workspace(m, n, k, b, p), dev)
-    _lib.check(L.sqr_trqrcp(A0.ptr, A0.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
-                            OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
-                            Yg.ptr, Yg.ld, Wg.ptr, Wg.ld, Rg.ptr, Rg.ld, ptr(perm), ptr(taus), ptr(Tb), ptr(st),
-                            ptr(ws), ws.numel(), stream_handle()), "sqr_trqrcp")
+    with _ws(L.sqr_trqrcp_workspace(m, n, k, b, p), dev) as ws:
+        _lib.check(L.sqr_trqrcp(A0.ptr, A0.ld, m, n, k, b, p, seed & ((1 << 64) - 1),
+                                OmT.ptr if OmT is not None else None, OmT.ld if OmT is not None else 0,
+                                Yg.ptr, Yg.ld, Wg.ptr, Wg.ld, Rg.ptr, Rg.ld, ptr(perm), ptr(taus), ptr(Tb),
+                                ptr(st), ptr(ws), ws.numel(), stream_handle()), "sqr_trqrcp")
     s = status_read(st)
     if _status is not None:
         _status.append(s)
@@ -783,6 +796,7 @@ def trqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, allow_large_k: boo
     widths = [(J * b, min(b, ach - J * b)) for J in range(nb)]
     tf._blocks_fn = lambda: _packed_blocks(Yg, taus, Tb, b, widths, m)
     tf._Yg = Yg
+    tf._permuted_input = True
     return tf
 
 
@@ -791,23 +805,26 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     """TRQRCP + QLP flip-flop passes (randomized.py:353-406)."""
     if j_max < 1:
         raise ValueError("j_max must be >= 1")
-    # trqrcp validates A and factors its own copy; A itself is then only read
-    # (A V_k), so a column-major device input is used in place
-    tf = trqrcp(A, k, b=b, p=p, seed=seed, allow_large_k=allow_large_k, omega=omega)
-    M, _ = _load(A, copy=False, check=False)
+    # ONE validated device copy of A (one H2D for host input): TRQRCP permutes
+    # it in place, after which the flip-flop products use (A P)(P^T V_k) = A V_k
+    # and U^T (A P) = (U^T A) P on the permuted copy.
+    M, _ = _load(A)
+    tf = _trqrcp_dev(M, k, b, p, seed, allow_large_k, omega)
     m, n = M.m, M.n
     dev = M.t.device
-    Aorig = M
+    permuted = getattr(tf, "_permuted_input", False)
+    L = _lib.lib()
     kh = tf.achieved_rank
     cnt = tf.counters
     if kh == 0:
         return TuxvResult(None, np.zeros((0, 0)), None, np.zeros(0), 0, cnt, m, n)
     # Z0 = R P^T; LQ of Z0 via QR of Z0^T (n x kh)
-    Rd = tf.R_device(dev)
-    inv = torch.empty_like(tf.perm_device(dev))
-    inv[tf.perm_device(dev)] = torch.arange(n, device=dev)
+    # Z0^T = (R P^T)^T: row j of R^T goes to row perm[j] (scatter, no inverse)
+    Rd = tf.R_device(dev)                                  # (kh, n) row-major = R^T column-major, ld n
+    permd = tf.perm_device(dev)
     Z0t = ColMajor.empty(n, kh, dev)
-    Z0t.view().copy_(Rd[:, inv].T)
+    _lib.check(L.sqr_scatter_rows(Rd.data_ptr(), n, n, kh, permd.data_ptr(), Z0t.ptr, Z0t.ld, stream_handle()),
+               "sqr_scatter_rows")
     vf = _qr_blocked_dev(Z0t, kh, b)
     cnt.merge(vf.counters)
     # the flip-flop passes use each factor as one composed block (QLP: U, V
@@ -817,7 +834,12 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     for j in range(1, j_max + 1):
         if j % 2 == 1:
             Vk = _q_columns_dev(v_blocks, n, kh, dev)
-            Z = gemm_nn(Aorig, Vk)
+            if permuted:                                   # P^T V_k for the permuted copy
+                Vp = ColMajor.empty(n, kh, dev)
+                _lib.check(L.sqr_gather_rows(Vk.ptr, Vk.ld, n, kh, permd.data_ptr(), Vp.ptr, Vp.ld,
+                                             stream_handle()), "sqr_gather_rows")
+                Vk = Vp
+            Z = gemm_nn(M, Vk)
             cnt.add_pass()
             cnt.add_blas3(m, n, kh)
             uf = _qr_blocked_dev(Z, kh, b)
@@ -826,9 +848,14 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
             X = uf.R_device(dev)[:kh, :kh].contiguous()
         else:
             Uk = _q_columns_dev(u_blocks, m, kh, dev)
-            Zt = gemm_tn(Uk, Aorig)  # kh x n
+            Zt = gemm_tn(Uk, M)  # kh x n  (= U^T A P on the permuted copy)
             Z = ColMajor.empty(n, kh, dev)
-            Z.view().copy_(Zt.view().T)
+            if permuted:                                   # (U^T A)^T = P (U^T A P)^T: scatter rows
+                Ztt = _transpose(Zt)
+                _lib.check(L.sqr_scatter_rows(Ztt.ptr, Ztt.ld, n, kh, permd.data_ptr(), Z.ptr, Z.ld,
+                                              stream_handle()), "sqr_scatter_rows")
+            else:
+                Z.view().copy_(Zt.view().T)
             cnt.add_pass()
             cnt.add_blas3(kh, m, n)
             vf = _qr_blocked_dev(Z, kh, b)

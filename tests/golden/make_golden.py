@@ -131,15 +131,11 @@ def main():
                                    res.counters.blas3_volume], dtype=np.int64)}
         np.savez_compressed(os.path.join(OUT, f"{name}.npz"), **d)
 
-    # --- config 1 / config 2 (BASELINE.md §3 inputs), summary outputs only ---
+    # --- config 1 (BASELINE.md §3 inputs), summary outputs only; C2-C5: make_golden_configs.py ---
     A1 = rng.giid(1000, 1000, seed=1)
     pf = randomized.rqrcp(A1, 1000, b=32, p=8, seed=0)
     np.savez_compressed(os.path.join(OUT, "c1.npz"), **pf_dict("", pf, full_r=False),
                         rel_residual=np.float64(pf.rel_residual(A1)))
-    A2 = synth.synth_decay(4000, 4000, ratio=10 ** (-10 / 4000), seed=2)
-    tf = randomized.trqrcp(A2, 200, b=32, p=8, seed=0)
-    np.savez_compressed(os.path.join(OUT, "c2.npz"), **pf_dict("", tf, full_r=False),
-                        R_top=tf.R[:, :200], rel_residual=np.float64(tf.rel_residual(A2, 200)))
     print("golden fixtures written to", OUT)
 
 

@@ -195,6 +195,30 @@ def test_rqrcp_streams_r_to_host(m, n, k, b):
     assert np.all(np.tril(out[: got.achieved_rank], -1) == 0.0)
 
 
+@pytest.mark.parametrize("case", ["golden_rankdef", "p_block_exit", "j_block_exit", "noise_floor"])
+def test_rqrcp_streams_r_to_host_rank_deficient(case):
+    """out= on inputs whose last block is SHORT (bhat < bb): the trailing update
+    of that block rewrites R rows of its own columns [i0+bhat, i0+bb), so the
+    streamed R must leave only after the update (advisor finding, driver.cu RSink)."""
+    if case == "golden_rankdef":
+        g = load_golden("r_rankdef")
+        A, kw = g["A"], golden_kwargs(g)
+    else:
+        r, seed, noise = {"p_block_exit": (39, 2, 0.0), "j_block_exit": (53, 1, 0.0),
+                          "noise_floor": (61, 7, 1e-13)}[case]
+        A = lowrank(200, 180, r, seed, noise)
+        kw = dict(k=180, b=16, p=8, seed=seed)
+    ref = G.rqrcp(A, **kw, omega="host")
+    assert ref.achieved_rank < kw["k"]
+    out = np.zeros((min(kw["k"], A.shape[0]), A.shape[1]), order="F")
+    got = G.rqrcp(A, **kw, omega="host", out=out)
+    assert got.achieved_rank == ref.achieved_rank
+    assert np.array_equal(got.perm, ref.perm)
+    assert np.array_equal(got.R, ref.R)
+    oref = O.rqrcp(A, **kw)
+    check_against(got, oref, A, normwise=True)
+
+
 def test_device_inputs_checked_and_untouched():
     """Column-major CUDA inputs go through the fused copy + finite scan
     (sqr_copy_check); tuxv reads A in place without modifying it; non-finite
@@ -264,3 +288,46 @@ def test_tuxv_wider_than_one_wy_kernel_block():
     assert np.abs(res.reconstruct() - ref.reconstruct()).max() <= 1e-9 * np.abs(A).max()
     U = res.u_columns()
     assert np.abs(U.T @ U - np.eye(160)).max() <= 1e-12
+
+
+@pytest.mark.parametrize("same_stream", [False, True])
+def test_concurrent_threads_disjoint_data(same_stream):
+    """The reference's concurrency contract: calls from several threads on
+    disjoint data are safe.  Two threads factor different
+    matrices at once (own CUDA streams, or one shared stream); every result is
+    bitwise equal to the same call made alone (deterministic kernels)."""
+    import threading
+    cases = [(gauss(900, 700, 50 + i), dict(k=600, b=32 + 32 * (i % 2), p=8, seed=i)) for i in range(4)]
+    # alone first; the 4th case needs a larger workspace than the others (grow path)
+    cases.append((gauss(3000, 2600, 60), dict(k=2600, b=128, p=8, seed=7)))
+    alone = [G.rqrcp(A, **kw, omega="host") for A, kw in cases]
+    want = [(pf.perm.copy(), pf.R.copy()) for pf in alone]
+    tr = [G.trqrcp(A, 64, b=16, p=8, seed=3, omega="host") for A, _ in cases[:2]]
+    want_t = [(tf.perm.copy(), tf.w_t.copy()) for tf in tr]
+    errors = []
+    shared = torch.cuda.Stream() if same_stream else None
+
+    def worker(tid):
+        try:
+            s = shared if same_stream else torch.cuda.Stream()
+            with torch.cuda.stream(s):
+                for rep in range(3):
+                    order = list(range(len(cases)))[tid::2] + list(range(len(cases)))[1 - tid::2]
+                    for i in order:
+                        A, kw = cases[i]
+                        pf = G.rqrcp(A, **kw, omega="host")
+                        if not (np.array_equal(pf.perm, want[i][0]) and np.array_equal(pf.R, want[i][1])):
+                            errors.append(f"thread {tid} rep {rep} case {i}: rqrcp differs")
+                    tf = G.trqrcp(cases[tid][0], 64, b=16, p=8, seed=3, omega="host")
+                    if not (np.array_equal(tf.perm, want_t[tid][0]) and np.array_equal(tf.w_t, want_t[tid][1])):
+                        errors.append(f"thread {tid} rep {rep}: trqrcp differs")
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(f"thread {tid}: {e!r}")
+
+    ths = [threading.Thread(target=worker, args=(t,)) for t in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors

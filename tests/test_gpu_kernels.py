@@ -7,7 +7,7 @@ implements (oracle/port.py), at sizes the oracle finishes in seconds.
 import numpy as np
 import pytest
 
-from conftest import gauss
+from conftest import gauss, load_golden
 from oracle import port as O
 
 torch = pytest.importorskip("torch")
@@ -142,6 +142,72 @@ def test_sample_qrcp_ties_and_exhaustion():
     B[:, 2] = 1.0
     ref = O.sample_pivots(B, 3)
     assert ref.achieved == 1
+
+
+# --------------------------------------------------------- sample update
+def _sample_then_update(B, bb, R11, R12, entry="sqr_sample_update"):
+    """sqr_sample_qrcp on B, then Bnext = [S12 - S11 R11^-1 R12; S22] through the ABI."""
+    ell, ntot = B.shape
+    Bd = upload(B, DEV)
+    Bf = ColMajor.empty(ell, ntot, DEV)
+    lperm = torch.empty(ntot, dtype=torch.int64, device=DEV)
+    moves = torch.empty(4 * bb + 8, dtype=torch.int32, device=DEV)
+    taus = torch.zeros(bb, dtype=torch.float64, device=DEV)
+    st = status_new(DEV)
+    _lib.check(L.sqr_sample_qrcp(Bd.ptr, Bd.ld, ell, ntot, bb, Bf.ptr, Bf.ld, lperm.data_ptr(), moves.data_ptr(),
+                                 taus.data_ptr(), 1, st.data_ptr(), stream_handle()))
+    R = upload(np.hstack([R11, R12]), DEV)
+    nt = R12.shape[1]
+    Bn = ColMajor.empty(ell, nt, DEV)
+    if entry == "sqr_sample_update":
+        _lib.check(L.sqr_sample_update(Bf.ptr, Bf.ld, ell, R.ptr, R.ld, nt, Bn.ptr, Bn.ld, st.data_ptr(),
+                                       stream_handle()))
+    elif entry == "sqr_sample_update_b":
+        mbuf = torch.zeros(bb * bb, dtype=torch.float64, device=DEV)
+        _lib.check(L.sqr_sample_update_b(Bf.ptr, Bf.ld, ell, R.ptr, R.ld, nt, bb, Bn.ptr, Bn.ld, st.data_ptr(),
+                                         mbuf.data_ptr(), stream_handle()))
+    else:  # prep + apply halves
+        mbuf = torch.zeros(bb * bb, dtype=torch.float64, device=DEV)
+        _lib.check(L.sqr_sample_update_prep(Bf.ptr, Bf.ld, R.ptr, R.ld, bb, mbuf.data_ptr(), st.data_ptr(),
+                                            stream_handle()))
+        _lib.check(L.sqr_sample_update_apply(Bf.ptr, Bf.ld, ell, R.ptr, R.ld, nt, bb, Bn.ptr, Bn.ld, st.data_ptr(),
+                                             mbuf.data_ptr(), stream_handle()))
+    return Bn.numpy(), status_read(st)
+
+
+@pytest.mark.parametrize("entry", ["sqr_sample_update", "sqr_sample_update_b", "prep_apply"])
+def test_sample_update_golden(entry):
+    """sketch.py:132-149 against the REAL reference's sample_update output
+    (tests/golden/sample.npz: s_next)."""
+    g = load_golden("sample")
+    got, s = _sample_then_update(g["sB"], 6, g["s_R11"], g["s_R12"], entry)
+    assert int(s["stop"]) == 0
+    assert relerr(got, g["s_next"]) <= 1e-12
+
+
+@pytest.mark.parametrize("ell,ntot,bb,seed", [(40, 1000, 32, 1), (136, 6000, 128, 2), (72, 2001, 64, 3), (9, 30, 1, 4)])
+def test_sample_update_matches_oracle(ell, ntot, bb, seed):
+    B = gauss(ell, ntot, seed)
+    ref = O.sample_pivots(B, bb)
+    R11 = np.triu(gauss(bb, bb, seed + 100)) + 3 * np.eye(bb)
+    R12 = gauss(bb, ntot - bb, seed + 200)
+    want = O.sample_refresh(ref, R11, R12)
+    for entry in ("sqr_sample_update", "sqr_sample_update_b"):
+        got, s = _sample_then_update(B, bb, R11, R12, entry)
+        assert int(s["stop"]) == 0
+        assert relerr(got, want) <= 1e-11
+
+
+def test_sample_update_singular_guard():
+    """_diag_ok (randomized.py:133-135): min |R11_ii| <= 2^-52 |R11_00| stops the
+    loop (reason r11_singular) instead of solving, as the reference breaks."""
+    B = gauss(12, 40, 5)
+    R11 = np.triu(gauss(6, 6, 6)) + 4 * np.eye(6)
+    R11[3, 3] = 2.0 ** -60 * abs(R11[0, 0])
+    with pytest.raises(np.linalg.LinAlgError):
+        O.sample_refresh(O.sample_pivots(B, 6), R11, gauss(6, 34, 7))
+    _, s = _sample_then_update(B, 6, R11, gauss(6, 34, 7))
+    assert int(s["stop"]) == 1 and _lib.STOP_REASONS[int(s["reason"])] == "r11_singular"
 
 
 # ----------------------------------------------------------------- panel
