@@ -30,7 +30,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .counters import rqrcp_counters
+from .counters import rqrcp_counters, trqrcp_counters
 
 _DIAG_FLOOR = 2.0 ** -52
 
@@ -270,6 +270,84 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
     counters = rqrcp_counters(m, n, b, ell, achieved, nblocks,
                               {"k_reached": 1, "short_block": 5, "no_trailing": 6}.get(reason, 0), False)
     return DistResult(achieved, nblocks, reason, perm, A_local, taus[:achieved], counters)
+
+
+def trqrcp_block_cyclic(S_local, m: int, n: int, k: int, b: int, p: int, seed: int, comm, ops,
+                        omega=None) -> DistResult:
+    """Distributed TRQRCP (randomized.py:250-341), same column block-cyclic
+    layout.  ``S_local`` stacks, per local column, the reference's three
+    column-permuted arrays: rows [0, m) = work (A, never updated), [m, m+k) =
+    Wg (W^T rows), [m+k, m+2k) = Rg (R rows) -- so one column move carries all
+    three (randomized.py:299-302).  Yg (m x k) is replicated: every rank
+    stores the broadcast panel reflectors.  Per block: replicated sample QRCP;
+    column moves; the owner materialises its panel through the accumulated
+    reflections and factors it (:304-307); broadcast of (Y, taus, R11); every
+    rank forms the adjusted inner products, W^T rows and R rows of its OWN
+    trailing columns (:318-330, all column-local); local sample update +
+    all-gather.  The panel tail is read synchronously (TRQRCP runs few blocks).
+    Returns a DistResult with A_local = S_local and ``Yg``/``nb`` attached."""
+    ell = b + p
+    lay = BlockCyclic(n, b, comm.size)
+    r = comm.rank
+    gloc = lay.global_of_local(r)
+    if hasattr(ops, "begin"):
+        ops.begin(lay, m, ell)
+    perm = np.arange(n, dtype=np.int64)
+    taus = np.zeros(max(k, 1))
+    B = ops.assemble(comm.all_gather(ops.pad_slab(ops.sketch(S_local, m, ell, seed, omega, gloc), lay, 0)),
+                     lay, ell)
+    Yg = ops.new_yg(m, k)
+    achieved, nblocks, reason = 0, 0, "k_reached"
+    first = True
+    while achieved < k:
+        i0 = achieved
+        bb = min(b, k - i0)
+        nt = n - i0
+        samp = ops.sample_qrcp(B, ell, nt, bb, first)
+        first = False
+        if samp.stop:
+            reason = samp.reason
+            break
+        moves = samp.moves
+        if len(moves):
+            ps = i0 + moves[:, 1]
+            pd = i0 + moves[:, 0]
+            ops.move_columns(S_local, ps, pd, lay, comm)
+            perm[pd] = perm[ps].copy()
+        owner = (i0 // b) % comm.size
+        lc = int(lay.local_index(i0)) if owner == r else -1
+        pan = ops.tr_panel(S_local, lc, i0, m, k, samp.achieved, bb, owner == r, Yg)
+        pan = ops.broadcast_panel(pan, owner, comm, m - i0, bb)
+        bhat, taus_h, R11_h = ops.read_tail(pan)
+        if bhat == 0:                                   # randomized.py:308-309
+            reason = "panel_zero"
+            break
+        taus[i0:i0 + bhat] = taus_h[:bhat]
+        nblocks += 1
+        t0 = lay.first_local_at_or_after(r, i0 + bhat)
+        ops.tr_update(S_local, t0, i0, m, k, pan, bhat, Yg, lc)
+        achieved = i0 + bhat
+        if bhat < bb:                                   # randomized.py:332-333
+            reason = "short_block"
+            break
+        if achieved >= k:
+            reason = "k_reached"
+            break
+        if n - achieved == 0:
+            reason = "no_trailing"
+            break
+        d = np.abs(np.diag(R11_h))
+        if not (d.size > 0 and d.min() > _DIAG_FLOOR * d[0]):   # randomized.py:334-335
+            reason = "r11_singular"
+            break
+        s0 = lay.first_local_at_or_after(r, achieved)
+        mine = gloc[s0:]
+        Bn_loc = ops.sample_update_local(samp, S_local, s0, mine - i0, i0, bb, pan, r_row0=m + k + i0)
+        B = ops.assemble_next(comm.all_gather(ops.pad_slab(Bn_loc, lay, achieved)), lay, achieved, ell)
+    counters = trqrcp_counters(m, n, b, ell, achieved, nblocks)
+    res = DistResult(achieved, nblocks, reason, perm, S_local, taus[:achieved], counters)
+    res.Yg = Yg
+    return res
 
 
 # ------------------------------------------------------------ GPU backend
@@ -542,10 +620,84 @@ class GpuOps:
                                                 ws.data_ptr(), ws.numel(), self._s()), "block_update")
         pan.T = T
 
+    # TRQRCP (trqrcp_block_cyclic): replicated Yg, panel materialisation, local W^T / R rows
+    def new_yg(self, m, k):
+        return torch.zeros((max(k, 1), m), dtype=torch.float64, device=self.dev)   # m x k column-major
+
+    def _gemm_tn(self, M, N, K, alpha, X, ldx, C, ldc, D, ldd):
+        if M <= 0 or N <= 0:
+            return
+        ws = self._ws(200 << 20)
+        self._chk(self.L.sqr_gemm_tn(M, N, K, alpha, X, ldx, C, ldc, 0.0, None, 0, D, ldd, ws.data_ptr(), ws.numel(),
+                                     self._s()), "gemm_tn")
+
+    def _gemm_nn(self, M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd):
+        if M <= 0 or N <= 0:
+            return
+        self._chk(self.L.sqr_gemm_nn(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, self._s()), "gemm_nn")
+
+    def tr_panel(self, S, lc, i0, m, k, w, bb, is_owner, Yg):
+        """Owner: panel = work[i0:, sel] - Yg[i0:, :i0] Wg[:i0, sel] (randomized.py:304-306),
+        then its Householder QR (:307) into the broadcast record."""
+        mr = m - i0
+        Y, taus, R11, st, rec, tail = self._panel_views(mr, bb)
+        if is_owner:
+            rec.zero_()
+            LD = S.shape[1]
+            base = S.data_ptr() + 8 * lc * LD
+            if not hasattr(self, "Pn") or self.Pn.numel() < bb * mr:
+                self.Pn = torch.empty(bb * m, dtype=torch.float64, device=self.dev)
+            Pn = self.Pn[:bb * mr].view(bb, mr)
+            if i0:
+                self._gemm_nn(mr, w, i0, -1.0, Yg.data_ptr() + 8 * i0, m, base + 8 * m, LD, 1.0, base + 8 * i0, LD,
+                              Pn.data_ptr(), mr)
+            else:
+                self._chk(self.L.sqr_copy_columns(base, LD, mr, None, Pn.data_ptr(), mr, None, w, self._s()), "panel")
+            ws = self._ws(self.L.sqr_block_workspace(mr, 0, bb))
+            self._chk(self.L.sqr_panel_factor(Pn.data_ptr(), mr, mr, w, Y.data_ptr(), mr, taus.data_ptr(), 1,
+                                              st.data_ptr(), ws.data_ptr(), ws.numel(), self._s()), "panel")
+            R11.copy_(Pn[:bb, :bb])
+        return _Panel(0, Y, taus, None, R11, None, st)
+
+    def tr_update(self, S, t0, i0, m, k, pan, bhat, Yg, lc):
+        """Yg block, R11 into Rg (owner), then for this rank's trailing columns:
+        G = Y2^T work - (Y2^T Y1) W1^T; Wg rows = T2^T G; R rows = work rows -
+        Yg[i0:i0+bhat, :i0+bhat] Wg[:i0+bhat] (randomized.py:311-330)."""
+        mr = m - i0
+        LD = S.shape[1]
+        Y = pan.Y                                   # (bb, mr): column c of Y2 is row c
+        Yg[i0:i0 + bhat, i0:].copy_(Y[:bhat])
+        if lc >= 0:                                 # Rg[i0:i0+bhat, panel] = triu(R11) on the owner
+            R11 = torch.triu(pan.R11[:bhat, :bhat].T).T    # stored column-major: row index = column
+            S[lc:lc + bhat, m + k + i0:m + k + i0 + bhat].copy_(R11)
+        nloc = S.shape[0] - t0 if S.shape[0] > t0 else 0
+        if nloc <= 0:
+            return
+        T2 = self.T.view(-1)[:bhat * bhat]
+        wsb = self._ws(bhat * bhat * 8 + (200 << 20))
+        self._chk(self.L.sqr_build_t(Y.data_ptr(), mr, mr, bhat, pan.taus.data_ptr(), T2.data_ptr(), bhat,
+                                     wsb.data_ptr(), wsb.numel(), self._s()), "build_t")
+        if not hasattr(self, "Gtr") or self.Gtr.numel() < bhat * (nloc + max(i0, 1)):
+            self.Gtr = torch.empty(bhat * (S.shape[0] + k + 1), dtype=torch.float64, device=self.dev)
+        G = self.Gtr[:bhat * nloc]
+        C1 = self.Gtr[bhat * nloc:bhat * (nloc + max(i0, 1))]
+        col = S.data_ptr() + 8 * t0 * LD
+        self._gemm_tn(bhat, nloc, mr, 1.0, Y.data_ptr(), mr, col + 8 * i0, LD, G.data_ptr(), bhat)
+        if i0:
+            self._gemm_tn(bhat, i0, mr, 1.0, Y.data_ptr(), mr, Yg.data_ptr() + 8 * i0, m, C1.data_ptr(), bhat)
+            self._gemm_nn(bhat, nloc, i0, -1.0, C1.data_ptr(), bhat, col + 8 * m, LD, 1.0, G.data_ptr(), bhat,
+                          G.data_ptr(), bhat)
+        self._gemm_tn(bhat, nloc, bhat, 1.0, T2.data_ptr(), bhat, G.data_ptr(), bhat, col + 8 * (m + i0), LD)
+        self._gemm_nn(bhat, nloc, i0 + bhat, -1.0, Yg.data_ptr() + 8 * i0, m, col + 8 * m, LD, 1.0,
+                      col + 8 * i0, LD, col + 8 * (m + k + i0), LD)
+
     # 6. sample update of my columns, written straight into the all-gather slab
-    def sample_update_local(self, samp, A, s0, rel, i0, bb, pan):
+    def sample_update_local(self, samp, A, s0, rel, i0, bb, pan, r_row0=None):
+        """r_row0: storage row of the block's first R row (RQRCP: i0, in place;
+        TRQRCP: the Rg rows of the stacked slab, m + k + i0)."""
         ell = samp.Bf.shape[1]
         nloc = len(rel)
+        r_row0 = i0 if r_row0 is None else r_row0
         prepped = self.prep_done is not None
         if prepped:  # the overlapped prep wrote mbuf and may have set samp.st->stop
             torch.cuda.current_stream(self.dev).wait_event(self.prep_done)
@@ -561,8 +713,8 @@ class GpuOps:
         Rl = self.Rl.view(-1)[:(bb + nloc) * bb].view(bb + nloc, bb)
         Rl[:bb].copy_(pan.R11)
         ld = A.shape[1]
-        self._chk(self.L.sqr_copy_columns(A.data_ptr() + 8 * (s0 * ld + i0), ld, bb, None, Rl.data_ptr() + 8 * bb * bb,
-                                          bb, None, nloc, self._s()), "gather R12")
+        self._chk(self.L.sqr_copy_columns(A.data_ptr() + 8 * (s0 * ld + r_row0), ld, bb, None,
+                                          Rl.data_ptr() + 8 * bb * bb, bb, None, nloc, self._s()), "gather R12")
         if prepped:  # M from the overlapped prep
             self._chk(self.L.sqr_sample_update_apply(Bfl.data_ptr(), ell, ell, Rl.data_ptr(), bb, nloc, bb,
                                                      self.slab.data_ptr(), ell, samp.st.data_ptr(),
@@ -718,3 +870,218 @@ def bench_main(args, bench):
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0
+
+
+# ------------------------------------------------------------ public API
+# The reference's call signatures (randomized.py:227, 250, 353) for a job of
+# one process per GPU: every rank calls with the SAME full A (host array or
+# tensor) and gets the same drop-in result object, assembled on every rank.
+# Each rank uploads only its own block-cyclic columns.
+def _comm(group):
+    if not dist.is_available() or not dist.is_initialized():
+        raise RuntimeError("distributed.rqrcp/trqrcp/tuxv need an initialised torch.distributed process group "
+                           "(one process per GPU, backend 'nccl')")
+    return TorchComm(group)
+
+
+def _local_slab(A, cols: np.ndarray, m: int, rows: int, dev) -> torch.Tensor:
+    """This rank's columns of the caller's full m x n A as (ncols, rows) device
+    storage (rows >= m; the extra rows are zero), plus the input contract of
+    validation.check_matrix on them (validation.py:21-38)."""
+    from . import _lib
+    nl = int(cols.size)
+    S = torch.zeros((max(nl, 1), rows), dtype=torch.float64, device=dev)
+    if nl:
+        if isinstance(A, torch.Tensor):
+            src = A.detach().to(device=dev, dtype=torch.float64)
+            S[:nl, :m] = src[:, torch.as_tensor(cols, device=dev)].T
+        else:
+            host = np.asarray(A, dtype=np.float64)[:, cols]
+            S[:nl, :m].copy_(torch.from_numpy(np.ascontiguousarray(host.T)))
+    cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+    if nl and m:
+        _lib.check(_lib.lib().sqr_copy_check(S.data_ptr(), rows, m, nl, None, 0, cnt.data_ptr(),
+                                             torch.cuda.current_stream(dev).cuda_stream), "sqr_copy_check")
+    return S, cnt
+
+
+def _shape_of(A):
+    if isinstance(A, torch.Tensor):
+        if A.dim() != 2:
+            raise ValueError(f"A must be 2-dimensional, got ndim={A.dim()}")
+        return tuple(int(x) for x in A.shape)
+    arr = np.asarray(A)
+    if arr.ndim != 2:
+        raise ValueError(f"A must be 2-dimensional, got ndim={arr.ndim}")
+    return arr.shape
+
+
+def _omega_arg(omega, ell, m, seed):
+    """None / "device": drawn on the device by every rank (same stream, same
+    bits); "host": the reference's NumPy recipe; else an explicit l x m array."""
+    if omega is None or (isinstance(omega, str) and omega == "device"):
+        return None
+    if isinstance(omega, str):
+        if omega != "host":
+            raise ValueError("omega must be 'device', 'host' or an l x m array")
+        from .rng import host_omega
+        return host_omega(ell, m, seed)
+    om = omega.detach().cpu().numpy() if isinstance(omega, torch.Tensor) else np.asarray(omega, dtype=np.float64)
+    if om.shape != (ell, m):
+        raise ValueError(f"omega must have shape ({ell}, {m}), got {om.shape}")
+    return om
+
+
+def _gather_columns(S: torch.Tensor, lay: BlockCyclic, comm, rows: int, dev):
+    """All ranks' slabs into one (rows x n) column-major matrix in global column order."""
+    from . import _lib
+    from ._dev import ColMajor
+    nmax = lay.n_local_max()
+    mine = torch.zeros((max(nmax, 1), rows), dtype=torch.float64, device=dev)
+    nl = lay.n_local(comm.rank)
+    if nl:
+        mine[:nl] = S[:nl, :rows]
+    parts = comm.all_gather(mine)
+    W = ColMajor.empty(rows, lay.n, dev, ld=rows)
+    s = torch.cuda.current_stream(dev).cuda_stream
+    for q, part in enumerate(parts):
+        g = lay.global_of_local(q)
+        if g.size:
+            gi = torch.as_tensor(g, device=dev)
+            _lib.check(_lib.lib().sqr_copy_columns(part.data_ptr(), rows, rows, None, W.ptr, rows, gi.data_ptr(),
+                                                   int(g.size), s), "gather columns")
+    return W
+
+
+def _prologue(A, k, b, p, comm, dev):
+    from . import factor as F
+    m, n = _shape_of(A)
+    F._check_block_args(m, n, k, b, p)
+    return m, n
+
+
+def _check_finite_all(cnt, comm):
+    if comm.max(float(cnt.item())) > 0:
+        raise ValueError("A contains non-finite entries")
+
+
+def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=None, device=None):
+    """Multi-GPU drop-in of randomized.rqrcp (randomized.py:227-229): column
+    block-cyclic over the process group, NCCL.  Returns the reference's
+    PivotedFactorization (R, perm, blocks, achieved_rank, counters) on every
+    rank."""
+    from . import factor as F
+    from ._dev import require_cuda
+    dev = require_cuda(device)
+    comm = _comm(group)
+    m, n = _prologue(A, k, b, p, comm, dev)
+    ell = b + p
+    if k == 0 or ell >= m:   # empty / the deterministic l >= m fallback (randomized.py:172-174): replicated
+        return F.rqrcp(A, k, b=b, p=p, seed=seed, omega=omega)
+    lay = BlockCyclic(n, b, comm.size)
+    S, bad = _local_slab(A, lay.global_of_local(comm.rank), m, m, dev)
+    _check_finite_all(bad, comm)
+    res = rqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev), omega=_omega_arg(omega, ell, m, seed))
+    W = _gather_columns(S, lay, comm, m, dev)
+    ach = res.achieved
+    pf = F.PivotedFactorization(m, n, None, None, None, ach, res.counters)
+    pf._Rd_fn = lambda: F._upper_rows(W, ach)
+    pf._permd = torch.as_tensor(res.perm, device=dev)
+    taus = torch.as_tensor(np.asarray(res.taus, dtype=np.float64), device=dev)
+    widths = [(J * b, min(b, ach - J * b)) for J in range(res.nblocks)]
+    pf._blocks_fn = lambda: F._packed_blocks(W, taus, None, b, widths, m)
+    pf._work = W
+    return pf
+
+
+def _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device):
+    from . import factor as F
+    from ._dev import ColMajor, require_cuda
+    dev = require_cuda(device)
+    comm = _comm(group)
+    m, n = _prologue(A, k, b, p, comm, dev)
+    if not allow_large_k and k > min(m, n) // 2:
+        raise ValueError("trqrcp targets k <= min(m, n)/2; pass allow_large_k=True to override")
+    ell = b + p
+    if k == 0 or ell >= m:
+        return None, None, None, dev, comm, m, n
+    lay = BlockCyclic(n, b, comm.size)
+    rows = m + 2 * k
+    S, bad = _local_slab(A, lay.global_of_local(comm.rank), m, rows, dev)
+    _check_finite_all(bad, comm)
+    res = trqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev), omega=_omega_arg(omega, ell, m, seed))
+    SW = _gather_columns(S, lay, comm, rows, dev)
+    ach = res.achieved
+    tf = F.TruncatedFactorization(m, n, None, None, None, ach, res.counters)
+    Rv = ColMajor(SW.t[:, m + k:], k, n, SW.ld)
+    tf._Rd = F._upper_rows(Rv, ach)
+    wt = torch.empty((ach, n), dtype=torch.float64, device=dev)
+    if ach:
+        from . import _lib
+        _lib.check(_lib.lib().sqr_transpose(SW.ptr + 8 * m, SW.ld, ach, n, wt.data_ptr(), n, 0,
+                                            torch.cuda.current_stream(dev).cuda_stream), "sqr_transpose")
+    tf._w_td = wt
+    tf._permd = torch.as_tensor(res.perm, device=dev)
+    taus = torch.as_tensor(np.asarray(res.taus, dtype=np.float64), device=dev)
+    widths = [(J * b, min(b, ach - J * b)) for J in range(res.nblocks)]
+    Yg = ColMajor(res.Yg, m, k, m)
+    tf._blocks_fn = lambda: F._packed_blocks(Yg, taus, None, b, widths, m)
+    return tf, S, lay, dev, comm, m, n
+
+
+def trqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, allow_large_k: bool = False, omega=None,
+           group=None, device=None):
+    """Multi-GPU drop-in of randomized.trqrcp (randomized.py:250-341); the
+    TruncatedFactorization (R, w_t, perm, blocks, counters) on every rank."""
+    from . import factor as F
+    tf, *_ = _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device)
+    if tf is None:
+        return F.trqrcp(A, k, b=b, p=p, seed=seed, allow_large_k=allow_large_k, omega=omega)
+    return tf
+
+
+def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refine_sigma: bool = False,
+         allow_large_k: bool = False, omega=None, group=None, device=None):
+    """Multi-GPU drop-in of randomized.tuxv (randomized.py:353-406): the
+    distributed TRQRCP, then the QLP flip-flop with A's products formed from
+    the local slabs -- A V_k as a sum of per-rank partials (all-reduce of the
+    m x k partial Z), (U^T A)^T as disjoint row blocks
+    (all-reduce of an n x k matrix that each rank fills only at its columns)."""
+    from . import factor as F
+    from . import _lib
+    from ._dev import ColMajor
+    if j_max < 1:
+        raise ValueError("j_max must be >= 1")
+    tf, S, lay, dev, comm, m, n = _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device)
+    if tf is None:
+        return F.tuxv(A, k, j_max=j_max, b=b, p=p, seed=seed, refine_sigma=refine_sigma,
+                      allow_large_k=allow_large_k, omega=omega)
+    L = _lib.lib()
+    rows = S.shape[1]
+    nl = lay.n_local(comm.rank)
+    Wloc = ColMajor(S, m, nl, rows)                            # this rank's columns of A P (work rows)
+    orig = torch.as_tensor(tf.perm[lay.global_of_local(comm.rank)], device=dev)   # their original columns
+
+    def s():
+        return torch.cuda.current_stream(dev).cuda_stream
+
+    def a_times(Vk):
+        Vl = ColMajor.empty(max(nl, 1), Vk.n, dev)
+        if nl:
+            _lib.check(L.sqr_gather_rows(Vk.ptr, Vk.ld, nl, Vk.n, orig.data_ptr(), Vl.ptr, Vl.ld, s()), "gather")
+            Vl.m = nl
+            Z = F.gemm_nn(Wloc, Vl)
+        else:
+            Z = ColMajor.empty(m, Vk.n, dev, zero=True)
+        dist.all_reduce(Z.t, group=comm.group)
+        return Z
+
+    def at_times(Uk):
+        Z = ColMajor.empty(n, Uk.n, dev, zero=True)
+        if nl:
+            Zt = F._transpose(F.gemm_tn(Uk, Wloc))            # nl x kh
+            _lib.check(L.sqr_scatter_rows(Zt.ptr, Zt.ld, nl, Uk.n, orig.data_ptr(), Z.ptr, Z.ld, s()), "scatter")
+        dist.all_reduce(Z.t, group=comm.group)
+        return Z
+
+    return F._qlp(tf, m, n, b, j_max, refine_sigma, a_times, at_times, dev)

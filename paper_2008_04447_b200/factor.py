@@ -814,6 +814,35 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     dev = M.t.device
     permuted = getattr(tf, "_permuted_input", False)
     L = _lib.lib()
+    permd = tf.perm_device(dev)
+
+    def a_times(Vk: ColMajor) -> ColMajor:            # A V_k  (m x kh)
+        if permuted:                                   # P^T V_k for the permuted copy
+            Vp = ColMajor.empty(Vk.m, Vk.n, dev)
+            _lib.check(L.sqr_gather_rows(Vk.ptr, Vk.ld, Vk.m, Vk.n, permd.data_ptr(), Vp.ptr, Vp.ld,
+                                         stream_handle()), "sqr_gather_rows")
+            Vk = Vp
+        return gemm_nn(M, Vk)
+
+    def at_times(Uk: ColMajor) -> ColMajor:           # (U_k^T A)^T  (n x kh)
+        Zt = gemm_tn(Uk, M)                            # kh x n  (= U^T A P on the permuted copy)
+        Z = ColMajor.empty(n, Uk.n, dev)
+        if permuted:                                   # (U^T A)^T = P (U^T A P)^T: scatter rows
+            Ztt = _transpose(Zt)
+            _lib.check(L.sqr_scatter_rows(Ztt.ptr, Ztt.ld, n, Uk.n, permd.data_ptr(), Z.ptr, Z.ld,
+                                          stream_handle()), "sqr_scatter_rows")
+        else:
+            Z.view().copy_(Zt.view().T)
+        return Z
+
+    return _qlp(tf, m, n, b, j_max, refine_sigma, a_times, at_times, dev)
+
+
+def _qlp(tf, m: int, n: int, b: int, j_max: int, refine_sigma: bool, a_times, at_times, dev) -> TuxvResult:
+    """The QLP flip-flop of TUXV after its TRQRCP (randomized.py:367-406), with
+    the two products of A supplied by the caller (single GPU: the permuted
+    device copy; multi-GPU: local slabs + all-reduce / all-gather)."""
+    L = _lib.lib()
     kh = tf.achieved_rank
     cnt = tf.counters
     if kh == 0:
@@ -833,13 +862,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     X = vf.R_device(dev)[:kh, :kh].T.contiguous()
     for j in range(1, j_max + 1):
         if j % 2 == 1:
-            Vk = _q_columns_dev(v_blocks, n, kh, dev)
-            if permuted:                                   # P^T V_k for the permuted copy
-                Vp = ColMajor.empty(n, kh, dev)
-                _lib.check(L.sqr_gather_rows(Vk.ptr, Vk.ld, n, kh, permd.data_ptr(), Vp.ptr, Vp.ld,
-                                             stream_handle()), "sqr_gather_rows")
-                Vk = Vp
-            Z = gemm_nn(M, Vk)
+            Z = a_times(_q_columns_dev(v_blocks, n, kh, dev))
             cnt.add_pass()
             cnt.add_blas3(m, n, kh)
             uf = _qr_blocked_dev(Z, kh, b)
@@ -847,15 +870,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
             u_blocks = uf._composed_fn()
             X = uf.R_device(dev)[:kh, :kh].contiguous()
         else:
-            Uk = _q_columns_dev(u_blocks, m, kh, dev)
-            Zt = gemm_tn(Uk, M)  # kh x n  (= U^T A P on the permuted copy)
-            Z = ColMajor.empty(n, kh, dev)
-            if permuted:                                   # (U^T A)^T = P (U^T A P)^T: scatter rows
-                Ztt = _transpose(Zt)
-                _lib.check(L.sqr_scatter_rows(Ztt.ptr, Ztt.ld, n, kh, permd.data_ptr(), Z.ptr, Z.ld,
-                                              stream_handle()), "sqr_scatter_rows")
-            else:
-                Z.view().copy_(Zt.view().T)
+            Z = at_times(_q_columns_dev(u_blocks, m, kh, dev))
             cnt.add_pass()
             cnt.add_blas3(kh, m, n)
             vf = _qr_blocked_dev(Z, kh, b)

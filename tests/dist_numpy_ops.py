@@ -121,7 +121,49 @@ class NumpyOps:
             W = T.T @ (Y.T @ C)
             C -= Y @ W
 
-    def sample_update_local(self, samp, A, s0, rel, i0, bb, pan):
+    # TRQRCP (distributed.trqrcp_block_cyclic)
+    def new_yg(self, m, k):
+        return np.zeros((m, max(k, 1)), order="F")
+
+    def tr_panel(self, S, lc, i0, m, k, w, bb, is_owner, Yg):
+        mr = m - i0
+        Y = torch.zeros((bb, mr), dtype=torch.float64)
+        taus = torch.zeros(bb, dtype=torch.float64)
+        R11 = torch.zeros((bb, bb), dtype=torch.float64)
+        st = torch.zeros(24, dtype=torch.uint8)
+        if is_owner:
+            M = self.mat(S)
+            panel = np.array(M[i0:m, lc:lc + w], order="F")
+            if i0:
+                panel -= Yg[i0:, :i0] @ M[m:m + i0, lc:lc + w]
+            Yp, tp, bh = O.panel_factor(panel, 0, w)
+            Y[:bh] = torch.from_numpy(np.ascontiguousarray(Yp.T))
+            taus[:bh] = torch.from_numpy(tp)
+            R11[:w, :w] = torch.from_numpy(np.ascontiguousarray(panel[:w, :w].T))   # (col, row) storage
+            st.view(torch.int32)[5] = bh
+            if bh == 0:
+                st.view(torch.int32)[0] = 1
+        return _Panel(0, Y, taus, None, R11, None, st)
+
+    def tr_update(self, S, t0, i0, m, k, pan, bhat, Yg, lc):
+        M = self.mat(S)
+        Y2 = pan.Y.numpy().T[:, :bhat]
+        Yg[i0:, i0:i0 + bhat] = Y2
+        if lc >= 0:
+            M[m + k + i0:m + k + i0 + bhat, lc:lc + bhat] = np.triu(pan.R11.numpy().T[:bhat, :bhat])
+        if S.shape[0] <= t0:
+            return
+        T2 = O.t_factor(Y2, pan.taus.numpy()[:bhat])
+        cols = slice(t0, S.shape[0])
+        G = Y2.T @ M[i0:m, cols]
+        if i0:
+            G -= (Y2.T @ Yg[i0:, :i0]) @ M[m:m + i0, cols]
+        M[m + i0:m + i0 + bhat, cols] = T2.T @ G
+        M[m + k + i0:m + k + i0 + bhat, cols] = (M[i0:i0 + bhat, cols]
+                                                  - Yg[i0:i0 + bhat, :i0 + bhat] @ M[m:m + i0 + bhat, cols])
+
+    def sample_update_local(self, samp, A, s0, rel, i0, bb, pan, r_row0=None):
+        r_row0 = i0 if r_row0 is None else r_row0
         ell = samp.Bf.shape[1]
         if len(rel) == 0:
             return torch.zeros((0, ell), dtype=torch.float64)
@@ -131,7 +173,7 @@ class NumpyOps:
             # speculative block (short panel / singular R11, settled at the next
             # sync): like the device guard, produce no sample
             return torch.zeros((len(rel), ell), dtype=torch.float64)
-        R12 = self.mat(A)[i0:i0 + bb, s0:s0 + len(rel)]
+        R12 = self.mat(A)[r_row0:r_row0 + bb, s0:s0 + len(rel)]
         X = O.back_solve(R11, R12)
         top = Bf[:bb, rel] - np.triu(Bf[:bb, :bb]) @ X
         Bn = np.vstack([top, Bf[bb:, rel]])

@@ -30,7 +30,7 @@ def _matrix(m, n, rr):
     return A
 
 
-def _worker(rank, world, port, m, n, k, b, p, seed, q, rr=0):
+def _worker(rank, world, port, m, n, k, b, p, seed, q, rr=0, algo="rqrcp"):
     import sys
     sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__))))
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -38,12 +38,19 @@ def _worker(rank, world, port, m, n, k, b, p, seed, q, rr=0):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from dist_numpy_ops import NumpyOps
-        from paper_2008_04447_b200.distributed import BlockCyclic, TorchComm, rqrcp_block_cyclic
+        from paper_2008_04447_b200.distributed import (BlockCyclic, TorchComm, rqrcp_block_cyclic,
+                                                       trqrcp_block_cyclic)
         A = _matrix(m, n, rr)
         lay = BlockCyclic(n, b, world)
         g = lay.global_of_local(rank)
-        A_loc = torch.from_numpy(np.ascontiguousarray(A[:, g].T))
-        res = rqrcp_block_cyclic(A_loc, m, n, k, b, p, seed, TorchComm(), NumpyOps())
+        if algo == "trqrcp":   # stacked [work; Wg; Rg] columns
+            A_loc = torch.zeros((g.size, m + 2 * k), dtype=torch.float64)
+            A_loc[:, :m] = torch.from_numpy(np.ascontiguousarray(A[:, g].T))
+            res = trqrcp_block_cyclic(A_loc, m, n, k, b, p, seed, TorchComm(), NumpyOps())
+            m = m + 2 * k      # gather the whole stacked slab below
+        else:
+            A_loc = torch.from_numpy(np.ascontiguousarray(A[:, g].T))
+            res = rqrcp_block_cyclic(A_loc, m, n, k, b, p, seed, TorchComm(), NumpyOps())
         parts = [torch.zeros((max(lay.n_local(r) for r in range(world)), m), dtype=torch.float64)
                  for _ in range(world)]
         mine = torch.zeros_like(parts[0])
@@ -63,7 +70,7 @@ def _worker(rank, world, port, m, n, k, b, p, seed, q, rr=0):
 @pytest.mark.parametrize("world,m,n,k,b,p,rr", [(2, 90, 70, 70, 8, 4, 0), (3, 120, 100, 60, 16, 8, 0),
                                                 (2, 64, 80, 64, 8, 8, 0), (2, 90, 70, 70, 8, 4, 29),
                                                 (3, 100, 90, 90, 16, 4, 37), (2, 90, 70, 70, 8, 4, -29),
-                                                (4, 130, 150, 120, 8, 8, 0)])
+                                                (4, 130, 150, 120, 8, 8, 0), (8, 140, 200, 136, 8, 4, 0)])
 def test_block_cyclic_matches_oracle(world, m, n, k, b, p, rr):
     from oracle import port as O
     ctx = mp.get_context("spawn")
@@ -129,3 +136,35 @@ def test_move_plan_is_a_simultaneous_permutation():
             for r in range(P):
                 got[lay.global_of_local(r)] = new[r]
             assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("world,m,n,k,b,p,rr", [(2, 90, 70, 30, 8, 4, 0), (3, 150, 120, 48, 16, 8, 0),
+                                                (4, 130, 150, 40, 8, 8, 0), (8, 120, 200, 64, 8, 4, 0),
+                                                (2, 90, 70, 35, 8, 4, 29), (3, 100, 90, 45, 8, 4, -21)])
+def test_trqrcp_block_cyclic_matches_oracle(world, m, n, k, b, p, rr):
+    """Distributed TRQRCP (distributed.trqrcp_block_cyclic): identical
+    permutation / counters, and R and W^T rows to 1e-10 of the single-process
+    oracle (randomized.py:250-341), including exits behind a short panel."""
+    from oracle import port as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, m, n, k, b, p, 5, q, rr, "trqrcp"))
+             for r in range(world)]
+    for pr in procs:
+        pr.start()
+    achieved, perm, S, cnt, reason = q.get(timeout=240)
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    A = _matrix(m, n, rr)
+    ref = O.trqrcp(A, k, b=b, p=p, seed=5, allow_large_k=True)
+    assert achieved == ref.achieved_rank
+    assert np.array_equal(perm, ref.perm)
+    assert cnt == [ref.counters.trailing_passes, ref.counters.blas3_volume]
+    Wt = S[m:m + achieved, :]
+    R = np.triu(S[m + k:m + k + achieved, :])
+    assert np.abs(R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
+    assert np.abs(Wt - ref.w_t).max() <= 1e-10 * max(np.abs(ref.w_t).max(), 1e-300)
+    # the stacked work rows are only permuted, never updated (randomized.py:278)
+    assert np.array_equal(S[:m, :], A[:, perm])

@@ -24,8 +24,8 @@ round differently from the build container's; the comparison still runs
 (rounding-level input changes do not move these pivots, SURVEY.md §8(c)
 near-tie evidence) and the mismatch is reported in the test output.
 """
-import importlib.util
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -42,9 +42,8 @@ import paper_2008_04447_b200 as G  # noqa: E402
 
 DEV = torch.device("cuda", 0)
 
-_spec = importlib.util.spec_from_file_location("config_inputs", os.path.join(GOLDEN, "config_inputs.py"))
-CI = importlib.util.module_from_spec(_spec)
-_spec.loader.exec_module(CI)
+sys.path.insert(0, GOLDEN)
+import config_inputs as CI  # noqa: E402  (importable by name: its pool workers unpickle it)
 
 OMEGAS = ["host", None]
 

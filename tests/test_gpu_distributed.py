@@ -78,3 +78,59 @@ def test_block_cyclic_gpu_lazy_exits(nccl1, kind):
         assert np.abs(np.abs(np.diag(R))[:j] - dr[:j]).max() <= 1e-10 * dr[0]
         return
     assert np.abs(R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
+
+
+@pytest.mark.parametrize("m,n,k,b,p", [(600, 500, 120, 32, 8), (1500, 900, 200, 64, 8), (300, 257, 90, 16, 4)])
+def test_trqrcp_block_cyclic_gpu_world1(nccl1, m, n, k, b, p):
+    """trqrcp_block_cyclic on GpuOps + NCCL (stacked [work; Wg; Rg] slab)."""
+    from paper_2008_04447_b200.distributed import trqrcp_block_cyclic
+    dev = nccl1
+    A = gauss(m, n, 8)
+    om = O.gauss_matrix(b + p, m, 11)
+    S = torch.zeros((n, m + 2 * k), dtype=torch.float64, device=dev)
+    S[:, :m] = torch.from_numpy(np.ascontiguousarray(A.T)).to(dev)
+    res = trqrcp_block_cyclic(S, m, n, k, b, p, 11, TorchComm(), GpuOps(dev), omega=om)
+    ref = O.trqrcp(A, k, b=b, p=p, seed=11, allow_large_k=True)
+    assert res.achieved == ref.achieved_rank
+    assert np.array_equal(res.perm, ref.perm)
+    assert [res.counters.trailing_passes, res.counters.blas3_volume] == \
+        [ref.counters.trailing_passes, ref.counters.blas3_volume]
+    W = S.cpu().numpy().T
+    R = np.triu(W[m + k:m + k + res.achieved])
+    assert np.abs(R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
+    assert np.abs(W[m:m + res.achieved] - ref.w_t).max() <= 1e-10 * np.abs(ref.w_t).max()
+    assert np.array_equal(W[:m], A[:, ref.perm])
+
+
+def test_public_multi_gpu_api_world1(nccl1):
+    """distributed.rqrcp / trqrcp / tuxv (the reference's signatures, one
+    process per GPU) return the drop-in result objects: same pivots, R, w_t,
+    blocks and counters as the oracle, methods (residual, Q columns) working."""
+    import paper_2008_04447_b200.distributed as D
+    A = gauss(700, 600, 21)
+    pf = D.rqrcp(A, 600, b=32, p=8, seed=0, omega="host")
+    ref = O.rqrcp(A, 600, b=32, p=8, seed=0)
+    assert pf.achieved_rank == ref.achieved_rank and np.array_equal(pf.perm, ref.perm)
+    assert np.abs(pf.R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
+    assert len(pf.blocks) == len(ref.blocks)
+    assert [pf.counters.trailing_passes, pf.counters.blas3_volume] == \
+        [ref.counters.trailing_passes, ref.counters.blas3_volume]
+    assert pf.rel_residual(A) <= 1e-12
+    Q = pf.q_columns()
+    assert np.abs(Q.T @ Q - np.eye(Q.shape[1])).max() <= 1e-12
+    tf = D.trqrcp(A, 96, b=32, p=8, seed=1, omega="host")
+    tref = O.trqrcp(A, 96, b=32, p=8, seed=1)
+    assert np.array_equal(tf.perm, tref.perm)
+    assert np.abs(tf.R - tref.R).max() <= 1e-10 * np.abs(tref.R).max()
+    assert np.abs(tf.w_t - tref.w_t).max() <= 1e-10 * np.abs(tref.w_t).max()
+    assert abs(tf.rel_residual(A, 96) - tref.rel_residual(A, 96)) <= 1e-10 * tref.rel_residual(A, 96)
+    for j_max in (1, 2):
+        x = D.tuxv(A, 24, j_max=j_max, b=8, p=8, seed=2, omega="host")
+        xref = O.tuxv(A, 24, j_max=j_max, b=8, p=8, seed=2)
+        assert np.abs(x.reconstruct() - xref.reconstruct()).max() <= 1e-9 * np.abs(A).max()
+        assert [x.counters.trailing_passes, x.counters.blas3_volume] == \
+            [xref.counters.trailing_passes, xref.counters.blas3_volume]
+    with pytest.raises(ValueError, match="non-finite"):
+        B = A.copy()
+        B[3, 4] = np.nan
+        D.rqrcp(B, 10, b=8, p=4)
