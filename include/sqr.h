@@ -256,6 +256,14 @@ int sqr_gather_rows(const double* src, int64_t lds, int64_t rows, int64_t cols, 
                     double* dst, int64_t ldd, void* stream);
 int sqr_scatter_rows(const double* src, int64_t lds, int64_t rows, int64_t cols, const int64_t* idx,
                      double* dst, int64_t ldd, void* stream);
+/* ------------------------------------------------------------ Jacobi SVD
+ * One-sided Jacobi SVD of W (m x n, m >= n, n <= 4096; jacobi.py:50-117) on
+ * one CTA: W is rotated in place into U diag(sigma), V (n x n, ldv) gets
+ * the accumulated rotations, sigma[c] the column norms (unsorted) and order
+ * their stable descending order; info[0] = sweeps used, -1 if max_sweeps
+ * did not converge.  tuxv(refine_sigma=True) uses it (randomized.py:402-403). */
+int sqr_jacobi_svd(double* W, int64_t ldw, int64_t m, int64_t n, double* V, int64_t ldv, double* sigma,
+                   int64_t* order, int max_sweeps, int32_t* info, void* stream);
 #ifdef __cplusplus
 }
 #endif

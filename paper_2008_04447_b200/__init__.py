@@ -9,14 +9,14 @@ __version__ = "0.1.0"
 
 from .counters import CommCounters
 from .factor import (PivotedFactorization, ReflectorBlock, TruncatedFactorization, TuxvResult, apply_blocks_q,
-                     apply_blocks_qt, blocks_q_columns, invert_permutation, qr_blocked, qrcp_blas2, qrcp_blocked,
+                     apply_blocks_qt, blocks_q_columns, invert_permutation, jacobi_svd, qr_blocked, qrcp_blas2, qrcp_blocked,
                      rqrcp, rsrqrcp, ssrqrcp, trqrcp, tuxv, wy_compose)
 from .rng import NormalStream, device_giid, giid, normals
 from . import callers  # noqa: E402  (quality / estimators callers of the hot path)
 
 __all__ = [
     "CommCounters", "PivotedFactorization", "ReflectorBlock", "TruncatedFactorization", "TuxvResult",
-    "apply_blocks_q", "apply_blocks_qt", "blocks_q_columns", "invert_permutation", "qr_blocked", "qrcp_blas2",
+    "apply_blocks_q", "apply_blocks_qt", "blocks_q_columns", "invert_permutation", "jacobi_svd", "qr_blocked", "qrcp_blas2",
     "qrcp_blocked", "rqrcp", "rsrqrcp", "ssrqrcp", "trqrcp", "tuxv", "wy_compose", "NormalStream",
     "device_giid", "giid", "normals",
 ]

@@ -78,6 +78,7 @@ SIGNATURES = {
     "sqr_unpack_reflectors": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_gather_rows": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "sqr_scatter_rows": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
+    "sqr_jacobi_svd": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_int, c_ptr, c_ptr]),
 }
 
 # struct sqr_status (include/sqr.h)

@@ -109,8 +109,9 @@ def run_quality(A, algorithm: str, rank: int, block: int = 32, pad: int = 8, see
     """quality.py:120-162: relative Frobenius errors over the rank grid, min /
     lower-median / max over `reps` seeded repetitions (one for the
     deterministic algorithms).  "svd" rows are the Eckart-Young errors from the
-    device SVD's singular values (the reference forms them from a Jacobi SVD;
-    both are the optimal rank-r errors to rounding)."""
+    singular values of the device Jacobi SVD (sqr_jacobi_svd; the reference
+    forms U diag(s) V^T of its Jacobi SVD, the same optimal rank-r errors to
+    rounding)."""
     if algorithm not in ALGORITHMS:
         raise ValueError(f"unknown algorithm {algorithm!r}")
     Ad = _device_matrix(A)
@@ -121,7 +122,16 @@ def run_quality(A, algorithm: str, rank: int, block: int = 32, pad: int = 8, see
     reps_eff = 1 if algorithm in DETERMINISTIC_ALGORITHMS else max(1, reps)
     errs: dict[int, list[float]] = {r: [] for r in ranks}
     if algorithm == "svd":
-        s = torch.linalg.svdvals(Ad)
+        if min(Ad.shape) <= 4096:   # the reference's Jacobi SVD (quality.py:133), on the device
+            W = F.ColMajor.empty(*Ad.shape, Ad.device) if Ad.shape[0] >= Ad.shape[1] else None
+            if W is not None:
+                W.view().copy_(Ad)
+            else:
+                W = F.ColMajor.empty(Ad.shape[1], Ad.shape[0], Ad.device)
+                W.view().copy_(Ad.T)
+            s = F._jacobi_svd_dev(W)[1]
+        else:
+            s = torch.linalg.svdvals(Ad)
         tail = torch.flip(torch.cumsum(torch.flip(s * s, [0]), 0), [0])  # tail[r] = sum_{i >= r} s_i^2
         for r in ranks:
             errs[r].append(float(torch.sqrt(tail[r]) / fro) if r < s.numel() else 0.0)

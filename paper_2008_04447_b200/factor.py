@@ -878,6 +878,66 @@ def _qlp(tf, m: int, n: int, b: int, j_max: int, refine_sigma: bool, a_times, at
             v_blocks = vf._composed_fn()
             X = vf.R_device(dev)[:kh, :kh].T.contiguous()
     sig = torch.abs(torch.diagonal(X))
-    if refine_sigma:
-        sig = torch.linalg.svdvals(X)
+    if refine_sigma:                                   # randomized.py:402-403
+        Xc = ColMajor.empty(kh, kh, dev)
+        Xc.view().copy_(X)
+        sig = _jacobi_svd_dev(Xc)[1]
     return TuxvResult(_compose_all(u_blocks), X, _compose_all(v_blocks), sig, kh, cnt, m, n)
+
+
+# ------------------------------------------------------------ Jacobi SVD
+_JACOBI_SWEEPS = 60
+
+
+def _jacobi_svd_dev(M: ColMajor, want_u: bool = False):
+    """(U, sigma, V) of the m x n device matrix M (m >= n), one-sided Jacobi
+    on the device (sqr_jacobi_svd, jacobi.py:50-117); M is overwritten.
+    U is None unless want_u."""
+    m, n = M.m, M.n
+    dev = M.t.device
+    V = ColMajor.empty(n, n, dev)
+    sig = torch.empty(n, dtype=torch.float64, device=dev)
+    order = torch.empty(n, dtype=torch.int64, device=dev)
+    info = torch.zeros(2, dtype=torch.int32, device=dev)
+    _lib.check(_lib.lib().sqr_jacobi_svd(M.ptr, M.ld, m, n, V.ptr, V.ld, ptr(sig), ptr(order), _JACOBI_SWEEPS,
+                                         ptr(info), stream_handle()), "sqr_jacobi_svd")
+    if int(info[0].item()) < 0:
+        raise np.linalg.LinAlgError("Jacobi sweeps did not converge")
+    L = _lib.lib()
+    sig = sig[order]
+    Vs = ColMajor.empty(n, n, dev)
+    _lib.check(L.sqr_copy_columns(V.ptr, V.ld, n, ptr(order), Vs.ptr, Vs.ld, None, n, stream_handle()), "sort V")
+    if not want_u:
+        return None, sig, Vs
+    Ws = ColMajor.empty(m, n, dev)
+    _lib.check(L.sqr_copy_columns(M.ptr, M.ld, m, ptr(order), Ws.ptr, Ws.ld, None, n, stream_handle()), "sort W")
+    smax = float(sig[0])
+    r = int(torch.count_nonzero(sig > smax * m * np.finfo(np.float64).eps))
+    U = ColMajor.empty(m, n, dev, zero=True)
+    if r:
+        U.view()[:, :r] = Ws.view()[:, :r] / sig[:r]
+    if r < n:   # orthonormal completion: columns r..n of the complete QR of U[:, :r] (jacobi.py:40-47)
+        Ur = ColMajor.empty(m, r, dev)
+        Ur.view().copy_(U.view()[:, :r])
+        qf = _qr_blocked_dev(Ur, r, 32)
+        U.view()[:, r:] = _q_columns_dev(qf.blocks, m, n, dev).view()[:, r:]
+    return U, sig, Vs
+
+
+def jacobi_svd(A):
+    """Economy SVD (U, sigma, V), A = U diag(sigma) V^T, sigma descending, by
+    one-sided Jacobi on the device (jacobi.py:50-117; same rotations, sweep
+    rule, ordering and rank-deficient completion)."""
+    M, _ = _load(A)
+    m, n = M.m, M.n
+    if min(m, n) > 4096:
+        raise ValueError("jacobi_svd targets desk-scale matrices (min dim <= 4096)")
+    if m < n:
+        V, s, U = jacobi_svd(_transpose(M).view())
+        return U, s, V
+    if n == 0:
+        return np.zeros((m, 0)), np.zeros(0), np.zeros((0, 0))
+    if float(torch.linalg.norm(M.view())) == 0.0:
+        return np.eye(m, n), np.zeros(n), np.eye(n)
+    U, sig, V = _jacobi_svd_dev(M, want_u=True)
+    return U.numpy(), sig.cpu().numpy(), V.numpy()

@@ -331,3 +331,43 @@ def test_concurrent_threads_disjoint_data(same_stream):
         t.join()
     torch.cuda.synchronize()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("shape,kind", [((100, 100), "gauss"), ((300, 64), "gauss"), ((40, 90), "gauss"),
+                                        ((80, 60), "rankdef"), ((33, 33), "decay"), ((20, 7), "zero")])
+def test_jacobi_svd_matches_oracle(shape, kind):
+    """Device one-sided Jacobi SVD (sqr_jacobi_svd) against the oracle's
+    restatement of jacobi.py:50-117: singular values to 1e-12 relative, the
+    same rotations (U, V equal to 1e-9), the rank-deficient completion
+    orthonormal."""
+    m, n = shape
+    if kind == "gauss":
+        A = gauss(m, n, 3)
+    elif kind == "rankdef":
+        A = np.asfortranarray(gauss(m, 17, 4) @ gauss(17, n, 5))
+    elif kind == "decay":
+        A = np.asfortranarray(O.synth_decay(m, n, 0.6, seed=2))
+    else:
+        A = np.zeros(shape, order="F")
+    U, s, V = G.jacobi_svd(A)
+    Ur, sr, Vr = O.jacobi_svd(A)
+    k = min(m, n)
+    assert U.shape == Ur.shape and V.shape == Vr.shape and s.shape == sr.shape
+    if kind == "zero":
+        assert np.array_equal(s, sr)
+        return
+    assert np.abs(s - sr).max() <= 1e-12 * sr[0]
+    r = int(np.count_nonzero(sr > sr[0] * 1e-10))
+    assert np.abs(U[:, :r] - Ur[:, :r]).max() <= 1e-9 and np.abs(V[:, :r] - Vr[:, :r]).max() <= 1e-9
+    assert np.abs(U.T @ U - np.eye(k)).max() <= 1e-12
+    assert np.abs((U * s) @ V.T - A).max() <= 1e-12 * sr[0]
+
+
+def test_tuxv_refine_sigma_uses_jacobi():
+    g = load_golden("x_refine")
+    kw = golden_kwargs(g)
+    kw["refine_sigma"] = True
+    res = G.tuxv(g["A"], **kw, omega="host")
+    assert np.abs(res.sigma_est - g["sigma_est"]).max() <= 1e-12 * g["sigma_est"].max()
+    X = res.X
+    assert np.abs(res.sigma_est - O.jacobi_svd(X)[1]).max() <= 1e-13 * res.sigma_est.max()
