@@ -31,8 +31,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "RQRCP/TRQRCP fp64 GFLOP/s (n=32768) at 1/2/4/8 B200; TUXV time-to-rank-k"
-PEAK_FP64_TFLOPS = 37.0   # builder-measured DMMA microbenchmark, profiles/fp64_peak_r01.log
-PEAK_SOURCE = ("builder-measured fp64 DMMA peak (mma.sync f64 microbenchmark, profiles/fp64_peak_r01.log; "
+PEAK_FP64_TFLOPS = 37.0   # builder-measured DMMA microbenchmark, profiles/fp64_peak.log
+PEAK_SOURCE = ("builder-measured fp64 DMMA peak (mma.sync f64 microbenchmark, profiles/fp64_peak.log; "
                "cuBLAS DGEMM 8192^3 = 35.4 TF); MEASURED_PEAKS.json has no fp64 entry")
 
 
@@ -360,6 +360,8 @@ def main():
     ap.add_argument("--cpu-sample-n", type=int, default=4096)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the TRQRCP / TUXV secondary timings")
+    ap.add_argument("--collectives", choices=["nccl", "symm"], default="nccl",
+                    help="multi-GPU: host-launched NCCL, or device-initiated puts into symmetric memory")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

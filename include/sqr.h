@@ -264,6 +264,27 @@ int sqr_scatter_rows(const double* src, int64_t lds, int64_t rows, int64_t cols,
  * did not converge.  tuxv(refine_sigma=True) uses it (randomized.py:402-403). */
 int sqr_jacobi_svd(double* W, int64_t ldw, int64_t m, int64_t n, double* V, int64_t ldv, double* sigma,
                    int64_t* order, int max_sweeps, int32_t* info, void* stream);
+/* ------------------------------------ device-initiated collectives (NVLink P2P)
+ * The multi-GPU driver's fused collectives (SURVEY.md §8(e) B200-native
+ * upgrade): the producing kernel stores straight into every peer's copy of a
+ * symmetric buffer and publishes an epoch into each peer's flag word (system-
+ * scope release); consumers gate their stream with sqr_peer_wait.  dst_ptrs /
+ * flag_ptrs are DEVICE arrays of peer base pointers (e.g. the buffer_ptrs of
+ * torch.distributed._symmetric_memory); counter is a device u32 owned by the
+ * calling stream, zero before the first call and left at zero.
+ * put: bytes (multiple of 16) from src to dst_ptrs[q] + dst_offset, q < npeers
+ *      -- the panel record broadcast (randomized.py:203-207 on every rank);
+ * put_columns: dst_ptrs[q][didx[j] * ldd + r] = src[j * lds + r] -- this
+ *      rank's sample-update columns into their global positions of every
+ *      replica (sketch.py:132-149): all-gather + assembly in one kernel;
+ * wait: until flags[i] >= epoch, i < nflags (acquire, system scope). */
+int sqr_peer_put(const void* src, int64_t bytes, void* const* dst_ptrs, int64_t dst_offset, int npeers,
+                 unsigned long long* const* flag_ptrs, int slot, unsigned long long epoch, unsigned* counter,
+                 void* stream);
+int sqr_peer_put_columns(const double* src, int64_t lds, int64_t rows, int64_t ncols, const int64_t* didx,
+                         double* const* dst_ptrs, int64_t ldd, int npeers, unsigned long long* const* flag_ptrs,
+                         int slot, unsigned long long epoch, unsigned* counter, void* stream);
+int sqr_peer_wait(const unsigned long long* flags, int nflags, unsigned long long epoch, void* stream);
 #ifdef __cplusplus
 }
 #endif

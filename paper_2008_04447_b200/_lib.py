@@ -78,6 +78,10 @@ SIGNATURES = {
     "sqr_unpack_reflectors": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr]),
     "sqr_gather_rows": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
     "sqr_scatter_rows": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_ptr]),
+    "sqr_peer_put": (c_int, [c_ptr, c_i64, c_ptr, c_i64, c_int, c_ptr, c_int, c_u64, c_ptr, c_ptr]),
+    "sqr_peer_put_columns": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_int, c_ptr, c_int, c_u64,
+                                     c_ptr, c_ptr]),
+    "sqr_peer_wait": (c_int, [c_ptr, c_int, c_u64, c_ptr]),
     "sqr_jacobi_svd": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_int, c_ptr, c_ptr]),
 }
 

@@ -157,6 +157,77 @@ class TorchComm:
         return float(t.item())
 
 
+def _gather_sample(ops, comm, slab, lay, p0, ell):
+    """Replicated sample for positions >= p0 from every rank's slab: the ops'
+    fused path if it has one (GpuOps over SymmComm: one put_columns kernel),
+    else all-gather + assembly."""
+    if hasattr(ops, "gather_sample"):
+        return ops.gather_sample(slab, lay, p0, ell, comm)
+    parts = comm.all_gather(ops.pad_slab(slab, lay, p0))
+    return ops.assemble(parts, lay, ell) if p0 == 0 else ops.assemble_next(parts, lay, p0, ell)
+
+
+class SymmComm(TorchComm):
+    """TorchComm plus one symmetric device allocation for the device-initiated
+    collectives of csrc/peer.cu (SURVEY.md §8(e) "B200-native upgrade"): the
+    panel record and the replicated sample live in symmetric buffers, the
+    producing rank's kernel stores into every peer's copy over NVLink and
+    releases an epoch into the peers' flag words, consumers wait on the
+    device.  No host-launched NCCL call and no host round trip sits between
+    a producer and its consumers; the column moves keep NCCL point-to-point.
+
+    Layout of the region: [flags: 2 kinds x P u64 | caller buffers ...];
+    every rank holds the same layout, peer base pointers come from the
+    torch.distributed._symmetric_memory rendezvous."""
+
+    KIND_PANEL, KIND_SAMPLE = 0, 1
+
+    def __init__(self, group=None, device=None):
+        super().__init__(group)
+        self.dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.symm = True
+        self.buf = None
+        self.epochs = [0, 0]          # per kind; advanced identically on every rank
+        self.counter = torch.zeros(16, dtype=torch.int32, device=self.dev)
+        self.flag_bytes = ((2 * self.size * 8 + 255) // 256) * 256
+
+    def allocate(self, nbytes: int) -> int:
+        """Collective: (re)allocate the region with >= nbytes of caller space;
+        returns the offset of the caller space."""
+        import torch.distributed._symmetric_memory as symm_mem
+        total = self.flag_bytes + int(nbytes)
+        if self.buf is not None and self.buf.numel() >= total:
+            return self.flag_bytes
+        group = self.group if self.group is not None else dist.group.WORLD
+        try:
+            symm_mem.enable_symm_mem_for_group(group.group_name)
+        except Exception:  # pragma: no cover - newer torch enables it implicitly
+            pass
+        buf = symm_mem.empty(total, dtype=torch.uint8, device=self.dev)
+        buf.zero_()
+        self.h = symm_mem.rendezvous(buf, group.group_name)
+        self.buf = buf
+        self.base = [int(x) for x in self.h.buffer_ptrs]
+        torch.cuda.synchronize(self.dev)
+        self.h.barrier()
+        self.epochs = [0, 0]
+        return self.flag_bytes
+
+    def peer_ptrs(self, offset: int, exclude_self: bool = False) -> torch.Tensor:
+        ptrs = [b + offset for q, b in enumerate(self.base) if not (exclude_self and q == self.rank)]
+        return torch.tensor(ptrs, dtype=torch.int64, device=self.dev)
+
+    def flag_ptrs(self, exclude_self: bool = False) -> torch.Tensor:
+        return self.peer_ptrs(0, exclude_self)
+
+    def local_flags(self, kind: int) -> int:
+        return self.buf.data_ptr() + 8 * kind * self.size
+
+    def next_epoch(self, kind: int) -> int:
+        self.epochs[kind] += 1
+        return self.epochs[kind]
+
+
 # ---------------------------------------------------------------- the loop
 @dataclass
 class DistResult:
@@ -182,8 +253,7 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
     perm = np.arange(n, dtype=np.int64)
     taus = np.zeros(max(k, 1))
     # 1. sketch: local slab, all-gathered into global column order.
-    B = ops.assemble(comm.all_gather(ops.pad_slab(ops.sketch(A_local, m, ell, seed, omega, gloc), lay, 0)),
-                     lay, ell)
+    B = _gather_sample(ops, comm, ops.sketch(A_local, m, ell, seed, omega, gloc), lay, 0, ell)
     achieved, nblocks, reason = 0, 0, "k_reached"
     first = True
     # The panel's outcome (bhat, taus, R11) is read LAZILY: block J's trailing
@@ -264,7 +334,7 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         s0 = lay.first_local_at_or_after(r, achieved)
         mine = gloc[s0:]
         Bn_loc = ops.sample_update_local(samp, A_local, s0, mine - i0, i0, bb, pan)
-        B = ops.assemble_next(comm.all_gather(ops.pad_slab(Bn_loc, lay, achieved)), lay, achieved, ell)
+        B = _gather_sample(ops, comm, Bn_loc, lay, achieved, ell)
     if pend is not None:
         settle(pend, ops.read_tail(pend[2]), False)
     counters = rqrcp_counters(m, n, b, ell, achieved, nblocks,
@@ -294,8 +364,7 @@ def trqrcp_block_cyclic(S_local, m: int, n: int, k: int, b: int, p: int, seed: i
         ops.begin(lay, m, ell)
     perm = np.arange(n, dtype=np.int64)
     taus = np.zeros(max(k, 1))
-    B = ops.assemble(comm.all_gather(ops.pad_slab(ops.sketch(S_local, m, ell, seed, omega, gloc), lay, 0)),
-                     lay, ell)
+    B = _gather_sample(ops, comm, ops.sketch(S_local, m, ell, seed, omega, gloc), lay, 0, ell)
     Yg = ops.new_yg(m, k)
     achieved, nblocks, reason = 0, 0, "k_reached"
     first = True
@@ -343,7 +412,7 @@ def trqrcp_block_cyclic(S_local, m: int, n: int, k: int, b: int, p: int, seed: i
         s0 = lay.first_local_at_or_after(r, achieved)
         mine = gloc[s0:]
         Bn_loc = ops.sample_update_local(samp, S_local, s0, mine - i0, i0, bb, pan, r_row0=m + k + i0)
-        B = ops.assemble_next(comm.all_gather(ops.pad_slab(Bn_loc, lay, achieved)), lay, achieved, ell)
+        B = _gather_sample(ops, comm, Bn_loc, lay, achieved, ell)
     counters = trqrcp_counters(m, n, b, ell, achieved, nblocks)
     res = DistResult(achieved, nblocks, reason, perm, S_local, taus[:achieved], counters)
     res.Yg = Yg
@@ -382,7 +451,7 @@ class GpuOps:
     sample QRCP status + moves, and the broadcast panel tail: status, taus,
     R11) and uploads one packed index array for the column moves."""
 
-    def __init__(self, device):
+    def __init__(self, device, comm=None):
         from . import _lib
         from ._dev import Workspace
         self.L = _lib.lib()
@@ -391,6 +460,9 @@ class GpuOps:
         self.Workspace = Workspace
         self._keep = []
         self._shape = None
+        # SymmComm: panel broadcast and sample all-gather as device-initiated
+        # NVLink puts into symmetric buffers (csrc/peer.cu)
+        self.symm = comm if getattr(comm, "symm", False) else None
 
     # helpers
     def _s(self):
@@ -420,14 +492,33 @@ class GpuOps:
             return
         self._shape = key
         n, b = lay.n, lay.b
+        self.b = b
         f64 = dict(dtype=torch.float64, device=self.dev)
-        self.Bglob = torch.zeros((max(n, 1), ell), **f64)            # replicated sample, global positions
+        prec = ((b * m + b + b * b + 9) + 1) // 2 * 2                  # panel record doubles (16-byte multiple)
+        if self.symm is not None:
+            # double-buffered (block parity) panel records and replicated samples
+            bg = max(n, 1) * ell
+            off = self.symm.allocate(8 * 2 * (bg + prec))
+            base = self.symm.buf[off:off + 8 * 2 * (bg + prec)].view(torch.float64)
+            self.Bglobs = [base[i * bg:(i + 1) * bg].view(max(n, 1), ell) for i in range(2)]
+            self.pbufs = [base[2 * bg + i * prec:2 * bg + (i + 1) * prec] for i in range(2)]
+            self.off_B = [off + 8 * i * bg for i in range(2)]
+            self.off_P = [off + 8 * (2 * bg + i * prec) for i in range(2)]
+            self.put_B = [self.symm.peer_ptrs(o) for o in self.off_B]
+            self.put_P = [self.symm.peer_ptrs(o, exclude_self=True) for o in self.off_P]
+            self.flags_all = self.symm.flag_ptrs()
+            self.flags_peers = self.symm.flag_ptrs(exclude_self=True)
+            self.Bglob = self.Bglobs[0]
+            self.pbuf = self.pbufs[0]
+        else:
+            self.Bglob = torch.zeros((max(n, 1), ell), **f64)            # replicated sample, global positions
         self.Bf = torch.zeros((max(n, 1), ell), **f64)
         self.lperm = torch.zeros(max(n, 1), dtype=torch.int64, device=self.dev)
         self.ctl = torch.zeros(128 + 4 * (4 * b + 8), dtype=torch.uint8, device=self.dev)
         self.staus = torch.zeros(b, **f64)
         # panel broadcast record: [Y (b x m) | taus (b) | R11 (b x b) | status (9 doubles)]
-        self.pbuf = torch.zeros(b * m + b + b * b + 9, **f64)
+        if self.symm is None:
+            self.pbuf = torch.zeros(prec, **f64)
         self.T = torch.zeros((b, b), **f64)
         nmax = lay.n_local_max()
         self.slab = torch.zeros((max(nmax, 1), ell), **f64)
@@ -478,6 +569,31 @@ class GpuOps:
 
     def assemble(self, parts, lay, ell):
         return self._assemble(parts, lay, ell, 0)
+
+    def gather_sample(self, slab, lay, p0, ell, comm):
+        """Replicated sample for positions >= p0.  SymmComm: this rank's slab
+        columns go straight to their global positions in every peer's sample
+        (one sqr_peer_put_columns: all-gather + assembly), then a device-side
+        wait for every rank's epoch.  Else NCCL all-gather + assembly."""
+        if self.symm is None:
+            parts = comm.all_gather(self.pad_slab(slab, lay, p0))
+            return self._assemble(parts, lay, ell, p0)
+        sy = self.symm
+        par = (p0 // lay.b) & 1
+        ep = sy.next_epoch(sy.KIND_SAMPLE)
+        s0 = lay.first_local_at_or_after(comm.rank, p0)
+        cnt = lay.n_local(comm.rank) - s0
+        self._chk(self.L.sqr_peer_put_columns(slab.data_ptr(), ell, ell, max(cnt, 0),
+                                              self.gidx[comm.rank][s0:].data_ptr(), self.put_B[par].data_ptr(), ell,
+                                              comm.size, self.flags_all.data_ptr(), sy.KIND_SAMPLE * comm.size
+                                              + comm.rank, ep, sy.counter.data_ptr(), self._s()), "peer_put_columns")
+        self._chk(self.L.sqr_peer_wait(sy.local_flags(sy.KIND_SAMPLE), comm.size, ep, self._s()), "peer_wait")
+        self.Bglob = self.Bglobs[par]
+        return self.Bglob[p0:]
+
+    def _select_panel_buffer(self, i0):
+        if self.symm is not None:
+            self.pbuf = self.pbufs[(i0 // self.b) & 1]
 
     def assemble_next(self, parts, lay, achieved, ell):
         return self._assemble(parts, lay, ell, achieved)
@@ -564,6 +680,7 @@ class GpuOps:
         return Y, taus, R11, st, self.pbuf[:y + bb + bb * bb + 9], self.pbuf[y:y + bb + bb * bb + 9]
 
     def panel(self, A, lc, i0, m, w, bb, is_owner):
+        self._select_panel_buffer(i0)
         mr = m - i0
         Y, taus, R11, st, rec, tail = self._panel_views(mr, bb)
         if is_owner:
@@ -578,7 +695,22 @@ class GpuOps:
 
     def broadcast_panel(self, pan, owner, comm, mr, bb):
         _, _, _, _, rec, tail = self._panel_views(mr, bb)
-        comm.broadcast(rec, owner)           # one message: Y, taus, R11, status
+        if self.symm is None:
+            comm.broadcast(rec, owner)       # one message: Y, taus, R11, status
+        elif comm.size > 1:
+            # the owner stores the record into every peer's copy (NVLink P2P)
+            # and releases the epoch; the others gate their stream on it
+            sy = self.symm
+            ep = sy.next_epoch(sy.KIND_PANEL)
+            par = 0 if self.pbuf.data_ptr() == self.pbufs[0].data_ptr() else 1
+            if comm.rank == owner:
+                nbytes = ((rec.numel() * 8 + 15) // 16) * 16
+                self._chk(self.L.sqr_peer_put(rec.data_ptr(), nbytes, self.put_P[par].data_ptr(), 0, comm.size - 1,
+                                              self.flags_peers.data_ptr(), sy.KIND_PANEL * comm.size + owner, ep,
+                                              sy.counter.data_ptr() + 4, self._s()), "peer_put")
+            else:
+                self._chk(self.L.sqr_peer_wait(sy.local_flags(sy.KIND_PANEL) + 8 * owner, 1, ep, self._s()),
+                          "peer_wait")
         pan.tail = tail                      # read with the next block's sample record
         return pan
 
@@ -639,6 +771,7 @@ class GpuOps:
     def tr_panel(self, S, lc, i0, m, k, w, bb, is_owner, Yg):
         """Owner: panel = work[i0:, sel] - Yg[i0:, :i0] Wg[:i0, sel] (randomized.py:304-306),
         then its Householder QR (:307) into the broadcast record."""
+        self._select_panel_buffer(i0)
         mr = m - i0
         Y, taus, R11, st, rec, tail = self._panel_views(mr, bb)
         if is_owner:
@@ -784,14 +917,14 @@ def bench_main(args, bench):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist.init_process_group("nccl", device_id=dev)
-    comm = TorchComm()
+    comm = SymmComm(None, dev) if getattr(args, "collectives", "nccl") == "symm" else TorchComm()
     from . import _lib
     L = _lib.lib()
     m = n = args.n
     b, p = args.b, args.p
     lay = BlockCyclic(n, b, comm.size)
     A0 = local_giid(m, n, b, 5, lay, comm.rank, dev)
-    ops = GpuOps(dev)
+    ops = GpuOps(dev, comm)
     tracer = None
     if os.environ.get("SQR_DIST_TRACE"):
         tracer = _OpsTimer(ops, dev)
@@ -856,7 +989,8 @@ def bench_main(args, bench):
         line = {"metric": bench.METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": comm.size,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": dict(bench.base_config(args, f"column block-cyclic x{comm.size} (NCCL)"),
+                "config": dict(bench.base_config(args, f"column block-cyclic x{comm.size} "
+                                                       f"({'symmetric-memory puts' if getattr(comm, 'symm', False) else 'NCCL'})"),
                                achieved_rank=res.achieved, l2="inputs larger than L2; no flush needed"),
                 "roofline": {"bound": "tensor", "kernel": dom, "achieved": ach_tf, "peak": bench.PEAK_FP64_TFLOPS,
                              "unit": "TFLOP/s", "frac": (ach_tf / bench.PEAK_FP64_TFLOPS) if ach_tf else None,
@@ -877,11 +1011,24 @@ def bench_main(args, bench):
 # one process per GPU: every rank calls with the SAME full A (host array or
 # tensor) and gets the same drop-in result object, assembled on every rank.
 # Each rank uploads only its own block-cyclic columns.
-def _comm(group):
+_COMMS: dict = {}
+
+
+def _comm(group, collectives="nccl", dev=None):
+    """collectives="nccl": host-launched NCCL broadcast / all-gather;
+    "symm": device-initiated puts into symmetric memory (SymmComm, csrc/peer.cu).
+    A SymmComm (and its symmetric region) is kept per (group, device)."""
     if not dist.is_available() or not dist.is_initialized():
         raise RuntimeError("distributed.rqrcp/trqrcp/tuxv need an initialised torch.distributed process group "
                            "(one process per GPU, backend 'nccl')")
-    return TorchComm(group)
+    if collectives == "nccl":
+        return TorchComm(group)
+    if collectives != "symm":
+        raise ValueError("collectives must be 'nccl' or 'symm'")
+    key = (id(group), str(dev))
+    if key not in _COMMS:
+        _COMMS[key] = SymmComm(group, dev)
+    return _COMMS[key]
 
 
 def _local_slab(A, cols: np.ndarray, m: int, rows: int, dev) -> torch.Tensor:
@@ -965,7 +1112,8 @@ def _check_finite_all(cnt, comm):
         raise ValueError("A contains non-finite entries")
 
 
-def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=None, device=None):
+def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=None, device=None,
+          collectives: str = "nccl"):
     """Multi-GPU drop-in of randomized.rqrcp (randomized.py:227-229): column
     block-cyclic over the process group, NCCL.  Returns the reference's
     PivotedFactorization (R, perm, blocks, achieved_rank, counters) on every
@@ -973,7 +1121,7 @@ def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=N
     from . import factor as F
     from ._dev import require_cuda
     dev = require_cuda(device)
-    comm = _comm(group)
+    comm = _comm(group, collectives, dev)
     m, n = _prologue(A, k, b, p, comm, dev)
     ell = b + p
     if k == 0 or ell >= m:   # empty / the deterministic l >= m fallback (randomized.py:172-174): replicated
@@ -981,7 +1129,7 @@ def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=N
     lay = BlockCyclic(n, b, comm.size)
     S, bad = _local_slab(A, lay.global_of_local(comm.rank), m, m, dev)
     _check_finite_all(bad, comm)
-    res = rqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev), omega=_omega_arg(omega, ell, m, seed))
+    res = rqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev, comm), omega=_omega_arg(omega, ell, m, seed))
     W = _gather_columns(S, lay, comm, m, dev)
     ach = res.achieved
     pf = F.PivotedFactorization(m, n, None, None, None, ach, res.counters)
@@ -994,11 +1142,11 @@ def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=N
     return pf
 
 
-def _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device):
+def _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device, collectives="nccl"):
     from . import factor as F
     from ._dev import ColMajor, require_cuda
     dev = require_cuda(device)
-    comm = _comm(group)
+    comm = _comm(group, collectives, dev)
     m, n = _prologue(A, k, b, p, comm, dev)
     if not allow_large_k and k > min(m, n) // 2:
         raise ValueError("trqrcp targets k <= min(m, n)/2; pass allow_large_k=True to override")
@@ -1009,7 +1157,7 @@ def _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device):
     rows = m + 2 * k
     S, bad = _local_slab(A, lay.global_of_local(comm.rank), m, rows, dev)
     _check_finite_all(bad, comm)
-    res = trqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev), omega=_omega_arg(omega, ell, m, seed))
+    res = trqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev, comm), omega=_omega_arg(omega, ell, m, seed))
     SW = _gather_columns(S, lay, comm, rows, dev)
     ach = res.achieved
     tf = F.TruncatedFactorization(m, n, None, None, None, ach, res.counters)
@@ -1030,18 +1178,18 @@ def _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device):
 
 
 def trqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, allow_large_k: bool = False, omega=None,
-           group=None, device=None):
+           group=None, device=None, collectives: str = "nccl"):
     """Multi-GPU drop-in of randomized.trqrcp (randomized.py:250-341); the
     TruncatedFactorization (R, w_t, perm, blocks, counters) on every rank."""
     from . import factor as F
-    tf, *_ = _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device)
+    tf, *_ = _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device, collectives)
     if tf is None:
         return F.trqrcp(A, k, b=b, p=p, seed=seed, allow_large_k=allow_large_k, omega=omega)
     return tf
 
 
 def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refine_sigma: bool = False,
-         allow_large_k: bool = False, omega=None, group=None, device=None):
+         allow_large_k: bool = False, omega=None, group=None, device=None, collectives: str = "nccl"):
     """Multi-GPU drop-in of randomized.tuxv (randomized.py:353-406): the
     distributed TRQRCP, then the QLP flip-flop with A's products formed from
     the local slabs -- A V_k as a sum of per-rank partials (all-reduce of the
@@ -1052,7 +1200,7 @@ def tuxv(A, k: int, j_max: int = 1, b: int = 32, p: int = 8, seed: int = 0, refi
     from ._dev import ColMajor
     if j_max < 1:
         raise ValueError("j_max must be >= 1")
-    tf, S, lay, dev, comm, m, n = _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device)
+    tf, S, lay, dev, comm, m, n = _trqrcp_dist(A, k, b, p, seed, allow_large_k, omega, group, device, collectives)
     if tf is None:
         return F.tuxv(A, k, j_max=j_max, b=b, p=p, seed=seed, refine_sigma=refine_sigma,
                       allow_large_k=allow_large_k, omega=omega)

@@ -134,3 +134,62 @@ def test_public_multi_gpu_api_world1(nccl1):
         B = A.copy()
         B[3, 4] = np.nan
         D.rqrcp(B, 10, b=8, p=4)
+
+
+def test_peer_put_kernels_fake_peers():
+    """csrc/peer.cu with P "peers" that are buffers of this one GPU (the same
+    pointer arrays a symmetric-memory rendezvous provides): every peer copy
+    receives the bytes / the scattered columns, every peer flag the epoch,
+    the arrival counter returns to zero, and the wait passes once the flags
+    carry the epoch."""
+    from paper_2008_04447_b200 import _lib
+    L = _lib.lib()
+    dev = torch.device("cuda", 0)
+    s = torch.cuda.current_stream().cuda_stream
+    P, nbytes = 4, 1 << 20
+    src = torch.randint(0, 255, (nbytes,), dtype=torch.uint8, device=dev)
+    dst = [torch.zeros(nbytes + 4096, dtype=torch.uint8, device=dev) for _ in range(P)]
+    flags = [torch.zeros(8, dtype=torch.int64, device=dev) for _ in range(P)]
+    dptr = torch.tensor([d.data_ptr() for d in dst], dtype=torch.int64, device=dev)
+    fptr = torch.tensor([f.data_ptr() for f in flags], dtype=torch.int64, device=dev)
+    ctr = torch.zeros(4, dtype=torch.int32, device=dev)
+    for ep in (1, 2):
+        _lib.check(L.sqr_peer_put(src.data_ptr(), nbytes, dptr.data_ptr(), 4096, P, fptr.data_ptr(), 3, ep,
+                                  ctr.data_ptr(), s))
+        _lib.check(L.sqr_peer_wait(flags[2].data_ptr() + 8 * 3, 1, ep, s))
+        torch.cuda.synchronize()
+        for q in range(P):
+            assert torch.equal(dst[q][4096:], src) and int(flags[q][3]) == ep
+        assert int(ctr[0]) == 0
+    # put_columns: 3 local columns of a 40-row slab -> global positions 5, 1, 9 of every replica
+    ell, n = 40, 12
+    slab = torch.randn((3, ell), dtype=torch.float64, device=dev)
+    didx = torch.tensor([5, 1, 9], dtype=torch.int64, device=dev)
+    reps = [torch.zeros((n, ell), dtype=torch.float64, device=dev) for _ in range(P)]
+    rptr = torch.tensor([r.data_ptr() for r in reps], dtype=torch.int64, device=dev)
+    _lib.check(L.sqr_peer_put_columns(slab.data_ptr(), ell, ell, 3, didx.data_ptr(), rptr.data_ptr(), ell, P,
+                                      fptr.data_ptr(), 5, 7, ctr.data_ptr(), s))
+    _lib.check(L.sqr_peer_wait(flags[0].data_ptr(), 8, 0, s))
+    torch.cuda.synchronize()
+    for q in range(P):
+        assert torch.equal(reps[q][[5, 1, 9]], slab) and int(reps[q].abs().sum(1).count_nonzero()) == 3
+        assert int(flags[q][5]) == 7
+
+
+@pytest.mark.parametrize("collectives", ["nccl", "symm"])
+def test_public_api_symmetric_collectives_world1(nccl1, collectives):
+    """The public multi-GPU entry points with the device-initiated collectives
+    (SymmComm over torch symmetric memory) match the NCCL path bitwise."""
+    import paper_2008_04447_b200.distributed as D
+    A = gauss(500, 420, 31)
+    pf = D.rqrcp(A, 420, b=32, p=8, seed=0, omega="host", collectives=collectives)
+    ref = O.rqrcp(A, 420, b=32, p=8, seed=0)
+    assert np.array_equal(pf.perm, ref.perm)
+    assert np.abs(pf.R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
+    tf = D.trqrcp(A, 64, b=16, p=8, seed=1, omega="host", collectives=collectives)
+    tref = O.trqrcp(A, 64, b=16, p=8, seed=1)
+    assert np.array_equal(tf.perm, tref.perm)
+    assert np.abs(tf.w_t - tref.w_t).max() <= 1e-10 * np.abs(tref.w_t).max()
+    if collectives == "symm":
+        nc = D.rqrcp(A, 420, b=32, p=8, seed=0, omega="host", collectives="nccl")
+        assert np.array_equal(nc.perm, pf.perm) and np.array_equal(nc.R, pf.R)
