@@ -256,6 +256,11 @@ int sqr_gather_rows(const double* src, int64_t lds, int64_t rows, int64_t cols, 
                     double* dst, int64_t ldd, void* stream);
 int sqr_scatter_rows(const double* src, int64_t lds, int64_t rows, int64_t cols, const int64_t* idx,
                      double* dst, int64_t ldd, void* stream);
+/* X R = S (X, S rows x n; R upper triangular n x n): S11 R11^{-1} of the
+ * sample update for blocks wider than 128 (sketch.py:122-149); upper_s != 0
+ * reads S as upper triangular (entries below its diagonal ignored). */
+int sqr_trsm_right_upper(const double* S, int64_t lds, int64_t rows, int64_t n, const double* R, int64_t ldr,
+                         double* X, int64_t ldx, int upper_s, void* stream);
 /* ------------------------------------------------------------ Jacobi SVD
  * One-sided Jacobi SVD of W (m x n, m >= n, n <= 4096; jacobi.py:50-117) on
  * one CTA: W is rotated in place into U diag(sigma), V (n x n, ldv) gets

@@ -82,6 +82,7 @@ SIGNATURES = {
     "sqr_peer_put_columns": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_i64, c_int, c_ptr, c_int, c_u64,
                                      c_ptr, c_ptr]),
     "sqr_peer_wait": (c_int, [c_ptr, c_int, c_u64, c_ptr]),
+    "sqr_trsm_right_upper": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_i64, c_int, c_ptr]),
     "sqr_jacobi_svd": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_int, c_ptr, c_ptr]),
 }
 

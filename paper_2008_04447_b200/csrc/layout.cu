@@ -137,3 +137,46 @@ extern "C" int sqr_scatter_rows(const double* src, int64_t lds, int64_t rows, in
   return permute_rows<true>(src, lds, rows, cols, idx, dst, ldd, static_cast<cudaStream_t>(stream),
                             "sqr_scatter_rows");
 }
+
+// X R = S for X (rows x n), R upper triangular n x n (ld ldr): the sample
+// update's S11 R11^{-1} for blocks wider than su_prep's 128 (sketch.py:122-149
+// as the row form of its back substitution).  One warp per row, left-looking:
+// X(i, c) = (S(i, c) - sum_{l < c} X(i, l) R(l, c)) / R(c, c), fixed-order
+// warp reduction (deterministic).  upper_s: S is upper triangular (entries
+// below its diagonal, e.g. reflector tails, are read as zero).
+namespace sqr {
+namespace {
+__global__ void __launch_bounds__(256) trsm_ru_kernel(const double* __restrict__ S, int64_t lds, int rows, int n,
+                                                      const double* __restrict__ R, int64_t ldr,
+                                                      double* __restrict__ X, int64_t ldx, int upper_s) {
+  const int lane = threadIdx.x & 31;
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (i >= rows) return;
+  for (int c = 0; c < n; ++c) {
+    if (upper_s && c < i) {
+      if (lane == 0) X[(int64_t)c * ldx + i] = 0.0;
+      continue;
+    }
+    double acc = 0.0;
+    for (int l = (upper_s ? i : 0) + lane; l < c; l += 32) acc = fma(X[(int64_t)l * ldx + i], R[(int64_t)c * ldr + l], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) X[(int64_t)c * ldx + i] = (S[(int64_t)c * lds + i] - acc) / R[(int64_t)c * ldr + c];
+    __syncwarp();
+  }
+}
+}  // namespace
+}  // namespace sqr
+
+extern "C" int sqr_trsm_right_upper(const double* S, int64_t lds, int64_t rows, int64_t n, const double* R,
+                                    int64_t ldr, double* X, int64_t ldx, int upper_s, void* stream) {
+  if (rows <= 0 || n <= 0) return SQR_OK;
+  if (S == nullptr || R == nullptr || X == nullptr || lds < rows || ldx < rows || ldr < n) {
+    set_error("sqr_trsm_right_upper: bad arguments");
+    return SQR_EINVAL;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  ProfScope ps(kTagSampleUpd, s);
+  trsm_ru_kernel<<<(unsigned)cdiv(rows, 8), 256, 0, s>>>(S, lds, (int)rows, (int)n, R, ldr, X, ldx, upper_s);
+  SQR_LAUNCH("trsm_ru_kernel");
+  return SQR_OK;
+}

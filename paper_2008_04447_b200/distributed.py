@@ -199,10 +199,6 @@ class SymmComm(TorchComm):
         if self.buf is not None and self.buf.numel() >= total:
             return self.flag_bytes
         group = self.group if self.group is not None else dist.group.WORLD
-        try:
-            symm_mem.enable_symm_mem_for_group(group.group_name)
-        except Exception:  # pragma: no cover - newer torch enables it implicitly
-            pass
         buf = symm_mem.empty(total, dtype=torch.uint8, device=self.dev)
         buf.zero_()
         self.h = symm_mem.rendezvous(buf, group.group_name)
@@ -1094,7 +1090,7 @@ def _gather_columns(S: torch.Tensor, lay: BlockCyclic, comm, rows: int, dev):
     for q, part in enumerate(parts):
         g = lay.global_of_local(q)
         if g.size:
-            gi = torch.as_tensor(g, device=dev)
+            gi = torch.tensor(g, device=dev)
             _lib.check(_lib.lib().sqr_copy_columns(part.data_ptr(), rows, rows, None, W.ptr, rows, gi.data_ptr(),
                                                    int(g.size), s), "gather columns")
     return W

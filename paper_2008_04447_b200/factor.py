@@ -150,7 +150,7 @@ def _build_t(Yd: ColMajor, taud: torch.Tensor) -> ColMajor:
     """T of I - Y T Y^T = H_1...H_j on the device (householder.py:52-61)."""
     j = Yd.n
     dev = Yd.t.device
-    if j > MAX_ELL:
+    if j > MAX_B:   # the T kernel takes <= 128 reflectors
         return _compose_t_recursive(Yd, taud)
     T = ColMajor.empty(j, j, dev, zero=True)
     with _ws(j * j * 8 + (200 << 20), dev) as ws:
@@ -636,8 +636,14 @@ def _randomized(A, k, b, p, seed, resample, omega=None, _status=None, out=None):
     ell = b + p
     if ell >= m:
         return _fallback_qrcp(M, k, b, True)
-    if b > MAX_B or ell > MAX_ELL:
-        raise ValueError(f"this build supports b <= {MAX_B} and b + p <= {MAX_ELL}")
+    if b > MAX_B or ell > MAX_ELL:   # wider than the fused driver: per-block loop (wide.py)
+        from .wide import rqrcp_wide
+        pf = rqrcp_wide(M, k, b, p, seed, resample, _omega_T(omega, ell, m, seed, dev) if not resample else None)
+        if out is not None:
+            out = _check_out(out, min(k, m), n)
+            out[:pf.achieved_rank] = pf.R
+            pf._R = out[:pf.achieved_rank]
+        return pf
     L = _lib.lib()
     OmT = _omega_T(omega, ell, m, seed, dev)
     nblk = -(-k // b)
@@ -767,8 +773,9 @@ def _trqrcp_dev(M: ColMajor, k, b, p, seed, allow_large_k=False, omega=None, _st
     ell = b + p
     if ell >= m:
         return _truncated_from_pivoted(_fallback_qrcp(M, k, b, True), M)
-    if b > MAX_B or ell > MAX_ELL:
-        raise ValueError(f"this build supports b <= {MAX_B} and b + p <= {MAX_ELL}")
+    if b > MAX_B or ell > MAX_ELL:   # wider than the fused driver: per-block loop (wide.py)
+        from .wide import trqrcp_wide
+        return trqrcp_wide(M, k, b, p, seed, _omega_T(omega, ell, m, seed, dev))
     L = _lib.lib()
     OmT = _omega_T(omega, ell, m, seed, dev)
     A0 = M  # permuted in place (the reference's `work`); the caller's A is untouched

@@ -7,6 +7,9 @@ for generating inputs exactly as the reference does.
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import torch
 
@@ -62,9 +65,26 @@ class NormalStream:
         return out
 
 
-def host_omega(ell: int, m: int, seed: int) -> np.ndarray:
-    """The reference's first draw of every sketch: NormalStream(seed).matrix(l, m)."""
-    return giid(ell, m, seed, 0)
+_CHUNK = 1 << 18
+
+
+def host_omega(ell: int, m: int, seed: int, threads: int | None = None) -> np.ndarray:
+    """The reference's first draw of every sketch: NormalStream(seed).matrix(l, m),
+    bit-identical, drawn by host threads in contiguous counter ranges (NumPy's
+    ufuncs release the GIL; each entry depends only on its counter)."""
+    total = ell * m
+    threads = threads or min(16, os.cpu_count() or 1)
+    if total <= 2 * _CHUNK or threads <= 1:
+        return giid(ell, m, seed, 0)
+    flat = np.empty(total, dtype=np.float64)
+
+    def fill(c0):
+        c1 = min(total, c0 + _CHUNK)
+        flat[c0:c1] = normals(seed, c1 - c0, c0)
+
+    with ThreadPoolExecutor(threads) as ex:
+        list(ex.map(fill, range(0, total, _CHUNK)))
+    return np.asfortranarray(flat.reshape((ell, m), order="F"))
 
 
 def device_giid(rows: int, cols: int, seed: int, offset: int = 0, transpose: bool = False,

@@ -371,3 +371,41 @@ def test_tuxv_refine_sigma_uses_jacobi():
     assert np.abs(res.sigma_est - g["sigma_est"]).max() <= 1e-12 * g["sigma_est"].max()
     X = res.X
     assert np.abs(res.sigma_est - O.jacobi_svd(X)[1]).max() <= 1e-13 * res.sigma_est.max()
+
+
+@pytest.mark.parametrize("fn,m,n,k,b,p,kind", [
+    ("rqrcp", 700, 600, 600, 160, 8, "gauss"),      # b > 128: two sub-panels per block
+    ("rqrcp", 900, 500, 400, 130, 20, "gauss"),     # b + p = 150 > 144
+    ("rqrcp", 600, 520, 520, 300, 4, "lowrank"),    # rank 210 ends inside the second sub-panel
+    ("rqrcp", 400, 380, 380, 256, 0, "zerocol"),    # exact zero columns: a short panel in sub-panel 2
+    ("rsrqrcp", 800, 640, 640, 200, 8, "gauss"),
+    ("trqrcp", 1000, 900, 420, 200, 8, "gauss"),
+    ("trqrcp", 900, 800, 300, 140, 16, "decay"),
+])
+def test_wide_blocks_match_oracle(fn, m, n, k, b, p, kind):
+    """Any b >= 1, p >= 0 (validation.py:75-82): blocks beyond the fused
+    driver's 128 / 144 limits run the per-block loop of wide.py and must
+    reproduce the reference loop (pivots, exits, R, w_t, counters)."""
+    if kind == "gauss":
+        A = gauss(m, n, 70)
+    elif kind == "lowrank":
+        A = lowrank(m, n, 210, 71)
+    elif kind == "decay":
+        A = np.asfortranarray(O.synth_decay(m, n, 10 ** (-8 / n), seed=3))
+    else:
+        A = gauss(m, n, 72)
+        A[:, 150:] = 0.0
+    extra = {} if fn == "rsrqrcp" else {"omega": "host"}
+    got = getattr(G, fn)(A, k, b=b, p=p, seed=4, **extra)
+    if fn == "rsrqrcp":   # device-drawn resamples: compare with the oracle fed the same draws is not possible;
+        ref = O.rsrqrcp(A, k, b=b, p=p, seed=4)   # pivots agree away from ties (Gaussian input)
+    else:
+        ref = getattr(O, fn)(A, k, b=b, p=p, seed=4)
+    check_against(got, ref, A, normwise=kind in ("lowrank", "zerocol", "decay"))
+    if fn == "trqrcp":
+        assert np.abs(got.w_t - ref.w_t).max() <= 1e-10 * np.abs(ref.w_t).max()
+    if fn != "trqrcp" and got.achieved_rank == min(m, n):   # full factorizations: A P = Q R
+        assert got.rel_residual(A) <= 1e-12
+    elif got.achieved_rank:                                   # truncated: the reference's rank-r error
+        assert abs(got.rel_residual(A, got.achieved_rank) - ref.rel_residual(A, got.achieved_rank)) <= \
+            1e-10 * max(ref.rel_residual(A, got.achieved_rank), 1e-300) + 1e-13
