@@ -131,6 +131,23 @@ def cpu_sample(n_sample, b, p, reps=1):
     return lapack_gflop(n_sample, n_sample), times
 
 
+def c5_reference_run():
+    """The full-size C5 run of the REAL reference (tests/golden/c5.npz, written
+    by tests/golden/make_golden_configs.py in the build container): the same
+    workload as this bench line, on the CPU, reported beside the bounded
+    sample."""
+    path = os.path.join(ROOT, "tests", "golden", "c5.npz")
+    if not os.path.exists(path):
+        return None
+    with np.load(path) as z:
+        secs = float(z["seconds"])
+        host = json.loads(str(z["host"]))
+    return {"workload": "C5 rqrcp(giid(32768, 32768, seed=5), 32768, b=128, p=8, seed=0)",
+            "seconds": secs, "value": lapack_gflop(32768, 32768) / secs, "unit": "GFLOP/s", "kind": "reference",
+            "cores": host.get("affinity"), "host": host.get("model"), "where": "build container (no GPU)",
+            "source": "tests/golden/c5.npz (make_golden_configs.py)"}
+
+
 def host_cores():
     try:
         from threadpoolctl import threadpool_info
@@ -320,6 +337,9 @@ def run_ours(args):
         cpu = {"value": g_s / t_s[0], "unit": "GFLOP/s", "cores": host_cores(), "kind": "port",
                "sample": f"oracle port rqrcp on giid({args.cpu_sample_n},{args.cpu_sample_n},seed=5), b={b}, "
                          f"p={p} (full rank), {t_s[0]:.1f} s"}
+        full = c5_reference_run()
+        if full is not None:
+            cpu["full_config"] = full
 
     phases = {t: {"ms_per_step": v[0] / args.steps, "launches_per_step": v[1] / args.steps}
               for t, v in prof.items() if v[1]}
