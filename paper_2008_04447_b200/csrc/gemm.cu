@@ -170,8 +170,11 @@ struct TnLoader2 {
   }
 };
 
+#ifndef SQR_TN_MINB
+#define SQR_TN_MINB 2   // resident CTAs per SM the register budget is sized for
+#endif
 template <int MT, int VEC>
-__global__ void __launch_bounds__(kThreads, 2)
+__global__ void __launch_bounds__(kThreads, SQR_TN_MINB)
     gemm_tn_kernel(int M, int N, int K, double alpha, const double* __restrict__ X, int64_t ldx,
                    const double* __restrict__ C, int64_t ldc, double beta, const double* E,
                    int64_t lde, double* D, int64_t ldd, int kchunk, double* part, unsigned* sems,
@@ -638,7 +641,7 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
   using Cfg = TnCfg<MT, VEC>;
   if (int rc = smem_optin((const void*)gemm_tn_kernel<MT, VEC>, Cfg::SMEM)) return rc;
   const int tiles = (int)cdiv(N, Cfg::BN);
-  const int sms = 2 * sm_count();  // resident CTAs (2 per SM)
+  const int sms = SQR_TN_MINB * sm_count();  // resident CTAs
   // Pick the split count that minimises waves/split (i.e. the padded work),
   // keeping >= 512 K per split; ties go to fewer splits.
   int best = 1;
