@@ -8,6 +8,7 @@ helpers raise.
 from __future__ import annotations
 
 import contextlib
+import os
 import threading
 
 import numpy as np
@@ -68,6 +69,62 @@ class ColMajor:
         return np.asfortranarray(self.view().cpu().numpy())
 
 
+_STAGE_BYTES = 64 << 20          # pinned staging chunk of the pipelined upload
+_PIPELINE_MIN = 32 << 20         # below this a plain copy is as fast
+_staging: dict = {}
+_staging_lock = threading.Lock()
+
+
+def _stagers(device):
+    """Two pinned staging buffers + their "free" events, one pair per device."""
+    key = str(device)
+    with _staging_lock:
+        st = _staging.get(key)
+        if st is None:
+            bufs = [torch.empty(_STAGE_BYTES, dtype=torch.uint8).pin_memory() for _ in range(2)]
+            st = _staging[key] = (bufs, threading.Lock())
+        return st
+
+
+def _h2d_pipelined(src: np.ndarray, dst: torch.Tensor) -> None:
+    """dst (contiguous CUDA tensor) <- src (contiguous pageable host array, same
+    bytes): host threads copy 64 MB chunks into two pinned staging buffers while
+    the copy engine moves the previous chunk, so a pageable input crosses
+    PCIe at pinned-memory speed instead of through the driver's pageable path."""
+    from concurrent.futures import ThreadPoolExecutor
+    sb = src.reshape(-1).view(np.uint8)
+    db = dst.view(-1).view(torch.uint8)
+    total = sb.size
+    (bufs, lock) = _stagers(dst.device)
+    stream = torch.cuda.current_stream(dst.device)
+    events = [None, None]
+    nthr = max(1, min(8, (os.cpu_count() or 1)))
+    with lock, ThreadPoolExecutor(nthr) as ex:
+        for i, c0 in enumerate(range(0, total, _STAGE_BYTES)):
+            c1 = min(total, c0 + _STAGE_BYTES)
+            k = i & 1
+            if events[k] is not None:
+                events[k].synchronize()             # the buffer's previous chunk has left
+            stage = bufs[k].numpy()
+            step = -(-(c1 - c0) // nthr)
+            list(ex.map(lambda j: np.copyto(stage[j:min(c1 - c0, j + step)], sb[c0 + j:min(c1, c0 + j + step)]),
+                        range(0, c1 - c0, step)))
+            db[c0:c1].copy_(bufs[k][:c1 - c0], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(stream)
+            events[k] = ev
+        for ev in events:
+            if ev is not None:
+                ev.synchronize()
+
+
+def _is_pinned(arr: np.ndarray) -> bool:
+    try:
+        return torch.from_numpy(arr).is_pinned()
+    except Exception:
+        return False
+
+
 def upload(A, device, copy: bool = True) -> ColMajor:
     """Copy a 2-D numpy array / torch tensor into fresh column-major device storage."""
     if isinstance(A, torch.Tensor):
@@ -82,12 +139,27 @@ def upload(A, device, copy: bool = True) -> ColMajor:
     arr = np.asarray(A)
     if arr.ndim != 2:
         raise ValueError(f"A must be 2-dimensional, got ndim={arr.ndim}")
-    arr = np.asfortranarray(arr, dtype=np.float64)
     m, n = arr.shape
+    big = arr.dtype == np.float64 and arr.nbytes >= _PIPELINE_MIN and not _is_pinned(arr)
+    if big and arr.flags.c_contiguous and not arr.flags.f_contiguous:
+        # C-ordered host input: rows up as they are, transposed on the device
+        rows = torch.empty((m, n), dtype=torch.float64, device=device)
+        _h2d_pipelined(arr, rows)
+        out = ColMajor.empty(m, n, device)
+        out.view().copy_(rows)
+        return out
+    arr = np.asfortranarray(arr, dtype=np.float64)
     out = ColMajor.empty(m, n, device)
     if m and n:
         host = torch.from_numpy(arr.T)  # (n, m) C-contiguous view of the Fortran array
-        if out.ld == m:
+        if big:
+            if out.ld == m:
+                _h2d_pipelined(arr.T, out.t[:n])
+            else:
+                tmp = torch.empty((n, m), dtype=torch.float64, device=device)
+                _h2d_pipelined(arr.T, tmp)
+                out.t[:n, :m].copy_(tmp)
+        elif out.ld == m:
             out.t[:n].copy_(host, non_blocking=False)
         else:
             out.t[:n, :m].copy_(host)
@@ -144,6 +216,18 @@ def load_checked(A, device, copy: bool = True, check: bool = True) -> ColMajor:
         else:
             M = ColMajor(A.as_strided((n, m), (lds, 1)), m, n, lds)
         bad = _copy_check(A.data_ptr(), lds, m, n, M if copy else None, device) if (copy or check) else 0
+    elif (isinstance(A, np.ndarray) and A.ndim == 2 and A.dtype == np.float64 and A.flags.c_contiguous
+          and not A.flags.f_contiguous and A.nbytes >= _PIPELINE_MIN and not _is_pinned(A)):
+        # C-ordered host input: pipelined upload of the rows, then the tiled
+        # transpose + finite scan in one device pass (no host transpose)
+        m, n = A.shape
+        rows = torch.empty((m, n), dtype=torch.float64, device=device)
+        _h2d_pipelined(A, rows)
+        M = ColMajor.empty(m, n, device)
+        cnt = torch.zeros(1, dtype=torch.int64, device=device)
+        _lib.check(_lib.lib().sqr_copy_check_t(rows.data_ptr(), n, m, n, M.ptr, M.ld, cnt.data_ptr(),
+                                               stream_handle()), "sqr_copy_check_t")
+        bad = int(cnt.item()) if check else 0
     else:
         M = upload(A, device)
         bad = _copy_check(M.ptr, M.ld, M.m, M.n, None, device) if (check and M.m and M.n) else 0

@@ -410,3 +410,26 @@ def test_wide_blocks_match_oracle(fn, m, n, k, b, p, kind):
     elif got.achieved_rank:                                   # truncated: the reference's rank-r error
         assert abs(got.rel_residual(A, got.achieved_rank) - ref.rel_residual(A, got.achieved_rank)) <= \
             1e-10 * max(ref.rel_residual(A, got.achieved_rank), 1e-300) + 1e-13
+
+
+@pytest.mark.parametrize("m,n,order", [(5000, 3001, "F"), (5001, 3000, "F"), (4000, 2500, "C"), (4001, 2499, "C")])
+def test_pipelined_host_upload(m, n, order):
+    """Large pageable host inputs go up through pinned staging chunks
+    (_dev._h2d_pipelined), C-ordered ones transposed on the device: the device
+    copy is bitwise the input, non-finite entries are still counted, and a
+    factorization from the host array equals the one from a device tensor."""
+    from paper_2008_04447_b200._dev import load_checked, upload
+    rng = np.random.default_rng(m + n)
+    A = rng.standard_normal((m, n))
+    A = np.asfortranarray(A) if order == "F" else np.ascontiguousarray(A)
+    assert np.array_equal(upload(A, torch.device("cuda", 0)).numpy(), A)
+    M = load_checked(A, torch.device("cuda", 0))
+    assert np.array_equal(M.numpy(), A)
+    B = A.copy(order=order)
+    B[m // 2, n // 3] = np.inf
+    with pytest.raises(ValueError, match="non-finite"):
+        load_checked(B, torch.device("cuda", 0))
+    if order == "C" and m == 4000:
+        got = G.trqrcp(A, 40, b=16, p=8, seed=2, omega="host")
+        dev = G.trqrcp(torch.from_numpy(A).cuda(), 40, b=16, p=8, seed=2, omega="host")
+        assert np.array_equal(got.perm, dev.perm) and np.array_equal(got.w_t, dev.w_t)

@@ -51,6 +51,13 @@ for mr, w in shapes:
         torch.cuda.synchronize()
         L.sqr_debug_trace(None)
         t = tr.cpu().numpy().astype(np.int64)
+        c1 = [int(t[8 * c + 1]) for c in range(min(w, 40))]
+        c2 = [int(t[8 * c + 2]) for c in range(min(w, 40))]
+        if c1[0]:
+            steps = [c1[i + 1] - c1[i] for i in range(min(w, 40) - 1) if c1[i + 1] and c1[i]]
+            bars = [c2[i] - c1[i] for i in range(min(w, 40)) if c2[i] and c1[i]]
+            print(f"  per-column step (ns): median {int(np.median(steps))}  barrier wait of CTA 0 median "
+                  f"{int(np.median(bars))}  (columns 0..{min(w, 40) - 1})", flush=True)
         for li in range(w // 32):
             bd = t[8 * (40 + li):8 * (40 + li) + 8]
             if bd[0]:
