@@ -98,7 +98,7 @@ def _h2d_pipelined(src: np.ndarray, dst: torch.Tensor) -> None:
     (bufs, lock) = _stagers(dst.device)
     stream = torch.cuda.current_stream(dst.device)
     events = [None, None]
-    nthr = max(1, min(8, (os.cpu_count() or 1)))
+    nthr = max(1, min(16, (os.cpu_count() or 1)))
     with lock, ThreadPoolExecutor(nthr) as ex:
         for i, c0 in enumerate(range(0, total, _STAGE_BYTES)):
             c1 = min(total, c0 + _STAGE_BYTES)
