@@ -1143,10 +1143,17 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
 
 }  // namespace
 
+int64_t sample_epoch_workspace(int64_t ell, int64_t nt, int64_t bb);
+bool sample_epoch_eligible(int64_t ell, int64_t nt);
+int sample_epoch(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf, int64_t ldbf,
+                 int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st, void* ws,
+                 int64_t ws_bytes, cudaStream_t s);
+
 struct SampleWorkspace {
   static int64_t bytes(int64_t ell, int64_t nt) {
     const int64_t G = 148;
-    return 64 + 2 * G * 16 + 2 * G * ell * 8 + 2 * G * 8 + nt * ell * 8 + 1024;
+    return std::max<int64_t>(64 + 2 * G * 16 + 2 * G * ell * 8 + 2 * G * 8 + nt * ell * 8 + 1024,
+                             sample_epoch_workspace(ell, nt, ell));
   }
 };
 
@@ -1213,6 +1220,8 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     set_error("sample_qrcp: workspace too small");
     return SQR_EINVAL;
   }
+  if (sample_epoch_eligible(ell, nt))
+    return sample_epoch(B, ldb, ell, nt, bb, Bf, ldbf, lperm, moves, taus, first, st, ws, ws_bytes, s);
   const int sms = sm_count();
   static const bool no_reg = env_flag("SQR_NO_REGSAMPLE");
   if (!no_reg && ell <= 144 && nt <= (int64_t)std::min(sms, 148) * kRT) {
