@@ -739,6 +739,20 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
 
 }  // namespace
 
+// Fixed-order split-K reduction shared with the TMA kernel (gemm_tma.cu).
+int splitk_reduce_launch(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
+                         const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, cudaStream_t s) {
+  const int64_t total = (int64_t)M * N;
+  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sm_count() * 8);
+  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn);
+  SQR_LAUNCH("splitk_reduce_kernel");
+  return SQR_OK;
+}
+
+int gemm_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* C, int64_t ldc,
+                double beta, const double* E, int64_t lde, double* D, int64_t ldd, double* ws, int64_t ws_bytes,
+                cudaStream_t s, GemmDyn dyn);
+
 int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
             const double* C, int64_t ldc, double beta, const double* E, int64_t lde, double* D,
             int64_t ldd, double* ws, int64_t ws_bytes, cudaStream_t s, GemmDyn dyn) {
@@ -749,6 +763,10 @@ int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int6
   }
   if (beta != 0.0 && E == nullptr) E = D;
   const int m = (int)M, n = (int)N, k = (int)K;
+  {
+    const int rc = gemm_tn_tma(m, n, k, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, s, dyn);
+    if (rc != -1) return rc;
+  }
 #define SQR_TN(MT)                                                                                  \
   if (M <= MT)                                                                                      \
     return dispatch_tn_vec<MT>(m, n, k, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
@@ -757,11 +775,19 @@ int gemm_tn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int6
   return SQR_EINVAL;
 }
 
+int gemm_nn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                double beta, const double* E, int64_t lde, double* D, int64_t ldd, cudaStream_t s, GemmDyn dyn);
+
 int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int64_t ldx,
             const double* Y, int64_t ldy, double beta, const double* E, int64_t lde, double* D,
             int64_t ldd, cudaStream_t s, GemmDyn dyn, double* ws, int64_t ws_bytes) {
   if (M <= 0 || N <= 0) return SQR_OK;
   if (beta != 0.0 && E == nullptr) E = D;
+  // TMA path unless launch_nn would split K (skinny long-K products with a workspace)
+  if (!(ws != nullptr && dyn.shift == nullptr && dyn.limit == nullptr && K >= 2048)) {
+    const int rc = gemm_nn_tma((int)M, (int)N, (int)K, alpha, X, ldx, Y, ldy, beta, E, lde, D, ldd, s, dyn);
+    if (rc != -1) return rc;
+  }
   const bool v2 = aligned16(X) && aligned16(Y) && (ldx % 2 == 0) && (ldy % 2 == 0) &&
                   (beta == 0.0 || (aligned16(E) && lde % 2 == 0));
   if (v2)

@@ -314,3 +314,33 @@ def test_gemm_nn_split_k(M, N, K, off):
     want = 0.5 * X[off:] @ Y[off:] - E
     assert relerr(outs[0].numpy(), want) <= 1e-13
     assert torch.equal(outs[0].view(), outs[1].view())
+
+
+# ------------------------------------------------- TMA vs cp.async GEMM paths
+@pytest.mark.parametrize("kind,M,N,K", [("tn", 128, 1000, 5000), ("tn", 64, 777, 333), ("tn", 100, 300, 70001),
+                                        ("nn", 1000, 1000, 256), ("nn", 4097, 300, 128), ("nn", 513, 129, 17)])
+def test_tma_gemm_bitwise_equals_cp_async(kind, M, N, K, monkeypatch):
+    """The TMA-staged warp-specialised GEMMs (csrc/gemm_tma.cu) accumulate in the
+    same k order as the cp.async kernels: bitwise equal results (SQR_NO_TMA is
+    read per call)."""
+    rng = np.random.default_rng(M + N + K)
+    E = upload(rng.standard_normal((M, N)), DEV)
+    w = ws(400 << 20)
+    if kind == "tn":
+        X, C = upload(rng.standard_normal((K, M)), DEV), upload(rng.standard_normal((K, N)), DEV)
+        call = lambda D: L.sqr_gemm_tn(M, N, K, 0.5, X.ptr, X.ld, C.ptr, C.ld, -2.0, E.ptr, E.ld, D.ptr, D.ld,
+                                       w.data_ptr(), w.numel(), stream_handle())
+    else:
+        X, Y = upload(rng.standard_normal((M, K)), DEV), upload(rng.standard_normal((K, N)), DEV)
+        call = lambda D: L.sqr_gemm_nn(M, N, K, 0.5, X.ptr, X.ld, Y.ptr, Y.ld, -2.0, E.ptr, E.ld, D.ptr, D.ld,
+                                       stream_handle())
+    out = []
+    for off in (None, "1"):
+        if off:
+            monkeypatch.setenv("SQR_NO_TMA", off)
+        else:
+            monkeypatch.delenv("SQR_NO_TMA", raising=False)
+        D = ColMajor.empty(M, N, DEV)
+        _lib.check(call(D))
+        out.append(D.numpy())
+    assert np.array_equal(out[0], out[1])

@@ -8,6 +8,7 @@ process) on the same inputs and is compared with the CPU oracle.
   SQR_EPOCH_SAMPLE       pivot-epoch sample QRCP (leader CTA over candidate columns)
   SQR_NO_CLUSTER_SAMPLE  grid-barrier sample QRCP for small samples
   SQR_NO_REGSAMPLE       shared-memory / L2 sample QRCP kernel
+  SQR_NO_TMA             cp.async-staged GEMMs instead of the TMA / mbarrier ones
   SQR_NO_BLOCKPANEL      32-wide leaf kernel + WY GEMMs for every panel
   SQR_NO_LEAF            (with SQR_NO_BLOCKPANEL) the generic sub-panel kernel
 """
@@ -47,7 +48,7 @@ print(json.dumps(out))
 CASES = {"wide": (300, 420, 300, 32, 1), "tall": (2000, 300, 300, 64, 2), "sq": (520, 520, 520, 16, 3)}
 VARIANTS = [{"SQR_NO_PAIRED_SWEEP": "1"}, {"SQR_NO_EARLY_PREP": "1"}, {"SQR_LOOKAHEAD": "1"},
             {"SQR_EPOCH_SAMPLE": "1"}, {"SQR_NO_CLUSTER_SAMPLE": "1"},
-            {"SQR_NO_REGSAMPLE": "1"}, {"SQR_NO_BLOCKPANEL": "1"},
+            {"SQR_NO_REGSAMPLE": "1"}, {"SQR_NO_TMA": "1"}, {"SQR_NO_BLOCKPANEL": "1"},
             {"SQR_NO_BLOCKPANEL": "1", "SQR_NO_LEAF": "1"}]
 
 
