@@ -411,6 +411,7 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
     }
 }
 
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static std::once_flag once;
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
