@@ -166,6 +166,21 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 extern unsigned long long* g_trace_host_ptr;
 
+// ------------------------------------------------------------ fp64 division
+// a / b correctly rounded from ry = RN(1/b) (Markstein: q = RN(a ry) is
+// within an ulp, the remainder a - b q is exact under fma, and one
+// correction q + (a - b q) ry rounds to RN(a / b)) for quotients in the
+// normal range -- the reflector tails a_r / (a_0 - beta) (|.| <= 1) and the
+// panel's s_c / y0.  Bitwise equal to a / b there, without the IEEE
+// division's per-quotient iteration and slow-path branch: one drcp per
+// reflector instead of one division per entry.
+__device__ __forceinline__ double div_rn(double a, double b, double ry) {
+  const double q = a * ry;
+  const double r = fma(-q, b, a);
+  return fma(r, ry, q);
+}
+
+
 // ---------------------------------------------------------------- reductions
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll

@@ -473,20 +473,21 @@ __global__ void __launch_bounds__(kLThreads, 1) leaf_kernel(PanelArgs a) {
       bhat = t;
       break;
     }
-    double beta = 0.0, tau = 0.0, y0 = 1.0;
+    double beta = 0.0, tau = 0.0, y0 = 1.0, ry = 1.0;
     if (nrm != 0.0) {
       beta = (at >= 0.0 ? -1.0 : 1.0) * nrm;
       y0 = at - beta;
+      ry = __drcp_rn(y0);
       tau = 2.0 / (1.0 + sa / (y0 * y0));
     }
-    if (tid >= 1 && tid < min(LW - t, w - t)) wv[tid] = tau * (rowv[tid] + vals[tid] / y0);
+    if (tid >= 1 && tid < min(LW - t, w - t)) wv[tid] = tau * (rowv[tid] + div_rn(vals[tid], y0, ry));
     if (g == 0 && tid == 0) a.taus[t] = tau;
     __syncthreads();
     // ---- apply reflector t to my rows (row t keeps beta and its R entries)
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
       if (rows[i] > t) {
-        const double yr = nrm != 0.0 ? x[i][t] / y0 : 0.0;
+        const double yr = nrm != 0.0 ? div_rn(x[i][t], y0, ry) : 0.0;
         x[i][t] = yr;
 #pragma unroll
         for (int v = 1; v < LW - t; ++v) x[i][t + v] = fma(-yr, wv[v], x[i][t + v]);

@@ -158,19 +158,21 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
         stopped = true;
         break;
       }
-      double beta = 0.0, tau = 0.0, y0 = 1.0;
+      double beta = 0.0, tau = 0.0, y0 = 1.0, ry = 1.0;
       if (nrm != 0.0) {
         beta = (at >= 0.0 ? -1.0 : 1.0) * nrm;
         y0 = at - beta;
+        ry = __drcp_rn(y0);
         tau = 2.0 / (1.0 + sa / (y0 * y0));
       }
-      if (tid < kLf) wv[tid] = (tid >= 1 && tid < L) ? tau * (rowv[tid] + vals[tid] / y0) : 0.0;
+      // a / y0 as div_rn (correctly rounded, bitwise equal to the IEEE quotient)
+      if (tid < kLf) wv[tid] = (tid >= 1 && tid < L) ? tau * (rowv[tid] + div_rn(vals[tid], y0, ry)) : 0.0;
       if (tid == 0) tau_s[t] = tau;
       if (g == 0 && tid == 0) a.taus[tc] = tau;
       __syncthreads();
       double yst;  // explicit Y entry of my row in column tc
       if (R > tc) {
-        const double yr = nrm != 0.0 ? x[0] / y0 : 0.0;
+        const double yr = nrm != 0.0 ? div_rn(x[0], y0, ry) : 0.0;
         x[0] = yr;
         yst = yr;
 #pragma unroll

@@ -228,17 +228,6 @@ __device__ __forceinline__ double warp_max_e(double v) {
 
 __device__ __forceinline__ int warp_isum(int v) { return __reduce_add_sync(0xffffffffu, v); }
 
-// a / b correctly rounded from ry = RN(1/b) (Markstein: q = RN(a ry) is
-// within an ulp, the remainder a - b q is exact under fma, and one
-// correction q + (a - b q) ry rounds to RN(a / b)); |a / b| <= 1 here, far
-// from overflow / underflow.  Bitwise equal to a / b, without the IEEE
-// division's per-quotient iteration and slow-path branch.
-__device__ __forceinline__ double div_rn(double a, double b, double ry) {
-  const double q = a * ry;
-  const double r = fma(-q, b, a);
-  return fma(r, ry, q);
-}
-
 __device__ __forceinline__ void st_release_word(unsigned* p, unsigned v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
 }

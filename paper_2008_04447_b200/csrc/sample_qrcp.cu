@@ -923,9 +923,11 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       s1 = warp_sum(s1);
       const double u0 = __shfl_sync(0xffffffffu, x[0], 0);
       nrm = sqrt(fma(u0, u0, s1));
+      double ry = 1.0;
       if (nrm != 0.0) {
         beta = (u0 >= 0.0 ? -1.0 : 1.0) * nrm;
         y0 = u0 - beta;
+        ry = __drcp_rn(y0);
         tau = 2.0 / (1.0 + s1 / (y0 * y0));
       }
       double* yf = ybuf(par);
@@ -933,7 +935,7 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
 #pragma unroll
       for (int i = 0; i < kMaxRowsPerLane; ++i) {
         const int r = lane + 32 * i;
-        if (r < len) yf[jn + r] = (r == 0) ? 1.0 : (nrm != 0.0 ? x[i] / y0 : 0.0);
+        if (r < len) yf[jn + r] = (r == 0) ? 1.0 : (nrm != 0.0 ? div_rn(x[i], y0, ry) : 0.0);
       }
     }
     if (lane == 0) {
