@@ -292,7 +292,8 @@ def run_ours(args):
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
-            traffic = json.load(open(tpath))[dom]["bytes_per_launch"]
+            tj = json.load(open(tpath))
+            traffic = (tj.get(dom + "_tma") or tj[dom])["bytes_per_launch"]  # TMA kernels since round 2
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf, "peak": PEAK_FP64_TFLOPS,
@@ -300,6 +301,12 @@ def run_ours(args):
                 "traffic": traffic, "peak_source": PEAK_SOURCE,
                 "launches_per_step": prof[dom][1] / args.steps,
                 "flops_per_step": fl[dom]}
+    # both sweep-GEMM classes (the dominant one above can switch between them)
+    roofline["classes"] = {
+        c: {"achieved": fl[c] / (prof[c][0] / args.steps / 1e3) / 1e12 if prof[c][0] > 0 else None,
+            "frac": (fl[c] / (prof[c][0] / args.steps / 1e3) / 1e12 / PEAK_FP64_TFLOPS) if prof[c][0] > 0 else None,
+            "ms_per_step": prof[c][0] / args.steps, "flops_per_step": fl[c]}
+        for c in ("gemm_tn", "gemm_nn")}
 
     # ---- end to end through the public API with pinned host buffers: a host
     # (NumPy) A in, R streamed back to a host array during the factorization
