@@ -237,38 +237,33 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
 // they drain after the last K-stage, so the epilogue reads E from shared
 // memory (no exposed global latency, no E registers: the 168-register
 // budget of two 5-warp CTAs per SM holds only the accumulators).
-constexpr int kNnTmaBM = 64;
 constexpr int kNnXBox = 8 * kTmaBK * 8;                          // 1 KB per {8 m, 16 k} box
-constexpr int kNnXBytes = (kNnTmaBM / 8) * kNnXBox;             // 8 KB
-constexpr int kNnEBoxN = 32;                                    // E box {64 m, 32 n} = 16 KB
-constexpr int kNnEBox = kNnTmaBM * kNnEBoxN * 8;
-// BN = 128: 2 CTAs / SM, 4 stages; BN = 64: 4 CTAs / SM, 3 stages (short K
-// needs the resident CTAs to hide each tile's fill and epilogue)
-template <int BN>
-struct NnTmaCfg {
-  static constexpr int NST = BN == 128 ? 4 : 3;
-  static constexpr int CTAS = BN == 128 ? 2 : 4;
-  static constexpr int YBYTES = BN * kTmaBK * 8;
-  static constexpr int STAGE = kNnXBytes + YBYTES;
-  static constexpr int EBOXES = BN / kNnEBoxN;
-  static constexpr int SMEM = STAGE * NST + 1024;
-  static_assert(EBOXES <= NST && kNnEBox <= STAGE, "E tile must fit the drained ring");
-};
-#ifndef SQR_NN_TMA_BN
-#define SQR_NN_TMA_BN 64
-#endif
+constexpr int kNnEBoxM = 64, kNnEBoxN = 32;                     // E box {64 m, 32 n} = 16 KB
+constexpr int kNnEBox = kNnEBoxM * kNnEBoxN * 8;
 #ifndef SQR_NN_TMA_GROUP
 #define SQR_NN_TMA_GROUP 16
 #endif
+// Tile BM x BN, consumer warps (BM / 32) x (BN / WTN) with warp tile 32 x WTN,
+// NST-deep ring, CTAS resident per SM.
+template <int BM, int BN, int WTN, int NST, int CTAS>
+struct NnTma {
+  static constexpr int CW = (BM / 32) * (BN / WTN);  // consumer warps
+  static constexpr int THREADS = (CW + 1) * 32;
+  static constexpr int XBYTES = (BM / 8) * kNnXBox;
+  static constexpr int YBYTES = BN * kTmaBK * 8;
+  static constexpr int STAGE = XBYTES + YBYTES;
+  static constexpr int EBOXES = (BM / kNnEBoxM) * (BN / kNnEBoxN);
+  static constexpr int SMEM = STAGE * NST + 1024;
+  static_assert(EBOXES <= NST && kNnEBox <= STAGE, "E tile must fit the drained ring");
+};
 
-template <int kNnTmaBN>
-__global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
+template <int BM, int BN, int WTN, int NST, int CTAS>
+__global__ void __launch_bounds__(NnTma<BM, BN, WTN, NST, CTAS>::THREADS, CTAS)
     gemm_nn_tma_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                        const __grid_constant__ CUtensorMap mapE, int M, int N, int K, double alpha, double beta,
                        double* D, int64_t ldd, GemmDyn dyn) {
-  using Cfg = NnTmaCfg<kNnTmaBN>;
-  constexpr int NST = Cfg::NST, NJ = kNnTmaBN / 16;
-  constexpr int kNnStage = Cfg::STAGE, kNnEBoxes = Cfg::EBOXES;
+  using Cfg = NnTma<BM, BN, WTN, NST, CTAS>;
+  constexpr int NJ = WTN / 8, CW = Cfg::CW, STAGE = Cfg::STAGE, EBOXES = Cfg::EBOXES;
   extern __shared__ uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[NST], empty[NST], ebar;
   if (dyn.stop && *dyn.stop) return;
@@ -291,7 +286,7 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
     mt = first + r % gsz;
     ntile = r / gsz;
   }
-  const int m0 = mt * kNnTmaBM, n0 = ntile * kNnTmaBN;
+  const int m0 = mt * BM, n0 = ntile * BN;
   if (n0 >= N) return;
   const int nk = K > 0 ? (int)cdiv(K, kTmaBK) : 0;
   const bool use_e = beta != 0.0;
@@ -300,43 +295,44 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(smem_u32(&full[s]), 1);
-      mbar_init(smem_u32(&empty[s]), kTmaConsumers);
+      mbar_init(smem_u32(&empty[s]), CW);
     }
     mbar_init(smem_u32(&ebar), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
-  if (warp == kTmaConsumers) {
+  if (warp == CW) {
     if (lane == 0) {
       const int yn = n0 + ((dyn.flags & kShiftB) ? sh : 0);
       for (int kt = 0; kt < nk; ++kt) {
         const int s = kt % NST;
         if (kt >= NST) mbar_wait(smem_u32(&empty[s]), ((kt / NST) & 1) ^ 1);
         const uint32_t fb = smem_u32(&full[s]);
-        mbar_expect_tx(fb, kNnStage);
-        const uint32_t dst = sbase + s * kNnStage;
+        mbar_expect_tx(fb, STAGE);
+        const uint32_t dst = sbase + s * STAGE;
         const int k = kt * kTmaBK;
 #pragma unroll
-        for (int q = 0; q < kNnTmaBM / 8; ++q) tma_load_2d(dst + q * kNnXBox, &mapX, m0 + 8 * q, k, fb);
-        tma_load_2d(dst + kNnXBytes, &mapY, k, yn, fb);
+        for (int q = 0; q < BM / 8; ++q) tma_load_2d(dst + q * kNnXBox, &mapX, m0 + 8 * q, k, fb);
+        tma_load_2d(dst + Cfg::XBYTES, &mapY, k, yn, fb);
       }
       if (use_e) {
-        // E box q goes to the q-th slot to drain after the last stage
+        // E box e = (m half, n quarter) goes to the e-th slot to drain after the last stage
         const uint32_t eb = smem_u32(&ebar);
-        mbar_expect_tx(eb, kNnEBoxes * kNnEBox);
+        mbar_expect_tx(eb, EBOXES * kNnEBox);
         const int en = n0 + ((dyn.flags & kShiftD) ? sh : 0);
-        for (int q = 0; q < kNnEBoxes; ++q) {
-          const int kt = nk + q;  // the ring iteration that would reuse the slot
+        for (int e = 0; e < EBOXES; ++e) {
+          const int kt = nk + e;
           const int s = kt % NST;
           if (kt >= NST) mbar_wait(smem_u32(&empty[s]), ((kt / NST) & 1) ^ 1);
-          tma_load_2d(sbase + s * kNnStage, &mapE, m0, en + q * kNnEBoxN, eb);
+          const int em = e % (BM / kNnEBoxM), enq = e / (BM / kNnEBoxM);
+          tma_load_2d(sbase + s * STAGE, &mapE, m0 + em * kNnEBoxM, en + enq * kNnEBoxN, eb);
         }
       }
     }
     return;
   }
   const int g = lane >> 2, t = lane & 3;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * (kNnTmaBN / 2);
+  const int wm = (warp % (BM / 32)) * 32, wn = (warp / (BM / 32)) * WTN;
   double acc[2][NJ][4];
 #pragma unroll
   for (int a = 0; a < 2; ++a)
@@ -358,7 +354,7 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
   for (int kt = 0; kt < nk; ++kt) {
     const int s = kt % NST;
     mbar_wait(smem_u32(&full[s]), (kt / NST) & 1);
-    const uint32_t sx = sbase + s * kNnStage, sy = sx + kNnXBytes;
+    const uint32_t sx = sbase + s * STAGE, sy = sx + Cfg::XBYTES;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       double a[2][2], b[NJ];
@@ -381,8 +377,8 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
     __syncwarp();
     if (lane == 0) mbar_arrive(smem_u32(&empty[s]));
   }
-  // epilogue: D = alpha acc + beta E, E from the drained ring (box q in slot
-  // (nk + q) % NST: column n of the tile at (n % 32) * 512 + m * 8)
+  // epilogue: D = alpha acc + beta E, E from the drained ring (box (ml / 64,
+  // nl / 32) in slot (nk + box) % NST, element at (nl % 32) * 512 + (ml % 64) * 8)
   if (use_e) mbar_wait(smem_u32(&ebar), 0);
 #pragma unroll
   for (int mi = 0; mi < 2; ++mi)
@@ -400,8 +396,9 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
           if (n >= N) continue;
           double v = alpha * acc[mi][nj][h * 2 + e];
           if (use_e) {
-            const int q = nl / kNnEBoxN;
-            const uint32_t ea = sbase + ((nk + q) % NST) * kNnStage + (uint32_t)((nl % kNnEBoxN) * kNnTmaBM + ml) * 8u;
+            const int box = (ml / kNnEBoxM) + (BM / kNnEBoxM) * (nl / kNnEBoxN);
+            const uint32_t ea = sbase + ((nk + box) % NST) * STAGE +
+                                (uint32_t)((nl % kNnEBoxN) * kNnEBoxM + ml % kNnEBoxM) * 8u;
             double ev;
             asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(ev) : "r"(ea));
             v = fma(beta, ev, v);
@@ -410,7 +407,6 @@ __global__ void __launch_bounds__(kTmaThreads, NnTmaCfg<kNnTmaBN>::CTAS)
         }
     }
 }
-
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static std::once_flag once;
@@ -522,27 +518,44 @@ int gemm_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx,
 }
 
 
+template <int BM, int BN, int WTN, int NST, int CTAS>
+int launch_nn_tma(const CUtensorMap& mX, const CUtensorMap& mY, const CUtensorMap& mE, int M, int N, int K,
+                  double alpha, double beta, double* D, int64_t ldd, cudaStream_t s, GemmDyn dyn) {
+  using Cfg = NnTma<BM, BN, WTN, NST, CTAS>;
+  auto kern = gemm_nn_tma_kernel<BM, BN, WTN, NST, CTAS>;
+  if (int rc = smem_optin((const void*)kern, Cfg::SMEM)) return rc;
+  dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN));
+  ProfScope ps(kTagGemmNn, s);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, dyn);
+  SQR_LAUNCH("gemm_nn_tma_kernel");
+  return SQR_OK;
+}
+
+#ifndef SQR_NN_TMA_CFG
+#define SQR_NN_TMA_CFG 0
+#endif
+
 int gemm_nn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                 double beta, const double* E, int64_t lde, double* D, int64_t ldd, cudaStream_t s, GemmDyn dyn) {
   if (env_flag("SQR_NO_TMA") || K < 1 || M < 1 || N < 1) return -1;
   if (!al16(X) || (ldx & 1) || !al16(Y) || (ldy & 1)) return -1;
   if (beta != 0.0 && (!al16(E) || (lde & 1))) return -1;
+  // config: 0 = 64 x 64 (4 warps, 3 stages, 4 CTAs/SM); 1 = 128 x 64 (8 warps, 4 stages, 2 CTAs/SM);
+  //         2 = 64 x 128 (8 warps, 4 stages, 2 CTAs/SM)
+  const int cfg = SQR_NN_TMA_CFG;
+  const int bm = cfg == 1 ? 128 : 64, bn = cfg == 2 ? 128 : 64;
   CUtensorMap mX, mY, mE;
   if (!make_map(&mX, X, M, K, ldx, kTmaBK, 8, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
-  if (!make_map(&mY, Y, K, N, ldy, SQR_NN_TMA_BN)) return -1;
+  if (!make_map(&mY, Y, K, N, ldy, bn)) return -1;
   if (beta != 0.0) {
-    if (!make_map(&mE, E, M, N, lde, kNnEBoxN, kNnTmaBM, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
+    if (!make_map(&mE, E, M, N, lde, kNnEBoxN, kNnEBoxM, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
   } else {
     mE = mX;  // never read
   }
-  constexpr int BN = SQR_NN_TMA_BN;
-  using Cfg = NnTmaCfg<BN>;
-  if (int rc = smem_optin((const void*)gemm_nn_tma_kernel<BN>, Cfg::SMEM)) return rc;
-  dim3 grid((unsigned)cdiv(M, kNnTmaBM), (unsigned)cdiv(N, BN));
-  ProfScope ps(kTagGemmNn, s);
-  gemm_nn_tma_kernel<BN><<<grid, kTmaThreads, Cfg::SMEM, s>>>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, dyn);
-  SQR_LAUNCH("gemm_nn_tma_kernel");
-  return SQR_OK;
+  (void)bm;
+  if (cfg == 1) return launch_nn_tma<128, 64, 32, 4, 2>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn);
+  if (cfg == 2) return launch_nn_tma<64, 128, 32, 4, 2>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn);
+  return launch_nn_tma<64, 64, 32, 3, 4>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn);
 }
 
 }  // namespace sqr

@@ -908,6 +908,9 @@ def bench_main(args, bench):
     import os
     import time
 
+    if "RANK" not in os.environ:  # --force-distributed without torchrun: a world of one
+        os.environ.update({"RANK": "0", "LOCAL_RANK": "0", "WORLD_SIZE": "1", "MASTER_ADDR": "127.0.0.1",
+                           "MASTER_PORT": os.environ.get("MASTER_PORT", "29531")})
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
