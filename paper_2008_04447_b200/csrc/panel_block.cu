@@ -97,6 +97,8 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
       const int par = step & 1;
       ++step;
       const int L = wl - t;  // live values this step: |a|^2 and L-1 dots
+      const bool ck = a.trace != nullptr && g == 0 && tid == 0 && tc < 100;
+      long long ck0 = ck ? clock64() : 0;
       double q[kLf];
       {
         const double av = R > tc ? x[0] : 0.0;
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
           q[i] = keep + __shfl_xor_sync(0xffffffffu, send, k);
         }
       }
+      long long ck1 = ck ? clock64() + (long long)(q[0] * 0.0) : 0;
       red[warp][lane] = q[0];
       __syncthreads();
       if (tid < L) {
@@ -126,9 +129,11 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
         for (int v = 0; v < kLf; ++v)
           if (v < L) a.rowt[par * (kLf + 1) + v] = x[v];
       }
+      long long ck2 = ck ? clock64() : 0;
       if (tc < 40) SQR_TRACE(a.trace, 8 * tc + 1);
       gb.sync();
       if (tc < 40) SQR_TRACE(a.trace, 8 * tc + 2);
+      long long ck3 = ck ? clock64() : 0;
       {
         if (tid < L) rowv[tid] = __ldcg(a.rowt + par * (kLf + 1) + tid);
         const int v = tid >> 3, qd = tid & 7;
@@ -151,6 +156,7 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
         }
       }
       __syncthreads();
+      long long ck4 = ck ? clock64() : 0;
       const double at = rowv[0], sa = vals[0];
       const double nrm = sqrt(fma(at, at, sa));
       if (nrm == 0.0 && a.stop_at_zero) {
@@ -170,6 +176,7 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
       if (tid == 0) tau_s[t] = tau;
       if (g == 0 && tid == 0) a.taus[tc] = tau;
       __syncthreads();
+      long long ck5 = ck ? clock64() : 0;
       double yst;  // explicit Y entry of my row in column tc
       if (R > tc) {
         const double yr = nrm != 0.0 ? div_rn(x[0], y0, ry) : 0.0;
@@ -190,6 +197,15 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
 #pragma unroll
       for (int v = 0; v < kLf - 1; ++v) x[v] = x[v + 1];
       x[kLf - 1] = 0.0;
+      if (ck) {
+        long long* c = reinterpret_cast<long long*>(a.trace) + 1200 + 8 * tc;
+        c[0] = ck1 - ck0;
+        c[1] = ck2 - ck1;
+        c[2] = ck3 - ck2;
+        c[3] = ck4 - ck3;
+        c[4] = ck5 - ck4;
+        c[5] = clock64() - ck5 + (long long)(x[0] * 0.0);
+      }
     }
     if (live) {
       for (int c = 0; c < t; ++c) {
