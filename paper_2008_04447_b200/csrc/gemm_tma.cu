@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <mutex>
 
 #include "common.cuh"
@@ -73,6 +74,19 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t a, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* map, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];\n" ::"l"(reinterpret_cast<uint64_t>(map)),
+               "r"(c0), "r"(c1)
+               : "memory");
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t mbar) {
   asm volatile(
@@ -243,6 +257,10 @@ constexpr int kNnEBox = kNnEBoxM * kNnEBoxN * 8;
 #ifndef SQR_NN_TMA_GROUP
 #define SQR_NN_TMA_GROUP 16
 #endif
+#ifndef SQR_NN_E_PREFETCH
+#define SQR_NN_E_PREFETCH 1
+#endif
+constexpr bool kNnEPrefetch = SQR_NN_E_PREFETCH != 0;
 // Tile BM x BN, consumer warps (BM / 32) x (BN / WTN) with warp tile 32 x WTN,
 // NST-deep ring, CTAS resident per SM.
 template <int BM, int BN, int WTN, int NST, int CTAS>
@@ -261,7 +279,7 @@ template <int BM, int BN, int WTN, int NST, int CTAS>
 __global__ void __launch_bounds__(NnTma<BM, BN, WTN, NST, CTAS>::THREADS, CTAS)
     gemm_nn_tma_kernel(const __grid_constant__ CUtensorMap mapX, const __grid_constant__ CUtensorMap mapY,
                        const __grid_constant__ CUtensorMap mapE, int M, int N, int K, double alpha, double beta,
-                       double* D, int64_t ldd, GemmDyn dyn) {
+                       double* D, int64_t ldd, GemmDyn dyn, int x3d) {
   using Cfg = NnTma<BM, BN, WTN, NST, CTAS>;
   constexpr int NJ = WTN / 8, CW = Cfg::CW, STAGE = Cfg::STAGE, EBOXES = Cfg::EBOXES;
   extern __shared__ uint8_t smem_raw[];
@@ -304,6 +322,13 @@ __global__ void __launch_bounds__(NnTma<BM, BN, WTN, NST, CTAS>::THREADS, CTAS)
   if (warp == CW) {
     if (lane == 0) {
       const int yn = n0 + ((dyn.flags & kShiftB) ? sh : 0);
+      if (use_e && kNnEPrefetch) {
+        // the beta E tile is read after the last stage: start pulling it from
+        // HBM into L2 now, so its epilogue TMA is an L2 hit
+        const int en = n0 + ((dyn.flags & kShiftD) ? sh : 0);
+        for (int e = 0; e < EBOXES; ++e)
+          tma_prefetch_2d(&mapE, m0 + (e % (BM / kNnEBoxM)) * kNnEBoxM, en + (e / (BM / kNnEBoxM)) * kNnEBoxN);
+      }
       for (int kt = 0; kt < nk; ++kt) {
         const int s = kt % NST;
         if (kt >= NST) mbar_wait(smem_u32(&empty[s]), ((kt / NST) & 1) ^ 1);
@@ -311,8 +336,13 @@ __global__ void __launch_bounds__(NnTma<BM, BN, WTN, NST, CTAS>::THREADS, CTAS)
         mbar_expect_tx(fb, STAGE);
         const uint32_t dst = sbase + s * STAGE;
         const int k = kt * kTmaBK;
+        if (x3d) {
+          // one 3-D box {8 m, 16 k, BM / 8 groups} lands as the BM / 8 boxes of the 2-D path
+          tma_load_3d(dst, &mapX, 0, k, m0 / 8, fb);
+        } else {
 #pragma unroll
-        for (int q = 0; q < BM / 8; ++q) tma_load_2d(dst + q * kNnXBox, &mapX, m0 + 8 * q, k, fb);
+          for (int q = 0; q < BM / 8; ++q) tma_load_2d(dst + q * kNnXBox, &mapX, m0 + 8 * q, k, fb);
+        }
         tma_load_2d(dst + Cfg::XBYTES, &mapY, k, yn, fb);
       }
       if (use_e) {
@@ -520,13 +550,13 @@ int gemm_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx,
 
 template <int BM, int BN, int WTN, int NST, int CTAS>
 int launch_nn_tma(const CUtensorMap& mX, const CUtensorMap& mY, const CUtensorMap& mE, int M, int N, int K,
-                  double alpha, double beta, double* D, int64_t ldd, cudaStream_t s, GemmDyn dyn) {
+                  double alpha, double beta, double* D, int64_t ldd, cudaStream_t s, GemmDyn dyn, int x3d) {
   using Cfg = NnTma<BM, BN, WTN, NST, CTAS>;
   auto kern = gemm_nn_tma_kernel<BM, BN, WTN, NST, CTAS>;
   if (int rc = smem_optin((const void*)kern, Cfg::SMEM)) return rc;
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN));
   ProfScope ps(kTagGemmNn, s);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, dyn);
+  kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, dyn, x3d);
   SQR_LAUNCH("gemm_nn_tma_kernel");
   return SQR_OK;
 }
@@ -545,17 +575,31 @@ int gemm_nn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx,
   const int cfg = SQR_NN_TMA_CFG;
   const int bm = cfg == 1 ? 128 : 64, bn = cfg == 2 ? 128 : 64;
   CUtensorMap mX, mY, mE;
-  if (!make_map(&mX, X, M, K, ldx, kTmaBK, 8, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
+  // X: M % 8 == 0 -> one 3-D map {8 m, k, m / 8} (strides ldx, 64 bytes) loaded with one TMA per stage;
+  // otherwise 2-D boxes {8 m, 16 k}
+  int x3d = (M % 8 == 0 && !env_flag("SQR_NN_X2D")) ? 1 : 0;
+  if (x3d) {
+    auto fn = encode_fn();
+    cuuint64_t dims[3] = {8, (cuuint64_t)K, (cuuint64_t)(M / 8)};
+    cuuint64_t strides[2] = {(cuuint64_t)ldx * 8, 64};
+    cuuint32_t box[3] = {8, (cuuint32_t)kTmaBK, (cuuint32_t)(bm / 8)};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (!fn || fn(&mX, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(X), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      x3d = 0;
+  }
+  if (!x3d && !make_map(&mX, X, M, K, ldx, kTmaBK, 8, CU_TENSOR_MAP_SWIZZLE_64B)) return -1;
+  if (env_flag("SQR_TMA_DEBUG")) fprintf(stderr, "gemm_nn_tma M=%d N=%d K=%d x3d=%d\n", M, N, K, x3d);
   if (!make_map(&mY, Y, K, N, ldy, bn)) return -1;
   if (beta != 0.0) {
     if (!make_map(&mE, E, M, N, lde, kNnEBoxN, kNnEBoxM, CU_TENSOR_MAP_SWIZZLE_NONE)) return -1;
   } else {
     mE = mX;  // never read
   }
-  (void)bm;
-  if (cfg == 1) return launch_nn_tma<128, 64, 32, 4, 2>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn);
-  if (cfg == 2) return launch_nn_tma<64, 128, 32, 4, 2>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn);
-  return launch_nn_tma<64, 64, 32, 3, 4>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn);
+    if (cfg == 1) return launch_nn_tma<128, 64, 32, 4, 2>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn, x3d);
+  if (cfg == 2) return launch_nn_tma<64, 128, 32, 4, 2>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn, x3d);
+  return launch_nn_tma<64, 64, 32, 3, 4>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, s, dyn, x3d);
 }
 
 }  // namespace sqr

@@ -97,7 +97,11 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
       const int par = step & 1;
       ++step;
       const int L = wl - t;  // live values this step: |a|^2 and L-1 dots
+#ifdef SQR_PANEL_CK  // per-column cycle probe (tools/panel_cycles.py; build with -DSQR_PANEL_CK)
       const bool ck = a.trace != nullptr && g == 0 && tid == 0 && tc < 100;
+#else
+      constexpr bool ck = false;
+#endif
       long long ck0 = ck ? clock64() : 0;
       double q[kLf];
       {

@@ -1,3 +1,8 @@
+"""Per-column cycle split of panel_block_kernel (CTA 0, thread 0) on a 32768 x 128
+panel.  Needs a build with the probe compiled in:
+    python -m paper_2008_04447_b200.build -DSQR_PANEL_CK --name=libsqr_ck.so
+    SQR_LIB=libsqr_ck.so python tools/panel_cycles.py
+"""
 import os, sys, numpy as np, torch
 sys.path.insert(0, "/root/repo")
 from paper_2008_04447_b200 import _lib
