@@ -539,7 +539,7 @@ int gemm_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ldx,
   if (dyn.npre > 0 && (dyn.npre % kTmaBN != 0 || !al16(dyn.pre) || (dyn.ldpre & 1))) return -1;
 #define SQR_TMA(MT) \
   if (M <= MT) return launch_tn_tma<MT>(M, N, K, alpha, X, ldx, C, ldc, beta, E, lde, D, ldd, ws, ws_bytes, dyn, s);
-  SQR_TMA(64) SQR_TMA(128)
+  SQR_TMA(16) SQR_TMA(32) SQR_TMA(48) SQR_TMA(64) SQR_TMA(80) SQR_TMA(96) SQR_TMA(112) SQR_TMA(128)
 #undef SQR_TMA
   // M in (128, 144] (the sketch, l = b + p rows) stays on the cp.async kernel:
   // measured 31.4 vs 32.1 TFLOP/s on the C5 sketch (the 144-row tile spills at
