@@ -344,3 +344,16 @@ def test_tma_gemm_bitwise_equals_cp_async(kind, M, N, K, monkeypatch):
         _lib.check(call(D))
         out.append(D.numpy())
     assert np.array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("M,N,K,beta", [(1000, 1000, 256, 1.0), (4096, 300, 128, -0.5), (513, 129, 17, 1.0),
+                                        (128, 5000, 128, 1.0)])
+def test_gemm_nn_unit_alpha(M, N, K, beta):
+    """alpha = 1, the trailing updates' form C + beta... (E in place of D)."""
+    rng = np.random.default_rng(M * 7 + N + K)
+    X, Y, E = rng.standard_normal((M, K)), rng.standard_normal((K, N)), rng.standard_normal((M, N))
+    Xd, Yd, Ed = upload(X, DEV), upload(Y, DEV), upload(E, DEV)
+    _lib.check(L.sqr_gemm_nn(M, N, K, 1.0, Xd.ptr, Xd.ld, Yd.ptr, Yd.ld, beta, Ed.ptr, Ed.ld, Ed.ptr, Ed.ld,
+                             stream_handle()))
+    want = X @ Y + beta * E
+    assert relerr(Ed.numpy(), want) <= 1e-13

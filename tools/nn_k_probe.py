@@ -20,7 +20,8 @@ for K in [int(x) for x in (sys.argv[1:] or ["128", "256", "384", "512"])]:
     W = torch.randn((n, K), dtype=torch.float64, device=dev, generator=g) * 1e-3
 
     def run():
-        _lib.check(L.sqr_gemm_nn(m, n, K, 1.0, Y.data_ptr(), m, W.data_ptr(), K, 1.0, C.data_ptr(), m,
+        beta = float(os.environ.get("NN_BETA", "1"))
+        _lib.check(L.sqr_gemm_nn(m, n, K, 1.0, Y.data_ptr(), m, W.data_ptr(), K, beta, C.data_ptr(), m,
                                  C.data_ptr(), m, s))
     run()
     torch.cuda.synchronize()
