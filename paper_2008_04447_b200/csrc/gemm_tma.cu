@@ -28,6 +28,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -410,32 +411,40 @@ __global__ void __launch_bounds__(NnTma<BM, BN, WTN, NST, CTAS>::THREADS, CTAS)
   // epilogue: D = alpha acc + beta E, E from the drained ring (box (ml / 64,
   // nl / 32) in slot (nk + box) % NST, element at (nl % 32) * 512 + (ml % 64) * 8)
   if (use_e) mbar_wait(smem_u32(&ebar), 0);
+  // alpha == 1 (the trailing updates) skips the multiply: epilogue fp64 ops
+  // issue on the same pipe as the DMMAs of the SM's other CTAs
+  auto epilogue = [&](auto unit) {
 #pragma unroll
-  for (int mi = 0; mi < 2; ++mi)
+    for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int ml = wm + mi * 16 + g + h * 8;
-      const int m = m0 + ml;
-      if (m >= M) continue;
+      for (int h = 0; h < 2; ++h) {
+        const int ml = wm + mi * 16 + g + h * 8;
+        const int m = m0 + ml;
+        if (m >= M) continue;
 #pragma unroll
-      for (int nj = 0; nj < NJ; ++nj)
+        for (int nj = 0; nj < NJ; ++nj)
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int nl = wn + nj * 8 + 2 * t + e;
-          const int n = n0 + nl;
-          if (n >= N) continue;
-          double v = alpha * acc[mi][nj][h * 2 + e];
-          if (use_e) {
-            const int box = (ml / kNnEBoxM) + (BM / kNnEBoxM) * (nl / kNnEBoxN);
-            const uint32_t ea = sbase + ((nk + box) % NST) * STAGE +
-                                (uint32_t)((nl % kNnEBoxN) * kNnEBoxM + ml % kNnEBoxM) * 8u;
-            double ev;
-            asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(ev) : "r"(ea));
-            v = fma(beta, ev, v);
+          for (int e = 0; e < 2; ++e) {
+            const int nl = wn + nj * 8 + 2 * t + e;
+            const int n = n0 + nl;
+            if (n >= N) continue;
+            double v = decltype(unit)::value ? acc[mi][nj][h * 2 + e] : alpha * acc[mi][nj][h * 2 + e];
+            if (use_e) {
+              const int box = (ml / kNnEBoxM) + (BM / kNnEBoxM) * (nl / kNnEBoxN);
+              const uint32_t ea = sbase + ((nk + box) % NST) * STAGE +
+                                  (uint32_t)((nl % kNnEBoxN) * kNnEBoxM + ml % kNnEBoxM) * 8u;
+              double ev;
+              asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(ev) : "r"(ea));
+              v = fma(beta, ev, v);
+            }
+            D[(int64_t)n * ldd + m] = v;
           }
-          D[(int64_t)n * ldd + m] = v;
-        }
-    }
+      }
+  };
+  if (alpha == 1.0)
+    epilogue(std::true_type{});
+  else
+    epilogue(std::false_type{});
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
