@@ -24,6 +24,7 @@ NCCL) and, in the CPU test-suite, on gloo with a NumPy reference backend.
 from __future__ import annotations
 
 import functools
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -260,6 +261,23 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
     # the speculative work past that point is discarded, and the panel columns
     # left of a short panel's stop get the block update they miss.
     pend = None
+    # Paired second sweep (as driver.cu's trailing_first / trailing_second,
+    # randomized.py:203-210): with storage rows [m, m + 2b) per column (the
+    # stacked W_P | W_J rows move with the column moves), block P = J - 1 of a
+    # pair applies only its R12 rows and defers the rest of its update; J's
+    # panel columns take P's update just before J's panel, J's first sweep is
+    # corrected by (Y_J^T Y_P) W_P, and one K = 2b update applies both.
+    pair_ok = (hasattr(ops, "block_update_defer") and A_local.shape[1] >= m + 2 * b
+               and not os.environ.get("SQR_DIST_NO_PAIR"))
+    pendP = None  # (i0, bb, pan, t0) of the block whose rows >= i0 + b still lack its update
+
+    def flush():
+        """Any exit while a block's update is deferred: apply the rest of it
+        (the reference applied each block's full update before its next step)."""
+        nonlocal pendP
+        if pendP is not None:
+            ops.flush_pending(A_local, pendP[3], pendP[0], m, pendP[2])
+            pendP = None
 
     def settle(pd, tail, may_continue):
         """Apply the reference's exits for the pending block; True = stop."""
@@ -295,9 +313,11 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
             stop = settle(pend, samp.prev_tail, True)
             pend = None
             if stop:
+                flush()
                 break
         if samp.stop:
             reason = samp.reason
+            flush()
             break
         # ---- column moves (positions relative to i0)
         moves = samp.moves
@@ -310,13 +330,23 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         J = i0 // b
         owner = J % comm.size
         lc = int(lay.local_index(i0)) if owner == r else -1
+        if pendP is not None and owner == r:  # J's panel columns get the deferred P first
+            ops.pending_panel(A_local, lc, i0, m, samp.achieved, pendP)
         pan = ops.panel(A_local, lc, i0, m, samp.achieved, bb, owner == r)
         pan = ops.broadcast_panel(pan, owner, comm, m - i0, bb)
         if hasattr(ops, "prep_sample_update"):  # overlaps the trailing update
             ops.prep_sample_update(samp, pan, bb)
         # ---- trailing update of my columns at global positions >= i0 + bb
         t0 = lay.first_local_at_or_after(r, i0 + bb)
-        ops.block_update(A_local, t0, i0, m, pan)
+        last = i0 + bb >= k or n - (i0 + bb) == 0
+        if pendP is not None:
+            ops.block_update_merge(A_local, t0, i0, m, pan, pendP)
+            pendP = None
+        elif pair_ok and not last and bb == b and i0 + 2 * b <= k:
+            ops.block_update_defer(A_local, t0, i0, m, pan)
+            pendP = (i0, bb, pan, t0)
+        else:
+            ops.block_update(A_local, t0, i0, m, pan)
         nblocks += 1
         achieved = i0 + bb
         pend = (i0, bb, pan, lc)
@@ -333,6 +363,7 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         B = _gather_sample(ops, comm, Bn_loc, lay, achieved, ell)
     if pend is not None:
         settle(pend, ops.read_tail(pend[2]), False)
+    flush()
     counters = rqrcp_counters(m, n, b, ell, achieved, nblocks,
                               {"k_reached": 1, "short_block": 5, "no_trailing": 6}.get(reason, 0), False)
     return DistResult(achieved, nblocks, reason, perm, A_local, taus[:achieved], counters)
@@ -514,7 +545,8 @@ class GpuOps:
         self.staus = torch.zeros(b, **f64)
         # panel broadcast record: [Y (b x m) | taus (b) | R11 (b x b) | status (9 doubles)]
         if self.symm is None:
-            self.pbuf = torch.zeros(prec, **f64)
+            self.pbufs = [torch.zeros(prec, **f64) for _ in range(2)]
+            self.pbuf = self.pbufs[0]
         self.T = torch.zeros((b, b), **f64)
         nmax = lay.n_local_max()
         self.slab = torch.zeros((max(nmax, 1), ell), **f64)
@@ -588,8 +620,8 @@ class GpuOps:
         return self.Bglob[p0:]
 
     def _select_panel_buffer(self, i0):
-        if self.symm is not None:
-            self.pbuf = self.pbufs[(i0 // self.b) & 1]
+        # by block parity: a deferred block P's record (Y_P) must survive J's panel
+        self.pbuf = self.pbufs[(i0 // self.b) & 1]
 
     def assemble_next(self, parts, lay, achieved, ell):
         return self._assemble(parts, lay, ell, achieved)
@@ -748,6 +780,85 @@ class GpuOps:
                                                 ws.data_ptr(), ws.numel(), self._s()), "block_update")
         pan.T = T
 
+    # 5b. paired second sweep (storage rows [m, m + b) = W_P, [m + b, m + 2b) = W_J)
+    def _build_t(self, Y, mr, bb, taus):
+        T = torch.empty((bb, bb), dtype=torch.float64, device=self.dev)
+        ws = self._ws(200 << 20)
+        self._chk(self.L.sqr_build_t(Y.data_ptr(), mr, mr, bb, taus.data_ptr(), T.data_ptr(), bb, ws.data_ptr(),
+                                     ws.numel(), self._s()), "build_t")
+        return T
+
+    def _scratch(self, name, numel):
+        buf = getattr(self, name, None)
+        if buf is None or buf.numel() < numel:
+            buf = torch.empty(max(numel, 1), dtype=torch.float64, device=self.dev)
+            setattr(self, name, buf)
+        return buf
+
+    def block_update_defer(self, A, t0, i0, m, pan):
+        """Block P of a pair: W_P = -T^T Y^T C into the W_P rows, and only the R12
+        rows C[i0:i0+b] += Y[:b] W_P (the sample update needs them)."""
+        ld = A.shape[1]
+        bb, mr = pan.Y.shape[0], m - i0
+        ncols = A.shape[0] - t0
+        T = self._build_t(pan.Y, mr, bb, pan.taus)
+        pan.T = T
+        if ncols <= 0:
+            return
+        base = A.data_ptr() + 8 * t0 * ld
+        C, Wp = base + 8 * i0, base + 8 * m
+        Wt = self._scratch("_wt", bb * ncols)
+        self._gemm_tn(bb, ncols, mr, 1.0, pan.Y.data_ptr(), mr, C, ld, Wt.data_ptr(), bb)
+        self._gemm_tn(bb, ncols, bb, -1.0, T.data_ptr(), bb, Wt.data_ptr(), bb, Wp, ld)
+        self._gemm_nn(bb, ncols, bb, 1.0, pan.Y.data_ptr(), mr, Wp, ld, 1.0, C, ld, C, ld)
+
+    def pending_panel(self, A, lc, i0, m, w, pendP):
+        """J's panel columns (owner) take the deferred P on rows >= i0, then
+        their W_P is retired (a short panel never sees P twice)."""
+        pi0, b, ppan, _ = pendP
+        ld, mrP = A.shape[1], m - pi0
+        if w <= 0:
+            return
+        col = A.data_ptr() + 8 * lc * ld
+        self._gemm_nn(m - i0, w, b, 1.0, ppan.Y.data_ptr() + 8 * (i0 - pi0), mrP, col + 8 * m, ld, 1.0,
+                      col + 8 * i0, ld, col + 8 * i0, ld)
+        A[lc:lc + w, m:m + b].zero_()
+
+    def block_update_merge(self, A, t0, i0, m, pan, pendP):
+        """Block J of a pair: [Y_J^T C] + (Y_J^T Y_P) W_P (C still lacks P),
+        W_J = -T_J^T (.), then C += [Y_P | Y_J] [W_P ; W_J] with K = b + bb."""
+        pi0, b, ppan, _ = pendP
+        ld = A.shape[1]
+        bb, mr, mrP = pan.Y.shape[0], m - i0, m - pi0
+        ncols = A.shape[0] - t0
+        T = self._build_t(pan.Y, mr, bb, pan.taus)
+        pan.T = T
+        if ncols <= 0:
+            return
+        base = A.data_ptr() + 8 * t0 * ld
+        C, Wp, Wj = base + 8 * i0, base + 8 * m, base + 8 * (m + b)
+        Ypj = ppan.Y.data_ptr() + 8 * (i0 - pi0)          # Y_P rows from i0, ld mrP
+        Wt = self._scratch("_wt", bb * ncols)
+        X = self._scratch("_yjyp", bb * b)
+        self._gemm_tn(bb, ncols, mr, 1.0, pan.Y.data_ptr(), mr, C, ld, Wt.data_ptr(), bb)
+        self._gemm_tn(bb, b, mr, 1.0, pan.Y.data_ptr(), mr, Ypj, mrP, X.data_ptr(), bb)
+        self._gemm_nn(bb, ncols, b, 1.0, X.data_ptr(), bb, Wp, ld, 1.0, Wt.data_ptr(), bb, Wt.data_ptr(), bb)
+        self._gemm_tn(bb, ncols, bb, -1.0, T.data_ptr(), bb, Wt.data_ptr(), bb, Wj, ld)
+        Ycat = self._scratch("_ycat", (b + bb) * mr)[:(b + bb) * mr].view(b + bb, mr)
+        Ycat[:b].copy_(ppan.Y[:, i0 - pi0:])
+        Ycat[b:].copy_(pan.Y)
+        self._gemm_nn(mr, ncols, b + bb, 1.0, Ycat.data_ptr(), mr, Wp, ld, 1.0, C, ld, C, ld)
+
+    def flush_pending(self, A, t0, i0, m, pan):
+        """The deferred rows >= i0 + b of a block whose pair partner never came."""
+        ld, b, mr = A.shape[1], pan.Y.shape[0], m - i0
+        ncols = A.shape[0] - t0
+        if ncols <= 0 or mr <= b:
+            return
+        base = A.data_ptr() + 8 * t0 * ld
+        self._gemm_nn(mr - b, ncols, b, 1.0, pan.Y.data_ptr() + 8 * b, mr, base + 8 * m, ld, 1.0,
+                      base + 8 * (i0 + b), ld, base + 8 * (i0 + b), ld)
+
     # TRQRCP (trqrcp_block_cyclic): replicated Yg, panel materialisation, local W^T / R rows
     def new_yg(self, m, k):
         return torch.zeros((max(k, 1), m), dtype=torch.float64, device=self.dev)   # m x k column-major
@@ -856,16 +967,18 @@ class GpuOps:
 
 
 # ----------------------------------------------------------------- bench
-def local_giid(m: int, n: int, b: int, seed: int, lay: BlockCyclic, r: int, device) -> torch.Tensor:
-    """This rank's columns of giid(m, n, seed) (column-major stream, rng.py:65-70)."""
+def local_giid(m: int, n: int, b: int, seed: int, lay: BlockCyclic, r: int, device, rows: int = 0) -> torch.Tensor:
+    """This rank's columns of giid(m, n, seed) (column-major stream, rng.py:65-70)
+    as (ncols, max(rows, m)) storage; rows beyond m are zero."""
     from . import _lib
     L = _lib.lib()
     nl = lay.n_local(r)
-    A = torch.empty((max(nl, 1), m), dtype=torch.float64, device=device)
+    ld = max(rows, m)
+    A = torch.zeros((max(nl, 1), ld), dtype=torch.float64, device=device)
     j = 0
     for c in lay.blocks_of(r):
         w = min(b, n - c * b)
-        L.sqr_gaussian(A.data_ptr() + 8 * j * m, m, m, w, seed, c * b * m, 0,
+        L.sqr_gaussian(A.data_ptr() + 8 * j * ld, ld, m, w, seed, c * b * m, 0,
                        torch.cuda.current_stream(device).cuda_stream)
         j += w
     return A
@@ -922,7 +1035,7 @@ def bench_main(args, bench):
     m = n = args.n
     b, p = args.b, args.p
     lay = BlockCyclic(n, b, comm.size)
-    A0 = local_giid(m, n, b, 5, lay, comm.rank, dev)
+    A0 = local_giid(m, n, b, 5, lay, comm.rank, dev, rows=m + 2 * b)  # + W rows (paired sweep)
     ops = GpuOps(dev, comm)
     tracer = None
     if os.environ.get("SQR_DIST_TRACE"):
@@ -1126,7 +1239,8 @@ def rqrcp(A, k: int, b: int = 32, p: int = 8, seed: int = 0, omega=None, group=N
     if k == 0 or ell >= m:   # empty / the deterministic l >= m fallback (randomized.py:172-174): replicated
         return F.rqrcp(A, k, b=b, p=p, seed=seed, omega=omega)
     lay = BlockCyclic(n, b, comm.size)
-    S, bad = _local_slab(A, lay.global_of_local(comm.rank), m, m, dev)
+    # rows [m, m + 2b): W_P | W_J of the paired second sweep (they move with the columns)
+    S, bad = _local_slab(A, lay.global_of_local(comm.rank), m, m + 2 * b, dev)
     _check_finite_all(bad, comm)
     res = rqrcp_block_cyclic(S, m, n, k, b, p, seed, comm, GpuOps(dev, comm), omega=_omega_arg(omega, ell, m, seed))
     W = _gather_columns(S, lay, comm, m, dev)

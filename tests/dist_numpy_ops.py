@@ -121,6 +121,50 @@ class NumpyOps:
             W = T.T @ (Y.T @ C)
             C -= Y @ W
 
+    # paired second sweep (storage rows [m, m + b) = W_P, [m + b, m + 2b) = W_J)
+    def block_update_defer(self, A, t0, i0, m, pan):
+        Y = pan.Y.numpy().T
+        T = O.t_factor(Y, pan.taus.numpy())
+        pan.T = T
+        M = self.mat(A)
+        C = M[i0:m, t0:]
+        if C.shape[1]:
+            bb = Y.shape[1]
+            W = -T.T @ (Y.T @ C)
+            M[m:m + bb, t0:] = W
+            C[:bb] += Y[:bb] @ W
+
+    def pending_panel(self, A, lc, i0, m, w, pendP):
+        pi0, b, ppan, _ = pendP
+        M = self.mat(A)
+        Yp = ppan.Y.numpy().T
+        M[i0:m, lc:lc + w] += Yp[i0 - pi0:] @ M[m:m + b, lc:lc + w]
+        M[m:m + b, lc:lc + w] = 0.0
+
+    def block_update_merge(self, A, t0, i0, m, pan, pendP):
+        pi0, b, ppan, _ = pendP
+        Yj = pan.Y.numpy().T
+        T = O.t_factor(Yj, pan.taus.numpy())
+        pan.T = T
+        M = self.mat(A)
+        C = M[i0:m, t0:]
+        if C.shape[1]:
+            bb = Yj.shape[1]
+            Yp = ppan.Y.numpy().T[i0 - pi0:]
+            Wp = M[m:m + b, t0:]
+            Wt = Yj.T @ C + (Yj.T @ Yp) @ Wp
+            Wj = -T.T @ Wt
+            M[m + b:m + b + bb, t0:] = Wj
+            C += np.hstack([Yp, Yj]) @ np.vstack([Wp, Wj])
+
+    def flush_pending(self, A, t0, i0, m, pan):
+        M = self.mat(A)
+        Yp = pan.Y.numpy().T
+        b = Yp.shape[1]
+        C = M[i0 + b:m, t0:]
+        if C.shape[1] and C.shape[0]:
+            C += Yp[b:] @ M[m:m + b, t0:]
+
     # TRQRCP (distributed.trqrcp_block_cyclic)
     def new_yg(self, m, k):
         return np.zeros((m, max(k, 1)), order="F")

@@ -31,18 +31,27 @@ def nccl1():
     dist.destroy_process_group()
 
 
+def _slab(A, m, rows, dev):
+    """(ncols, rows) storage, rows [m, rows) zero: rows >= m + 2b turn on the
+    paired second sweep (W_P | W_J rows)."""
+    S = torch.zeros((A.shape[1], rows), dtype=torch.float64)
+    S[:, :m] = torch.from_numpy(np.ascontiguousarray(A.T))
+    return S.to(dev)
+
+
+@pytest.mark.parametrize("paired", [False, True])
 @pytest.mark.parametrize("m,n,k,b,p", [(600, 500, 500, 32, 8), (2000, 700, 300, 64, 8), (300, 257, 257, 16, 4)])
-def test_block_cyclic_gpu_world1(nccl1, m, n, k, b, p):
+def test_block_cyclic_gpu_world1(nccl1, m, n, k, b, p, paired):
     dev = nccl1
     A = gauss(m, n, 3)
     om = O.gauss_matrix(b + p, m, 11)
     lay = BlockCyclic(n, b, 1)
-    A_loc = torch.from_numpy(np.ascontiguousarray(A.T)).to(dev)
+    A_loc = _slab(A, m, m + 2 * b if paired else m, dev)
     res = rqrcp_block_cyclic(A_loc, m, n, k, b, p, 11, TorchComm(), GpuOps(dev), omega=om)
     ref = O.rqrcp(A, k, b=b, p=p, seed=11)
     assert res.achieved == ref.achieved_rank
     assert np.array_equal(res.perm, ref.perm)
-    W = A_loc.cpu().numpy().T
+    W = A_loc[:, :m].cpu().numpy().T
     R = np.triu(W[:res.achieved, :])
     assert np.abs(R - ref.R).max() <= 1e-10 * np.abs(ref.R).max()
     assert [res.counters.trailing_passes, res.counters.blas3_volume] == \
@@ -51,8 +60,9 @@ def test_block_cyclic_gpu_world1(nccl1, m, n, k, b, p):
     assert np.array_equal(single.perm, res.perm)
 
 
+@pytest.mark.parametrize("paired", [False, True])
 @pytest.mark.parametrize("kind", ["short_panel", "lowrank"])
-def test_block_cyclic_gpu_lazy_exits(nccl1, kind):
+def test_block_cyclic_gpu_lazy_exits(nccl1, kind, paired):
     """Early exits settled lazily (the panel tail read with the next block's
     sample record): a short panel and a sample-floor stop behind a pending block."""
     dev = nccl1
@@ -63,13 +73,13 @@ def test_block_cyclic_gpu_lazy_exits(nccl1, kind):
     else:
         A = np.asfortranarray(gauss(m, 61, 5) @ gauss(61, n, 6))
     om = O.gauss_matrix(b + p, m, 13)
-    A_loc = torch.from_numpy(np.ascontiguousarray(A.T)).to(dev)
+    A_loc = _slab(A, m, m + 2 * b if paired else m, dev)
     res = rqrcp_block_cyclic(A_loc, m, n, n, b, p, 13, TorchComm(), GpuOps(dev), omega=om)
     ref = O.rqrcp(A, n, b=b, p=p, seed=13)
     assert res.achieved == ref.achieved_rank
     assert [res.counters.trailing_passes, res.counters.blas3_volume] == \
         [ref.counters.trailing_passes, ref.counters.blas3_volume]
-    W = A_loc.cpu().numpy().T
+    W = A_loc[:, :m].cpu().numpy().T
     R = np.triu(W[:res.achieved, :])
     d = np.nonzero(res.perm != ref.perm)[0]
     if d.size:  # documented near-tie: pivots among columns already at the noise floor
