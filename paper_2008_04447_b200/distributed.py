@@ -283,7 +283,7 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         """Apply the reference's exits for the pending block; True = stop."""
         nonlocal achieved, nblocks, reason
         pi0, pbb, pan, lc_owner = pd
-        bhat, taus_host, R11_host = tail
+        bhat, taus_host, r11_diag = tail
         if bhat == 0:  # randomized.py:197: no block, no update (ours used Y = 0: a no-op)
             achieved, nblocks, reason = pi0, nblocks - 1, "panel_zero"
             return True
@@ -296,7 +296,7 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
             return True
         if not may_continue:
             return True
-        d = np.abs(np.diag(R11_host))
+        d = np.abs(r11_diag)
         if not (d.size > 0 and d.min() > _DIAG_FLOOR * d[0]):
             reason = "r11_singular"
             return True
@@ -324,7 +324,7 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
         if len(moves):
             ps = i0 + moves[:, 1]
             pd = i0 + moves[:, 0]
-            ops.move_columns(A_local, ps, pd, lay, comm)
+            ops.move_columns(A_local, ps, pd, lay, comm, i0=i0, samp=samp)
             perm[pd] = perm[ps].copy()
         # ---- panel on the owner, broadcast of (Y, taus, bhat, R11)
         J = i0 // b
@@ -364,6 +364,8 @@ def rqrcp_block_cyclic(A_local, m: int, n: int, k: int, b: int, p: int, seed: in
     if pend is not None:
         settle(pend, ops.read_tail(pend[2]), False)
     flush()
+    if hasattr(ops, "finish"):
+        ops.finish()
     counters = rqrcp_counters(m, n, b, ell, achieved, nblocks,
                               {"k_reached": 1, "short_block": 5, "no_trailing": 6}.get(reason, 0), False)
     return DistResult(achieved, nblocks, reason, perm, A_local, taus[:achieved], counters)
@@ -414,7 +416,7 @@ def trqrcp_block_cyclic(S_local, m: int, n: int, k: int, b: int, p: int, seed: i
         lc = int(lay.local_index(i0)) if owner == r else -1
         pan = ops.tr_panel(S_local, lc, i0, m, k, samp.achieved, bb, owner == r, Yg)
         pan = ops.broadcast_panel(pan, owner, comm, m - i0, bb)
-        bhat, taus_h, R11_h = ops.read_tail(pan)
+        bhat, taus_h, r11_diag = ops.read_tail(pan)
         if bhat == 0:                                   # randomized.py:308-309
             reason = "panel_zero"
             break
@@ -432,7 +434,7 @@ def trqrcp_block_cyclic(S_local, m: int, n: int, k: int, b: int, p: int, seed: i
         if n - achieved == 0:
             reason = "no_trailing"
             break
-        d = np.abs(np.diag(R11_h))
+        d = np.abs(r11_diag)
         if not (d.size > 0 and d.min() > _DIAG_FLOOR * d[0]):   # randomized.py:334-335
             reason = "r11_singular"
             break
@@ -455,7 +457,7 @@ class _Sample:
     moves: np.ndarray
     Bf: object
     st: object
-    prev_tail: object = None  # (bhat, taus, R11) of the previous block's panel, read with this record
+    prev_tail: object = None  # (bhat, taus, diag R11) of the previous block's panel, read with this record
 
 
 @dataclass
@@ -487,13 +489,23 @@ class GpuOps:
         self.Workspace = Workspace
         self._keep = []
         self._shape = None
+        self._stage_h = self._stage_np = self._stage_d = None
+        self._stage_used = 0
+        self._tail = None       # deferred rows of a merged second sweep (lookahead)
+        self._stream = torch.cuda.current_stream(self.dev)
+        self._sh = self._stream.cuda_stream
+        self.lookahead = not os.environ.get("SQR_DIST_NO_LOOKAHEAD")
+        self.plan_moves = bool(os.environ.get("SQR_DIST_PLAN_MOVES"))   # world 1: exercise the P2P plan path
         # SymmComm: panel broadcast and sample all-gather as device-initiated
         # NVLink puts into symmetric buffers (csrc/peer.cu)
         self.symm = comm if getattr(comm, "symm", False) else None
 
     # helpers
     def _s(self):
-        return torch.cuda.current_stream(self.dev).cuda_stream
+        return self._sh   # the caller's current stream, fixed per factorization (begin)
+
+    def _cur(self):
+        return self._stream
 
     def _ws(self, nbytes):
         return self.Workspace.get(nbytes, self.dev)
@@ -502,18 +514,34 @@ class GpuOps:
         self.lib.check(rc, what)
 
     def _idx(self, a):
-        # Index arrays must outlive the asynchronous launch that reads them: a
-        # temporary freed inside an argument list could be handed to the next
-        # allocation of the same call.  Keep them until the next sync point.
-        t = torch.as_tensor(np.asarray(a, dtype=np.int64)).pin_memory().to(self.dev, non_blocking=True)
+        """Upload an index list (asynchronously).  Bump-allocated from one
+        pinned staging buffer and its device twin, both reset at the per-block
+        host synchronisation: every copy and kernel enqueued before it has
+        finished by then (stream order), so neither side is reused early."""
+        a = np.asarray(a, dtype=np.int64)
+        n = a.size
+        if self._stage_h is not None and self._stage_used + n <= self._stage_h.numel():
+            o = self._stage_used
+            self._stage_used = o + ((n + 15) // 16) * 16
+            self._stage_np[o:o + n] = a
+            d = self._stage_d[o:o + n]
+            d.copy_(self._stage_h[o:o + n], non_blocking=True)
+            return d
+        # overflow (never at the shapes the driver uses): a private pinned copy,
+        # kept alive until the next sync point
+        t = torch.as_tensor(a).pin_memory().to(self.dev, non_blocking=True)
         self._keep.append(t)
-        if len(self._keep) > 64:
-            self._keep = self._keep[-64:]
         return t
+
+    def _synced(self):
+        self._stage_used = 0
+        self._keep.clear()
 
     def begin(self, lay, m, ell):
         """Per-shape persistent buffers (allocated on the first call of a
         factorization of this shape)."""
+        self._stream = torch.cuda.current_stream(self.dev)
+        self._sh = self._stream.cuda_stream
         key = (lay.n, lay.b, lay.P, m, ell)
         if self._shape == key:
             return
@@ -557,8 +585,16 @@ class GpuOps:
         self.side = torch.cuda.Stream(self.dev, priority=-1)
         self.prep_done = None
         self.h_ctl = torch.zeros(self.ctl.numel(), dtype=torch.uint8).pin_memory()
+        self.h_ctl_i32 = self.h_ctl.numpy().view(np.int32)
+        self.h_ctl_f64 = self.h_ctl.numpy()[:72].view(np.float64)
         self.h_tail = torch.zeros(b + b * b + 9, dtype=torch.float64).pin_memory()
+        self.h_tail_np = self.h_tail.numpy()
         self.gidx = [torch.tensor(lay.global_of_local(q), device=self.dev) for q in range(lay.P)]
+        ns = 2 * max(nmax, 1) + 64 * b + 1024
+        self._stage_h = torch.zeros(ns, dtype=torch.int64).pin_memory()
+        self._stage_np = self._stage_h.numpy()
+        self._stage_d = torch.zeros(ns, dtype=torch.int64, device=self.dev)
+        self._stage_used = 0
 
     # 1. sketch of the local slab
     def sketch(self, A, m, ell, seed, omega, gloc):
@@ -629,7 +665,7 @@ class GpuOps:
     # 2. replicated sample QRCP
     def _join_prep(self):
         if self.prep_done is not None:
-            torch.cuda.current_stream(self.dev).wait_event(self.prep_done)
+            self._cur().wait_event(self.prep_done)
             self.prep_done = None
 
     def sample_qrcp(self, B, ell, nt, bb, first, pend_pan=None):
@@ -643,29 +679,40 @@ class GpuOps:
                                             self.lperm.data_ptr(), moves.data_ptr(), self.staus.data_ptr(),
                                             1 if first else 0, st.data_ptr(), self.sws.data_ptr(), self.sws.numel(),
                                             self._s()), "sample_qrcp")
-        # one host synchronisation: status + moves, plus the previous panel's tail
+        # one host synchronisation: status + moves, plus the previous panel's tail;
+        # the deferred rows of a merged second sweep run behind it (lookahead)
         self.h_ctl.copy_(self.ctl, non_blocking=True)
         if pend_pan is not None:
             self.h_tail[:pend_pan.tail.numel()].copy_(pend_pan.tail, non_blocking=True)
-        torch.cuda.current_stream(self.dev).synchronize()
-        h = self.h_ctl.numpy()
-        prev_tail = self._parse_tail(self.h_tail.numpy(), pend_pan.Y.shape[0]) if pend_pan is not None else None
-        s = np.frombuffer(h[:72].tobytes(), dtype=self.lib.STATUS_DTYPE)[0]
+        ev = torch.cuda.Event()
+        ev.record(self._cur())
+        self.run_tail()
+        ev.synchronize()
+        self._synced()
+        prev_tail = self._parse_tail(self.h_tail_np, pend_pan.Y.shape[0]) if pend_pan is not None else None
+        hi = self.h_ctl_i32       # sqr_status words: stop, reason, .., sample_achieved (4), .., nmoves (6)
         if first:
-            self._floor = float(s["floor_sq"])
-        stop = bool(s["stop"])
-        reason = {2: "sample_floor", 3: "sample_rank"}.get(int(s["reason"]), "none")
-        nm = int(s["nmoves"])
-        mv = h[128:128 + 8 * nm].view(np.int32).reshape(nm, 2).astype(np.int64)
+            self._floor = float(self.h_ctl_f64[4])   # floor_sq (byte 32)
+        stop = bool(hi[0])
+        reason = {2: "sample_floor", 3: "sample_rank"}.get(int(hi[1]), "none")
+        nm = int(hi[6])
+        mv = hi[32:32 + 2 * nm].reshape(nm, 2).astype(np.int64)   # moves (byte 128): (dst, src) pairs
         mv = mv[(mv[:, 0] >= 0) & (mv[:, 0] != mv[:, 1])]  # drop no-op slots (dst = -1) and self-moves
-        self._keep.clear()
-        smp = _Sample(stop, reason, int(s["sample_achieved"]), mv, self.Bf[:max(nt, 1)], st)
+        smp = _Sample(stop, reason, int(hi[4]), mv, self.Bf[:max(nt, 1)], st)
         smp.prev_tail = prev_tail
         return smp
 
     # 3. point-to-point column moves
-    def move_columns(self, A, ps, pd, lay, comm):
+    def move_columns(self, A, ps, pd, lay, comm, i0=None, samp=None):
         ld = A.shape[1]
+        if comm.size == 1 and samp is not None and not self.plan_moves:
+            # a world of one: every move is local -- the sample QRCP's device
+            # move list drives the register-staged permutation kernel directly
+            # (the single-GPU driver's apply_moves), no host plan or packing
+            nmv = 2 * self.b
+            self._chk(self.L.sqr_apply_moves(A.data_ptr(), ld, ld, i0, None, self.ctl[128:].data_ptr(),
+                                             samp.st.data_ptr(), nmv, self._s()), "apply_moves")
+            return
         plan = move_plan(ps, pd, lay, comm.rank)
         peers_out, peers_in = list(plan.send), list(plan.recv)
         # one upload for every index list of this block
@@ -744,21 +791,35 @@ class GpuOps:
 
     @staticmethod
     def _parse_tail(h, bb):
-        """(bhat, taus, triu R11[:bhat, :bhat]) from a [taus | R11 | status] record."""
+        """(bhat, taus, diag R11[:bhat]) from a [taus | R11 | status] record
+        (the drivers read only R11's diagonal: randomized.py:217-219, 334-335)."""
         meta = h[bb + bb * bb:bb + bb * bb + 9].view(np.int32)
         bhat = 0 if meta[0] else int(meta[5])
-        R = h[bb:bb + bb * bb].reshape(bb, bb).T[:bhat, :bhat]  # (bb, bb) storage is column-major
-        return bhat, h[:bb].copy(), np.triu(R)
+        d = h[bb:bb + bb * bb:bb + 1][:bhat].copy()   # (bb, bb) column-major: stride bb + 1
+        return bhat, h[:bb].copy(), d
 
     def read_tail(self, pan):
         self._join_prep()
-        return self._parse_tail(pan.tail.cpu().numpy(), pan.Y.shape[0])
+        self.run_tail()
+        out = self._parse_tail(pan.tail.cpu().numpy(), pan.Y.shape[0])
+        self._synced()
+        return out
+
+    def run_tail(self):
+        """Enqueue the deferred rows >= i0 + bb of the last merged second sweep."""
+        if self._tail is not None:
+            M, N, K, X, ldx, W, ld, C = self._tail
+            self._tail = None
+            self._gemm_nn(M, N, K, 1.0, X, ldx, W, ld, 1.0, C, ld, C, ld)
+
+    def finish(self):
+        self.run_tail()
 
     # 4b. sample-update prep (R11 guard, M = S11 R11^-1) on a high-priority side
     #     stream while the trailing update runs (cf. driver.cu EarlyPrep)
     def prep_sample_update(self, samp, pan, bb):
         ev = torch.cuda.Event()
-        ev.record(torch.cuda.current_stream(self.dev))
+        ev.record(self._cur())
         self.side.wait_event(ev)
         ell = samp.Bf.shape[1]
         self._chk(self.L.sqr_sample_update_prep(samp.Bf.data_ptr(), ell, pan.R11.data_ptr(), bb, bb,
@@ -847,7 +908,14 @@ class GpuOps:
         Ycat = self._scratch("_ycat", (b + bb) * mr)[:(b + bb) * mr].view(b + bb, mr)
         Ycat[:b].copy_(ppan.Y[:, i0 - pi0:])
         Ycat[b:].copy_(pan.Y)
-        self._gemm_nn(mr, ncols, b + bb, 1.0, Ycat.data_ptr(), mr, Wp, ld, 1.0, C, ld, C, ld)
+        if self.lookahead and mr > bb:
+            # the R12 rows now (the sample update reads them); the rows below
+            # run after the next block's sample QRCP is launched, so they cover
+            # that block's host synchronisation (run_tail)
+            self._gemm_nn(bb, ncols, b + bb, 1.0, Ycat.data_ptr(), mr, Wp, ld, 1.0, C, ld, C, ld)
+            self._tail = (mr - bb, ncols, b + bb, Ycat.data_ptr() + 8 * bb, mr, Wp, ld, C + 8 * bb)
+        else:
+            self._gemm_nn(mr, ncols, b + bb, 1.0, Ycat.data_ptr(), mr, Wp, ld, 1.0, C, ld, C, ld)
 
     def flush_pending(self, A, t0, i0, m, pan):
         """The deferred rows >= i0 + b of a block whose pair partner never came."""
@@ -940,10 +1008,22 @@ class GpuOps:
         r_row0 = i0 if r_row0 is None else r_row0
         prepped = self.prep_done is not None
         if prepped:  # the overlapped prep wrote mbuf and may have set samp.st->stop
-            torch.cuda.current_stream(self.dev).wait_event(self.prep_done)
+            self._cur().wait_event(self.prep_done)
             self.prep_done = None
         if nloc == 0:
             return self.slab[:0]
+        ld = A.shape[1]
+        if prepped and rel[-1] - rel[0] == nloc - 1 and s0 >= bb:
+            # no gathers: the apply reads only S12 = Bf[:, b:] and R12 = R[:, b:]
+            # (M = S11 R11^-1 came from the prep), so both are passed in place,
+            # based b columns before my first trailing column (contiguous: a
+            # world of one, or the last rank's tail)
+            Sb = samp.Bf.data_ptr() + 8 * (int(rel[0]) - bb) * ell
+            Rb = A.data_ptr() + 8 * ((s0 - bb) * ld + r_row0)
+            self._chk(self.L.sqr_sample_update_apply(Sb, ell, ell, Rb, ld, nloc, bb, self.slab.data_ptr(), ell,
+                                                     samp.st.data_ptr(), self.mbuf.data_ptr(), self._s()),
+                      "sample_update")
+            return self.slab[:nloc]
         # Bf_loc = [S11 | Bf[:, rel]] and R_loc = [R11 | R12 of my columns]
         Bfl = self.Bfl[:bb + nloc]
         Bfl[:bb].copy_(samp.Bf[:bb])
@@ -952,7 +1032,6 @@ class GpuOps:
                                           Bfl.data_ptr() + 8 * bb * ell, ell, None, nloc, self._s()), "gather S")
         Rl = self.Rl.view(-1)[:(bb + nloc) * bb].view(bb + nloc, bb)
         Rl[:bb].copy_(pan.R11)
-        ld = A.shape[1]
         self._chk(self.L.sqr_copy_columns(A.data_ptr() + 8 * (s0 * ld + r_row0), ld, bb, None,
                                           Rl.data_ptr() + 8 * bb * bb, bb, None, nloc, self._s()), "gather R12")
         if prepped:  # M from the overlapped prep

@@ -63,7 +63,7 @@ class NumpyOps:
         moves = np.stack([q, lp[q]], axis=1).astype(np.int64)
         return _Sample(False, "none", st.achieved, moves, torch.from_numpy(np.ascontiguousarray(st.B.T)), st)
 
-    def move_columns(self, A, ps, pd, lay, comm):
+    def move_columns(self, A, ps, pd, lay, comm, i0=None, samp=None):
         # the same plan GpuOps executes (distributed.move_plan)
         plan = move_plan(ps, pd, lay, comm.rank)
         packed = A[torch.as_tensor(plan.pack)].clone() if plan.pack.size else None
@@ -109,7 +109,7 @@ class NumpyOps:
     def read_tail(self, pan):
         mh = pan.tail.numpy()
         bhat = 0 if mh[0] else int(mh[5])
-        return bhat, pan.taus.numpy().copy(), np.triu(pan.R11.numpy().T[:bhat, :bhat])
+        return bhat, pan.taus.numpy().copy(), np.diag(pan.R11.numpy().T[:bhat, :bhat]).copy()
 
     def block_update(self, A, t0, i0, m, pan, ncols=None):
         Y = pan.Y.numpy().T

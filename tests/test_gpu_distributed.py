@@ -17,7 +17,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import torch.distributed as dist  # noqa: E402
 
 import paper_2008_04447_b200 as G  # noqa: E402
-from paper_2008_04447_b200.distributed import BlockCyclic, GpuOps, TorchComm, rqrcp_block_cyclic  # noqa: E402
+from paper_2008_04447_b200.distributed import GpuOps, TorchComm, rqrcp_block_cyclic  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -39,15 +39,19 @@ def _slab(A, m, rows, dev):
     return S.to(dev)
 
 
+@pytest.mark.parametrize("plan", [False, True])
 @pytest.mark.parametrize("paired", [False, True])
 @pytest.mark.parametrize("m,n,k,b,p", [(600, 500, 500, 32, 8), (2000, 700, 300, 64, 8), (300, 257, 257, 16, 4)])
-def test_block_cyclic_gpu_world1(nccl1, m, n, k, b, p, paired):
+def test_block_cyclic_gpu_world1(nccl1, m, n, k, b, p, paired, plan):
+    """plan=False: a world of one applies the sample QRCP's device move list
+    directly; plan=True forces the P2P path (move plan, pack, exchange, unpack)."""
     dev = nccl1
     A = gauss(m, n, 3)
     om = O.gauss_matrix(b + p, m, 11)
-    lay = BlockCyclic(n, b, 1)
     A_loc = _slab(A, m, m + 2 * b if paired else m, dev)
-    res = rqrcp_block_cyclic(A_loc, m, n, k, b, p, 11, TorchComm(), GpuOps(dev), omega=om)
+    ops = GpuOps(dev)
+    ops.plan_moves = plan
+    res = rqrcp_block_cyclic(A_loc, m, n, k, b, p, 11, TorchComm(), ops, omega=om)
     ref = O.rqrcp(A, k, b=b, p=p, seed=11)
     assert res.achieved == ref.achieved_rank
     assert np.array_equal(res.perm, ref.perm)
