@@ -542,6 +542,7 @@ class GpuOps:
         factorization of this shape)."""
         self._stream = torch.cuda.current_stream(self.dev)
         self._sh = self._stream.cuda_stream
+        self._P = lay.P
         key = (lay.n, lay.b, lay.P, m, ell)
         if self._shape == key:
             return
@@ -640,6 +641,8 @@ class GpuOps:
         (one sqr_peer_put_columns: all-gather + assembly), then a device-side
         wait for every rank's epoch.  Else NCCL all-gather + assembly."""
         if self.symm is None:
+            if comm.size == 1 and slab.data_ptr() == self.Bglob[p0:].data_ptr():
+                return self.Bglob[p0:]     # already in place (sample_update_local)
             parts = comm.all_gather(self.pad_slab(slab, lay, p0))
             return self._assemble(parts, lay, ell, p0)
         sy = self.symm
@@ -1020,10 +1023,12 @@ class GpuOps:
             # world of one, or the last rank's tail)
             Sb = samp.Bf.data_ptr() + 8 * (int(rel[0]) - bb) * ell
             Rb = A.data_ptr() + 8 * ((s0 - bb) * ld + r_row0)
-            self._chk(self.L.sqr_sample_update_apply(Sb, ell, ell, Rb, ld, nloc, bb, self.slab.data_ptr(), ell,
+            # a world of one (NCCL path): straight into the replicated sample
+            out = self.Bglob[i0 + bb:i0 + bb + nloc] if (self.symm is None and self._P == 1) else self.slab[:nloc]
+            self._chk(self.L.sqr_sample_update_apply(Sb, ell, ell, Rb, ld, nloc, bb, out.data_ptr(), ell,
                                                      samp.st.data_ptr(), self.mbuf.data_ptr(), self._s()),
                       "sample_update")
-            return self.slab[:nloc]
+            return out
         # Bf_loc = [S11 | Bf[:, rel]] and R_loc = [R11 | R12 of my columns]
         Bfl = self.Bfl[:bb + nloc]
         Bfl[:bb].copy_(samp.Bf[:bb])
