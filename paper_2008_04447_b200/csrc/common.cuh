@@ -228,6 +228,19 @@ struct GemmDyn {
   int limit_off = 0;
 };
 
+// "Every CTA of this launch is resident" signal of the whole-SM chain kernels
+// (sample QRCP, panel): CTA 0 stores val to *flag after the kernel's first
+// grid / cluster barrier (or on an early exit).  The driver holds a GEMM on
+// another stream behind wait_resident() until then, so the chain kernel
+// takes its SMs first and the GEMM's CTAs fill the rest (driver.cu, Overlap).
+struct ResidentSig {
+  unsigned* flag = nullptr;
+  unsigned val = 0;
+};
+__device__ __forceinline__ void signal_resident(const ResidentSig& s) {
+  if (s.flag != nullptr) st_release_u32(s.flag, s.val);
+}
+
 __host__ __device__ constexpr int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __host__ __device__ constexpr int64_t rup(int64_t a, int64_t b) { return cdiv(a, b) * b; }
 
@@ -244,12 +257,16 @@ int gemm_nn(int64_t M, int64_t N, int64_t K, double alpha, const double* X, int6
 int64_t sample_qrcp_workspace(int64_t ell, int64_t nt);
 int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf, int64_t ldbf,
                 int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st, void* ws,
-                int64_t ws_bytes, cudaStream_t s);
+                int64_t ws_bytes, cudaStream_t s, ResidentSig sig = {});
+// Holds stream s until *sig.flag == sig.val (bounded by timeout_us).
+int wait_resident(ResidentSig sig, int timeout_us, cudaStream_t s);
+int signal_resident_host(ResidentSig sig, cudaStream_t s);
 int64_t panel_workspace(int64_t w);
 int64_t panel_block_max_rows();
 int64_t panel_block_workspace();
 int panel_block(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
-                double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s);
+                double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s,
+                ResidentSig sig = {});
 int panel_qr(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
              double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s,
              int64_t c0 = 0);

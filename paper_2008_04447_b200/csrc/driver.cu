@@ -40,6 +40,8 @@ struct RqrcpWs {
   int32_t* moves;
   int32_t* snap;  // {stop .. bhat} of the block whose bulk update is in flight
   int32_t* guard; // R11 guard verdict of the early sample-update prep (EarlyPrep)
+  double* Ypan2;  // second [Y_P | Y_J] buffer: pairs alternate (Overlap)
+  unsigned* sig;  // ResidentSig word of the overlapped chain kernels
   void *sample, *panel;
   int64_t sample_bytes, panel_bytes;
   int64_t total;
@@ -68,8 +70,15 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.pscr = c.take<double>(PanelScratch::doubles(b));
   w.snap = c.take<int32_t>(8);
   w.guard = c.take<int32_t>(8);
+  w.sig = reinterpret_cast<unsigned*>(c.take<int32_t>(16));
+  w.Ypan2 = c.take<double>(m * 2 * b);
   w.total = c.off + 256;
   return w;
+}
+
+bool panel_is_block(int64_t mr, int64_t bb) {
+  static const bool no_block = env_flag("SQR_NO_BLOCKPANEL");
+  return !no_block && mr <= panel_block_max_rows() && bb <= 128;
 }
 
 // Panel QR (randomized.py:107-130 / reference.py:281-291) as 32-wide leaves
@@ -80,11 +89,11 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
 // and WY updates never touch columns beyond it.
 int panel_factor(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t wstat, double* Y, int64_t ldy,
                  double* taus, int stop_at_zero, sqr_status* st, void* pws, int64_t pwsb, const PanelScratch& sc,
-                 double* gws, cudaStream_t s) {
-  static const bool no_block = env_flag("SQR_NO_BLOCKPANEL");
-  if (!no_block && mr <= panel_block_max_rows() && bb <= 128)
-    return panel_block(P, lda, mr, wstat, bb, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s);
+                 double* gws, cudaStream_t s, ResidentSig sig = {}) {
+  if (panel_is_block(mr, bb))
+    return panel_block(P, lda, mr, wstat, bb, Y, ldy, taus, stop_at_zero, st, pws, pwsb, s, sig);
   int rc;
+  if ((rc = signal_resident_host(sig, s))) return rc;
   // 16-wide leaves when the panel needs 3-4 rows per thread (register file)
   const int64_t rows1 = (int64_t)std::min(sm_count(), 148) * 256;
   const int64_t leaf = (mr > 2 * rows1 && mr <= 4 * rows1) ? 16 : kLeaf;
@@ -193,7 +202,8 @@ int pending_panel_update(double* P, int64_t lda, int64_t mr, int64_t bb, int64_t
 
 int trailing_second(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, int64_t b, const double* Ycat,
                     int64_t ldy, const double* taus, double* T, int64_t ldt, double* GWt, int64_t ldw,
-                    double* Wcat, int64_t ldwc, sqr_status* st, double* gws, cudaStream_t s) {
+                    double* Wcat, int64_t ldwc, sqr_status* st, double* gws, cudaStream_t s,
+                    bool skip_merged = false) {
   const double* Yj = Ycat + b * ldy + b;  // rows from i0_J
   GemmDyn d1{&st->stop, &st->bhat, kShiftB};
   d1.pre = Ycat + b;  // [Y_P | Y_J] rows from i0_J
@@ -209,7 +219,7 @@ int trailing_second(double* P, int64_t lda, int64_t mr, int64_t nt, int64_t bb, 
   if (rc) return rc;
   rc = gemm_tn(bb, nt, bb, -1.0, T, ldt, Wt, ldw, 0.0, nullptr, 0, Wcat + b, ldwc, gws, kGemmWsBytes, s,
                GemmDyn{&st->stop, &st->bhat, kShiftD});
-  if (rc) return rc;
+  if (rc || skip_merged) return rc;
   return gemm_nn(mr, nt, b + bb, 1.0, Ycat + b, ldy, Wcat, ldwc, 1.0, P, lda, P, lda, s,
                  GemmDyn{&st->stop, &st->bhat, kShiftB | kShiftD});
 }
@@ -248,6 +258,63 @@ struct Lookahead {
     return SQR_OK;
   }
 };
+
+// Chain / bulk overlap of the paired schedule.  The chain kernels (sample
+// QRCP, panel) are latency-bound and hold their working set on chip: each of
+// their CTAs takes a whole SM, but only ceil(n_t / 256) (sample) or
+// ceil(m_r / 256) (panel) SMs -- the rest of the chip idles for ~1.2 ms per
+// block.  The merged second sweep of a pair (the bulk rows below the R12
+// rows, randomized.py:207) is therefore split by rows around the next
+// block's chain:
+//   R12 rows -> finish_block -> sample update
+//   { next sample QRCP  ||  bulk rows A }          next pivots known
+//   column moves on C and on [W_P ; W_J]; the next panel's columns get the
+//   pair's update in rows B from their own K = 2b GEMM
+//   { next panel        ||  bulk rows B of the other columns }
+// Each chain kernel goes first (high-priority stream; the GEMM's stream is
+// held until the kernel reports all CTAs resident, ResidentSig), the GEMM's
+// CTAs fill the SMs it leaves free and spread over the chip when it ends.
+// Per entry the arithmetic is that of the single merged sweep (same K order),
+// so results are bitwise unchanged.  The bulk GEMMs gate on a snapshot of
+// {stop, bhat} taken before finish_block, like Lookahead.
+struct Overlap {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  unsigned epoch = 0;
+  ~Overlap() {
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+    if (side) cudaStreamDestroy(side);
+  }
+  int init() {
+    int lo = 0, hi = 0;
+    SQR_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    SQR_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+    SQR_CUDA(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    SQR_CUDA(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    return SQR_OK;
+  }
+  int fork_from(cudaStream_t s) {
+    SQR_CUDA(cudaEventRecord(fork, s));
+    SQR_CUDA(cudaStreamWaitEvent(side, fork, 0));
+    return SQR_OK;
+  }
+  int mark_join() {
+    SQR_CUDA(cudaEventRecord(join, side));
+    return SQR_OK;
+  }
+  int join_to(cudaStream_t s) {
+    SQR_CUDA(cudaStreamWaitEvent(s, join, 0));
+    return SQR_OK;
+  }
+};
+// bulk rows of a pair still to be applied when the next block starts
+struct OverlapCarry {
+  bool on = false;
+  int64_t i0p = 0, bbp = 0, mrp = 0, rB = 0;  // the merging block's i0 / width / rows; first row of part B
+  const double* Ycat = nullptr;               // the pair's [Y_P | Y_J]
+};
+constexpr int kResidentTimeoutUs = 100;
 
 // M = S11 R11^-1 and the R11 guard of the sample update (sketch.py:132-149,
 // randomized.py:217-219) depend only on the block's factored sample and its
@@ -415,28 +482,66 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
   EarlyPrep ep;
   const bool early = !resample && !la.on && !no_early;
   if (early && (rc = ep.init())) return rc;
-  if (pair) SQR_CUDA(cudaMemset2DAsync(w.Ypan + b * m, m * 8, 0, b * 8, b, s));  // Y_J's zero top rows
+  static const bool no_overlap = env_flag("SQR_NO_OVERLAP");
+  const bool overlap = pair && !no_overlap;
+  Overlap ov;
+  OverlapCarry cy;
+  if (overlap) {
+    if ((rc = ov.init())) return rc;
+    SQR_CUDA(cudaMemsetAsync(w.sig, 0, 64, s));
+  }
+  if (pair) {  // Y_J's zero top rows
+    SQR_CUDA(cudaMemset2DAsync(w.Ypan + b * m, m * 8, 0, b * 8, b, s));
+    if (overlap) SQR_CUDA(cudaMemset2DAsync(w.Ypan2 + b * m, m * 8, 0, b * 8, b, s));
+  }
   for (int64_t J = 0; J < nblk; ++J) {
     const int64_t i0 = J * b, bb = std::min(b, k - i0), nt = n - i0, mr = m - i0;
     double* P = A + i0 + i0 * lda;
     double* TJ = T + J * b * b;
     const bool second = pair && (J & 1);                      // merges the pending block J-1
     const bool first = pair && !(J & 1) && J + 1 < nblk;      // second sweep deferred to J+1
-    double* Yj = second ? w.Ypan + b * m + b : w.Ypan;         // ld m, rows from i0
-    if ((J == 0 || !la.on) &&
-        (rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
-                          w.sample_bytes, s)))
+    double* Ypair = (overlap && ((J >> 1) & 1)) ? w.Ypan2 : w.Ypan;  // this pair's [Y_P | Y_J]
+    double* Yj = second ? Ypair + b * m + b : Ypair;          // ld m, rows from i0
+    if (cy.on) {
+      if ((rc = ov.join_to(s))) return rc;  // the sample QRCP launched behind the previous block's R12 rows
+    } else if ((J == 0 || !la.on) &&
+               (rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
+                                 w.sample_bytes, s)))
       return rc;
     if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
     if (second) {
       if ((rc = apply_moves(w.W, 2 * b, b, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
-      if ((rc = pending_panel_update(P, lda, mr, bb, b, w.Ypan, m, w.W, 2 * b, st, s))) return rc;
+      if ((rc = pending_panel_update(P, lda, mr, bb, b, Ypair, m, w.W, 2 * b, st, s))) return rc;
     }
-    {
-      PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
-      if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm, s)))
+    PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
+    if (cy.on) {
+      // Rows B of the previous pair's merged sweep (see Overlap): W follows
+      // the moves, the panel columns are updated on their own, the panel
+      // runs beside the update of the other columns.
+      cy.on = false;
+      const int64_t kk = b + cy.bbp, mB = cy.mrp - cy.rB;
+      double* Wm = w.W + cy.bbp * 2 * b;  // column i0 of A
+      if ((rc = apply_moves(Wm, 2 * b, kk, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
+      const double* YB = cy.Ycat + b + cy.rB;
+      double* PB = A + (cy.i0p + cy.rB) + i0 * lda;
+      const GemmDyn dsn{&w.snap[0], nullptr, 0};
+      if (mB > 0 && (rc = gemm_nn(mB, bb, kk, 1.0, YB, m, Wm, 2 * b, 1.0, PB, lda, PB, lda, s, dsn))) return rc;
+      if ((rc = ov.fork_from(s))) return rc;
+      const ResidentSig sig{w.sig, ++ov.epoch};
+      if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm,
+                             ov.side, sig)))
         return rc;
-    }
+      if ((rc = ov.mark_join())) return rc;
+      if (mB > 0 && nt - bb > 0) {
+        if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
+        if ((rc = gemm_nn(mB, nt - bb, kk, 1.0, YB, m, Wm + bb * 2 * b, 2 * b, 1.0, PB + bb * lda, lda,
+                          PB + bb * lda, lda, s, dsn)))
+          return rc;
+      }
+      if ((rc = ov.join_to(s))) return rc;
+    } else if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm,
+                                  s)))
+      return rc;
     const bool prep = early && J + 1 < nblk && nt - bb > 0;
     if (prep && (rc = ep.launch(w.Bf, ell, P, lda, bb, w.Gm, st, w.guard, s))) return rc;
     if (la.on) {
@@ -461,13 +566,48 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       SQR_CUDA(cudaStreamWaitEvent(s, la.join, 0));
       continue;
     }
+    // Overlap: worth it while the bulk rows outlast the chain kernels they hide
+    // (and those leave an SM for the waiting thread).
+    const int64_t top = std::min(bb, mr);
+    const bool split = overlap && second && J + 1 < nblk && nt > 1 && mr - top >= 1024 &&
+                       (mr - top) * (nt - bb) >= (int64_t)3 << 22 && nt - bb <= 147 * 256 && mr - bb <= 147 * 256;
     if (first)
-      rc = trailing_first(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s);
+      rc = trailing_first(P, lda, mr, nt, bb, Ypair, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s);
     else if (second)
-      rc = trailing_second(P, lda, mr, nt, bb, b, w.Ypan, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s);
+      rc = trailing_second(P, lda, mr, nt, bb, b, Ypair, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s,
+                           split);
     else
-      rc = trailing_update(P, lda, mr, nt, bb, w.Ypan, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s);
+      rc = trailing_update(P, lda, mr, nt, bb, Ypair, m, taus + i0, TJ, b, w.Wt, w.W, b, st, w.gemm, s);
     if (rc) return rc;
+    if (split) {
+      // R12 rows of the merged sweep now, the bulk rows around the next chain.
+      SQR_CUDA(cudaMemcpyAsync(w.snap, st, 6 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      const GemmDyn dm{&w.snap[0], &w.snap[5], kShiftB | kShiftD};
+      if ((rc = gemm_nn(top, nt, b + bb, 1.0, Ypair + b, m, w.W, 2 * b, 1.0, P, lda, P, lda, s, dm))) return rc;
+      if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
+      if (prep && (rc = ep.wait(s))) return rc;
+      if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s, prep ? w.guard : nullptr))) return rc;
+      if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, bb, Bn, ell, st, w.Gm, s, prep))) return rc;
+      std::swap(Bc, Bn);
+      if ((rc = ov.fork_from(s))) return rc;
+      const ResidentSig sig{w.sig, ++ov.epoch};
+      if ((rc = sample_qrcp(Bc, ell, ell, nt - bb, std::min(b, k - i0 - bb), w.Bf, ell, w.lperm, w.moves, w.stau, 0,
+                            st, w.sample, w.sample_bytes, ov.side, sig)))
+        return rc;
+      if ((rc = ov.mark_join())) return rc;
+      if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
+      const int64_t rB = top + rup((mr - top) / 2, 64);
+      if ((rc = gemm_nn(rB - top, nt, b + bb, 1.0, Ypair + b + top, m, w.W, 2 * b, 1.0, P + top, lda, P + top, lda, s,
+                        dm)))
+        return rc;
+      cy.on = true;
+      cy.i0p = i0;
+      cy.bbp = bb;
+      cy.mrp = mr;
+      cy.rB = rB;
+      cy.Ycat = Ypair;
+      continue;
+    }
     // R columns [i0, i0+bb) go out only now: a short panel (bhat < bb) leaves
     // columns [i0+bhat, i0+bb) in the trailing matrix, whose R rows
     // [i0, i0+bhat) the update above has just rewritten (randomized.py:203-213).

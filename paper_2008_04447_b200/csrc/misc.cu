@@ -386,6 +386,18 @@ __global__ void copy_columns_kernel(const double* src, int64_t lds, int64_t rows
   }
 }
 
+// One thread holds its stream until a chain kernel on another stream has
+// signalled that all its CTAs are resident (ResidentSig, common.cuh); the
+// timeout bounds the wait if that kernel cannot start first.
+__global__ void wait_resident_kernel(const unsigned* flag, unsigned val, unsigned long long timeout_ns) {
+  const unsigned long long t0 = gtimer();
+  while ((int)(ld_acquire_u32(flag) - val) < 0) {
+    if (gtimer() - t0 > timeout_ns) break;
+    __nanosleep(200);
+  }
+}
+__global__ void signal_resident_kernel(ResidentSig sig) { signal_resident(sig); }
+
 // W[0:rows, c] = 0 for c < min(ncols, *lim) (gated on *gate): retires the
 // columns of a deferred block update that were already applied in place.
 __global__ void zero_columns_kernel(double* W, int64_t ld, int rows, int ncols, const int32_t* lim,
@@ -558,6 +570,20 @@ int copy_columns(const double* src, int64_t lds, int64_t rows, const int64_t* si
   dim3 grid((unsigned)std::min<int64_t>(cdiv(rows, 256), 64), (unsigned)std::min<int64_t>(n, 4096));
   copy_columns_kernel<<<grid, 256, 0, s>>>(src, lds, rows, sidx, dst, ldd, didx, n);
   SQR_LAUNCH("copy_columns_kernel");
+  return SQR_OK;
+}
+
+int wait_resident(ResidentSig sig, int timeout_us, cudaStream_t s) {
+  if (sig.flag == nullptr) return SQR_OK;
+  wait_resident_kernel<<<1, 1, 0, s>>>(sig.flag, sig.val, (unsigned long long)timeout_us * 1000ull);
+  SQR_LAUNCH("wait_resident_kernel");
+  return SQR_OK;
+}
+
+int signal_resident_host(ResidentSig sig, cudaStream_t s) {
+  if (sig.flag == nullptr) return SQR_OK;
+  signal_resident_kernel<<<1, 1, 0, s>>>(sig);
+  SQR_LAUNCH("signal_resident_kernel");
   return SQR_OK;
 }
 

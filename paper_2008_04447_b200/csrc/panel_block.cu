@@ -43,6 +43,7 @@ struct BlockPanelArgs {
   double* mpart;  // [4096][G]        boundary partials (value-major)
   double* mred;   // [4096]           boundary sums
   unsigned long long* trace;
+  ResidentSig sig;
 };
 
 constexpr int kWP = kLf + 4;        // W pitch (4 mod 32: conflict-free B fragments)
@@ -64,7 +65,10 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
   __shared__ double vals[kLf];
   __shared__ double rowv[kLf];
   __shared__ double wv[kLf];
-  if (a.st->stop) return;
+  if (a.st->stop) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) signal_resident(a.sig);
+    return;
+  }
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   const int w = max(0, min(a.wstat < 0 ? a.st->sample_achieved : a.wstat, a.wmax));
@@ -136,6 +140,7 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
       long long ck2 = ck ? clock64() : 0;
       if (tc < 40) SQR_TRACE(a.trace, 8 * tc + 1);
       gb.sync();
+      if (step == 1 && g == 0 && tid == 0) signal_resident(a.sig);  // first barrier passed: all CTAs resident
       if (tc < 40) SQR_TRACE(a.trace, 8 * tc + 2);
       long long ck3 = ck ? clock64() : 0;
       {
@@ -481,6 +486,7 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
     for (int c = ((w + kLf - 1) / kLf) * kLf; c < a.wmax; ++c) a.Y[(int64_t)c * a.ldy + R] = 0.0;
   }
   if (g == 0 && tid == 0) {
+    if (step == 0) signal_resident(a.sig);  // empty panel: no barrier was reached
     for (int c = bhat; c < a.wmax; ++c) a.taus[c] = 0.0;
     a.st->bhat = bhat;
     if (bhat == 0 && a.stop_at_zero) {
@@ -499,8 +505,9 @@ int64_t panel_block_workspace() {
 }
 
 int panel_block(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, double* Y, int64_t ldy,
-                double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s) {
-  if (mr <= 0 || wmax <= 0) return SQR_OK;
+                double* taus, int stop_at_zero, sqr_status* st, void* ws, int64_t ws_bytes, cudaStream_t s,
+                ResidentSig sig) {
+  if (mr <= 0 || wmax <= 0) return sig.flag ? signal_resident_host(sig, s) : SQR_OK;
   if (wmax > 128 || mr > panel_block_max_rows() || ws_bytes < panel_block_workspace()) {
     set_error("panel_block: unsupported panel %lld x %lld", (long long)mr, (long long)wmax);
     return SQR_EINVAL;
@@ -529,6 +536,7 @@ int panel_block(double* P, int64_t ldp, int64_t mr, int64_t w, int64_t wmax, dou
   p += (int64_t)4096 * 148 * 8;
   a.mred = reinterpret_cast<double*>(p);
   a.trace = g_trace_host_ptr;
+  a.sig = sig;
   const int smem = kSmemDoubles * 8;
   if (int rc = smem_optin((const void*)panel_block_kernel, smem)) return rc;
   void* args[] = {&a};

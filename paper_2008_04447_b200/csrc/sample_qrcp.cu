@@ -706,6 +706,7 @@ struct RegArgs {
   double* psum;
   double* pmax;
   unsigned long long* trace;
+  ResidentSig sig;
 };
 
 __device__ __forceinline__ void add_move(const RegArgs& a, int dst, int src) {
@@ -741,7 +742,10 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
     double beta, tau;
   };
   __shared__ Bcast bc_s;
-  if (a.st->stop) return;
+  if (a.st->stop) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) signal_resident(a.sig);
+    return;
+  }
   GridBarrier gb;
   if (!CL) gb.init(a.bar);
   namespace cg = cooperative_groups;
@@ -824,6 +828,7 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       gmax = fmax(gmax, __ldcg(a.pmax + i));
     }
   }
+  if (g == 0 && tid == 0) signal_resident(a.sig);  // every CTA has passed a barrier: all resident
   const double fro = sqrt(total);
   const double rank_floor_sq = (kRankFloor * fro) * (kRankFloor * fro);
   const double sample_floor = a.first ? kSampleFloor * kSampleFloor * gmax : __ldcg(&a.st->floor_sq);
@@ -1212,7 +1217,7 @@ int64_t sample_qrcp_workspace(int64_t ell, int64_t nt) { return SampleWorkspace:
 
 int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf,
                 int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st,
-                void* ws, int64_t ws_bytes, cudaStream_t s) {
+                void* ws, int64_t ws_bytes, cudaStream_t s, ResidentSig sig) {
   if (ell <= 0 || nt < 0 || bb < 0 || bb > ell || bb > nt) {
     set_error("sample_qrcp: bad shape ell=%lld nt=%lld bb=%lld", (long long)ell, (long long)nt,
               (long long)bb);
@@ -1222,12 +1227,18 @@ int sample_qrcp(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t b
     set_error("sample_qrcp: workspace too small");
     return SQR_EINVAL;
   }
-  if (sample_epoch_eligible(ell, nt))
-    return sample_epoch(B, ldb, ell, nt, bb, Bf, ldbf, lperm, moves, taus, first, st, ws, ws_bytes, s);
   const int sms = sm_count();
   static const bool no_reg = env_flag("SQR_NO_REGSAMPLE");
-  if (!no_reg && ell <= 144 && nt <= (int64_t)std::min(sms, 148) * kRT) {
+  const bool reg_path = !sample_epoch_eligible(ell, nt) && !no_reg && ell <= 144 &&
+                        nt <= (int64_t)std::min(sms, 148) * kRT;
+  // kernels without the in-kernel signal: release the waiter up front
+  if (sig.flag != nullptr && !reg_path)
+    if (int rc = signal_resident_host(sig, s)) return rc;
+  if (sample_epoch_eligible(ell, nt))
+    return sample_epoch(B, ldb, ell, nt, bb, Bf, ldbf, lperm, moves, taus, first, st, ws, ws_bytes, s);
+  if (reg_path) {
     RegArgs a{};
+    a.sig = sig;
     a.B = B;
     a.ldb = ldb;
     a.ell = (int)ell;
