@@ -42,6 +42,7 @@ struct RqrcpWs {
   int32_t* guard; // R11 guard verdict of the early sample-update prep (EarlyPrep)
   double* Ypan2;  // second [Y_P | Y_J] buffer: pairs alternate (Overlap)
   unsigned* sig;  // ResidentSig word of the overlapped chain kernels
+  int32_t* snap2; // {stop .. bhat} of a pair's first block (early rows, Overlap)
   void *sample, *panel;
   int64_t sample_bytes, panel_bytes;
   int64_t total;
@@ -71,6 +72,7 @@ RqrcpWs carve_rqrcp(void* ws, int64_t m, int64_t n, int64_t b, int64_t p, bool n
   w.snap = c.take<int32_t>(8);
   w.guard = c.take<int32_t>(8);
   w.sig = reinterpret_cast<unsigned*>(c.take<int32_t>(16));
+  w.snap2 = c.take<int32_t>(8);
   w.Ypan2 = c.take<double>(m * 2 * b);
   w.total = c.off + 256;
   return w;
@@ -312,8 +314,22 @@ struct Overlap {
 struct OverlapCarry {
   bool on = false;
   int64_t i0p = 0, bbp = 0, mrp = 0, rB = 0;  // the merging block's i0 / width / rows; first row of part B
+  int64_t koff = 0;                           // b when rows B already hold P's update (early rows): K = bbp
   const double* Ycat = nullptr;               // the pair's [Y_P | Y_J]
 };
+// The second block's chain is hidden the same way behind the pair's FIRST
+// block: while its sample QRCP runs, the bottom rows [ra, mr) of P's own
+// second sweep are applied (K = b, every trailing column, before the column
+// moves), and Y_P's rows there are zeroed -- so the pending panel update, the
+// corrected first sweep (prefix Gram over the remaining rows only) and a
+// K = 2b sweep would all skip them by themselves; the merged sweep then runs
+// K = 2b above ra (beside the next sample QRCP) and K = b, Y_J only, below
+// (beside the next panel).  ra is sized to the SMs the sample QRCP leaves.
+struct EarlyRows {
+  bool sample_launched = false;  // the second block's sample QRCP is already on the side stream
+  int64_t ra = 0;                // first early row relative to the second block's i0 (0 = none)
+};
+constexpr double kEarlyRowsWork = 0.9 * 31.4e12 * 0.66e-3 / 2.0;  // row x column x K products one sample QRCP hides
 constexpr int kResidentTimeoutUs = 100;
 
 // M = S11 R11^-1 and the R11 guard of the sample update (sketch.py:132-149,
@@ -486,6 +502,13 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
   const bool overlap = pair && !no_overlap;
   Overlap ov;
   OverlapCarry cy;
+  EarlyRows er;
+  static const bool no_early_rows = env_flag("SQR_NO_EARLY_ROWS");
+  auto will_split = [&](int64_t Jn) {  // the merged sweep of second block Jn runs split around the next chain
+    const int64_t i0n = Jn * b, bbn = std::min(b, k - i0n), ntn = n - i0n, mrn = m - i0n, topn = std::min(bbn, mrn);
+    return overlap && (Jn & 1) && Jn + 1 < nblk && ntn > 1 && mrn - topn >= 1024 &&
+           (mrn - topn) * (ntn - bbn) >= (int64_t)3 << 22 && ntn - bbn <= 147 * 256 && mrn - bbn <= 147 * 256;
+  };
   if (overlap) {
     if ((rc = ov.init())) return rc;
     SQR_CUDA(cudaMemsetAsync(w.sig, 0, 64, s));
@@ -502,8 +525,9 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     const bool first = pair && !(J & 1) && J + 1 < nblk;      // second sweep deferred to J+1
     double* Ypair = (overlap && ((J >> 1) & 1)) ? w.Ypan2 : w.Ypan;  // this pair's [Y_P | Y_J]
     double* Yj = second ? Ypair + b * m + b : Ypair;          // ld m, rows from i0
-    if (cy.on) {
+    if (cy.on || er.sample_launched) {
       if ((rc = ov.join_to(s))) return rc;  // the sample QRCP launched behind the previous block's R12 rows
+      er.sample_launched = false;
     } else if ((J == 0 || !la.on) &&
                (rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
                                  w.sample_bytes, s)))
@@ -519,10 +543,10 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       // the moves, the panel columns are updated on their own, the panel
       // runs beside the update of the other columns.
       cy.on = false;
-      const int64_t kk = b + cy.bbp, mB = cy.mrp - cy.rB;
-      double* Wm = w.W + cy.bbp * 2 * b;  // column i0 of A
+      const int64_t kk = b + cy.bbp - cy.koff, mB = cy.mrp - cy.rB;
+      double* Wm = w.W + cy.bbp * 2 * b + cy.koff;  // column i0 of A
       if ((rc = apply_moves(Wm, 2 * b, kk, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
-      const double* YB = cy.Ycat + b + cy.rB;
+      const double* YB = cy.Ycat + b + cy.rB + cy.koff * m;
       double* PB = A + (cy.i0p + cy.rB) + i0 * lda;
       const GemmDyn dsn{&w.snap[0], nullptr, 0};
       if (mB > 0 && (rc = gemm_nn(mB, bb, kk, 1.0, YB, m, Wm, 2 * b, 1.0, PB, lda, PB, lda, s, dsn))) return rc;
@@ -569,8 +593,7 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     // Overlap: worth it while the bulk rows outlast the chain kernels they hide
     // (and those leave an SM for the waiting thread).
     const int64_t top = std::min(bb, mr);
-    const bool split = overlap && second && J + 1 < nblk && nt > 1 && mr - top >= 1024 &&
-                       (mr - top) * (nt - bb) >= (int64_t)3 << 22 && nt - bb <= 147 * 256 && mr - bb <= 147 * 256;
+    const bool split = will_split(J);
     if (first)
       rc = trailing_first(P, lda, mr, nt, bb, Ypair, m, taus + i0, TJ, b, w.Wt, b, w.W, 2 * b, st, w.gemm, s);
     else if (second)
@@ -596,7 +619,7 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
         return rc;
       if ((rc = ov.mark_join())) return rc;
       if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
-      const int64_t rB = top + rup((mr - top) / 2, 64);
+      const int64_t rB = er.ra > 0 ? er.ra : top + rup((mr - top) / 2, 64);
       if ((rc = gemm_nn(rB - top, nt, b + bb, 1.0, Ypair + b + top, m, w.W, 2 * b, 1.0, P + top, lda, P + top, lda, s,
                         dm)))
         return rc;
@@ -605,7 +628,9 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       cy.bbp = bb;
       cy.mrp = mr;
       cy.rB = rB;
+      cy.koff = er.ra > 0 ? b : 0;
       cy.Ycat = Ypair;
+      er.ra = 0;
       continue;
     }
     // R columns [i0, i0+bb) go out only now: a short panel (bhat < bb) leaves
@@ -613,7 +638,35 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     // [i0, i0+bhat) the update above has just rewritten (randomized.py:203-213).
     if ((rc = sink.block(A, lda, i0, bb, b, J, s))) return rc;
     if (prep && (rc = ep.wait(s))) return rc;
+    int64_t early_rows = 0;
+    if (first && !no_early_rows && will_split(J + 1)) {
+      const int64_t ntj = nt - bb, mrj = mr - bb, free_sms = 148 - cdiv(ntj, 256);
+      early_rows = (int64_t)(kEarlyRowsWork * (double)free_sms / 148.0 / (double)(b * ntj)) / 64 * 64;
+      early_rows = std::min(early_rows, (mrj - b) * 6 / 10 / 64 * 64);
+      if (early_rows < 256) early_rows = 0;
+      if (early_rows) SQR_CUDA(cudaMemcpyAsync(w.snap2, st, 6 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+    }
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s, prep ? w.guard : nullptr))) return rc;
+    if (early_rows) {
+      // the second block's sample QRCP beside P's own second sweep on the bottom rows (see EarlyRows)
+      if ((rc = sample_update(w.Bf, ell, ell, P, lda, nt - bb, bb, Bn, ell, st, w.Gm, s, prep))) return rc;
+      std::swap(Bc, Bn);
+      if ((rc = ov.fork_from(s))) return rc;
+      const ResidentSig sig{w.sig, ++ov.epoch};
+      if ((rc = sample_qrcp(Bc, ell, ell, nt - bb, std::min(b, k - i0 - bb), w.Bf, ell, w.lperm, w.moves, w.stau, 0,
+                            st, w.sample, w.sample_bytes, ov.side, sig)))
+        return rc;
+      if ((rc = ov.mark_join())) return rc;
+      if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
+      const int64_t ra = mr - early_rows;  // relative to i0
+      if ((rc = gemm_nn(early_rows, nt, bb, 1.0, Ypair + ra, m, w.W, 2 * b, 1.0, P + ra, lda, P + ra, lda, s,
+                        GemmDyn{&w.snap2[0], &w.snap2[5], kShiftD})))
+        return rc;
+      SQR_CUDA(cudaMemset2DAsync(Ypair + ra, m * 8, 0, early_rows * 8, bb, s));
+      er.sample_launched = true;
+      er.ra = ra - bb;
+      continue;
+    }
     if (J + 1 < nblk) {
       const int64_t a1 = i0 + bb;  // achieved if the block completed
       if (resample) {

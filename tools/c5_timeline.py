@@ -43,12 +43,13 @@ for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:16]:
     print(f"{v[0] / 1e3:9.2f} ms {v[1]:6d}  {k}")
 # one pair in the middle (blocks 100, 101): every event in order with gaps
 mid = [e for e in evs if "sample_qrcp" in e.name]
-if len(mid) > 102:
-    a, b = mid[100].time_range.start, mid[102].time_range.start
+blk = int(os.environ.get("BLK", "100"))  # even: the pair (blk, blk + 1), from the previous block's sample QRCP on
+if len(mid) > blk + 2:
+    a, b = mid[blk - 1 if blk else 0].time_range.start, mid[blk + 2].time_range.start
     prev = None
     for e in evs:
         if a <= e.time_range.start < b:
             gap = (e.time_range.start - prev) if prev is not None else 0
             print(f"{(e.time_range.start - a) / 1e3:8.3f} ms  +{gap:6.1f} us  {(e.time_range.end - e.time_range.start):8.1f} us  "
                   f"{e.name.split('(')[0][-40:]}")
-            prev = e.time_range.end
+            prev = e.time_range.end if prev is None else max(prev, e.time_range.end)  # gap < 0: overlapped
