@@ -329,6 +329,16 @@ struct EarlyRows {
   bool sample_launched = false;  // the second block's sample QRCP is already on the side stream
   int64_t ra = 0;                // first early row relative to the second block's i0 (0 = none)
 };
+constexpr double kEarlyRowsWork2 = 0.9 * 31.4e12 * 0.53e-3 / 2.0;  // ... one panel hides
+// rows of P's second sweep to run beside the second block's panel (0 = none)
+inline int64_t early_rows2(int64_t mr, int64_t nt, int64_t bb, int64_t b, int64_t ra) {
+  static const bool off = env_flag("SQR_NO_EARLY_ROWS2");
+  if (off || nt - bb <= 0) return 0;
+  const int64_t free_sms = 148 - cdiv(mr, 256);
+  int64_t a2 = (int64_t)(kEarlyRowsWork2 * (double)free_sms / 148.0 / (double)(b * (nt - bb))) / 64 * 64;
+  a2 = std::min(a2, (ra - bb) / 2 / 64 * 64);  // leave rows for the K = 2b part beside the next sample QRCP
+  return a2 < 256 ? 0 : a2;
+}
 constexpr double kEarlyRowsWork = 0.9 * 31.4e12 * 0.66e-3 / 2.0;  // row x column x K products one sample QRCP hides
 constexpr int kResidentTimeoutUs = 100;
 
@@ -563,6 +573,26 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
           return rc;
       }
       if ((rc = ov.join_to(s))) return rc;
+    } else if (second && er.ra > 0 && panel_is_block(mr, bb) && early_rows2(mr, nt, bb, b, er.ra) > 0) {
+      // the panel beside more of P's second sweep: the rows just above the
+      // early rows, columns right of the panel (whose rows the pending update
+      // above has already covered); Y_P's rows there are retired too
+      const int64_t a2 = early_rows2(mr, nt, bb, b, er.ra), ra2 = er.ra - a2;
+      SQR_CUDA(cudaMemcpyAsync(w.snap2, st, 6 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
+      if ((rc = ov.fork_from(s))) return rc;
+      const ResidentSig sig{w.sig, ++ov.epoch};
+      if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm,
+                             ov.side, sig)))
+        return rc;
+      if ((rc = ov.mark_join())) return rc;
+      if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
+      double* Pa = P + ra2 + bb * lda;
+      if ((rc = gemm_nn(a2, nt - bb, b, 1.0, Ypair + b + ra2, m, w.W + bb * 2 * b, 2 * b, 1.0, Pa, lda, Pa, lda, s,
+                        GemmDyn{&w.snap2[0], nullptr, 0})))
+        return rc;
+      SQR_CUDA(cudaMemset2DAsync(Ypair + b + ra2, m * 8, 0, a2 * 8, b, s));
+      if ((rc = ov.join_to(s))) return rc;
+      er.ra = ra2;
     } else if ((rc = panel_factor(P, lda, mr, bb, -1, Yj, m, taus + i0, 1, st, w.panel, w.panel_bytes, sc, w.gemm,
                                   s)))
       return rc;
