@@ -229,8 +229,8 @@ struct GemmDyn {
 };
 
 // "Every CTA of this launch is resident" signal of the whole-SM chain kernels
-// (sample QRCP, panel): CTA 0 stores val to *flag after the kernel's first
-// grid / cluster barrier (or on an early exit).  The driver holds a GEMM on
+// (sample QRCP, panel): the last CTA stores val to *flag when it starts (CTAs
+// are dispatched in index order; CTA 0 on an early exit).  The driver holds a GEMM on
 // another stream behind wait_resident() until then, so the chain kernel
 // takes its SMs first and the GEMM's CTAs fill the rest (driver.cu, Overlap).
 struct ResidentSig {

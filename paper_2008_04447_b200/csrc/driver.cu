@@ -329,7 +329,7 @@ struct EarlyRows {
   bool sample_launched = false;  // the second block's sample QRCP is already on the side stream
   int64_t ra = 0;                // first early row relative to the second block's i0 (0 = none)
 };
-constexpr double kEarlyRowsWork2 = 0.9 * 31.4e12 * 0.53e-3 / 2.0;  // ... one panel hides
+constexpr double kEarlyRowsWork2 = 1.1 * 31.4e12 * 0.53e-3 / 2.0;  // ... one panel hides
 // rows of P's second sweep to run beside the second block's panel (0 = none)
 inline int64_t early_rows2(int64_t mr, int64_t nt, int64_t bb, int64_t b, int64_t ra) {
   static const bool off = env_flag("SQR_NO_EARLY_ROWS2");
@@ -339,7 +339,7 @@ inline int64_t early_rows2(int64_t mr, int64_t nt, int64_t bb, int64_t b, int64_
   a2 = std::min(a2, (ra - bb) / 2 / 64 * 64);  // leave rows for the K = 2b part beside the next sample QRCP
   return a2 < 256 ? 0 : a2;
 }
-constexpr double kEarlyRowsWork = 0.9 * 31.4e12 * 0.66e-3 / 2.0;  // row x column x K products one sample QRCP hides
+constexpr double kEarlyRowsWork = 1.0 * 31.4e12 * 0.66e-3 / 2.0;  // row x column x K products one sample QRCP hides
 constexpr int kResidentTimeoutUs = 100;
 
 // M = S11 R11^-1 and the R11 guard of the sample update (sketch.py:132-149,

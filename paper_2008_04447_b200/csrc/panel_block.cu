@@ -70,6 +70,8 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
     return;
   }
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  // CTAs are dispatched in index order: once the last one runs, all are resident
+  if (g == G - 1 && tid == 0) signal_resident(a.sig);
   const int lane = tid & 31, warp = tid >> 5;
   const int w = max(0, min(a.wstat < 0 ? a.st->sample_achieved : a.wstat, a.wmax));
   const int R = g * kBT + tid;
@@ -140,7 +142,6 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
       long long ck2 = ck ? clock64() : 0;
       if (tc < 40) SQR_TRACE(a.trace, 8 * tc + 1);
       gb.sync();
-      if (step == 1 && g == 0 && tid == 0) signal_resident(a.sig);  // first barrier passed: all CTAs resident
       if (tc < 40) SQR_TRACE(a.trace, 8 * tc + 2);
       long long ck3 = ck ? clock64() : 0;
       {
@@ -486,7 +487,6 @@ __global__ void __launch_bounds__(kBT, 1) panel_block_kernel(BlockPanelArgs a) {
     for (int c = ((w + kLf - 1) / kLf) * kLf; c < a.wmax; ++c) a.Y[(int64_t)c * a.ldy + R] = 0.0;
   }
   if (g == 0 && tid == 0) {
-    if (step == 0) signal_resident(a.sig);  // empty panel: no barrier was reached
     for (int c = bhat; c < a.wmax; ++c) a.taus[c] = 0.0;
     a.st->bhat = bhat;
     if (bhat == 0 && a.stop_at_zero) {

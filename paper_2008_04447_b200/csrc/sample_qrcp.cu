@@ -750,6 +750,8 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
   if (!CL) gb.init(a.bar);
   namespace cg = cooperative_groups;
   const int G = gridDim.x, g = blockIdx.x, tid = threadIdx.x;
+  // CTAs are dispatched in index order: once the last one runs, all are resident
+  if (g == G - 1 && tid == 0) signal_resident(a.sig);
   const int lane = tid & 31, warp = tid >> 5;
   const int col = g * kRT + tid;
   const bool own = col < a.nt;
@@ -828,7 +830,6 @@ __global__ void __launch_bounds__(kRT, 1) sample_qrcp_reg_kernel(RegArgs a) {
       gmax = fmax(gmax, __ldcg(a.pmax + i));
     }
   }
-  if (g == 0 && tid == 0) signal_resident(a.sig);  // every CTA has passed a barrier: all resident
   const double fro = sqrt(total);
   const double rank_floor_sq = (kRankFloor * fro) * (kRankFloor * fro);
   const double sample_floor = a.first ? kSampleFloor * kSampleFloor * gmax : __ldcg(&a.st->floor_sq);

@@ -35,7 +35,7 @@ print(f"span {(t1 - t0) / 1e3:.1f} ms, device busy (union) {busy / 1e3:.1f} ms, 
       f"kernels {len(evs)}")
 agg = {}
 for e in evs:
-    k = e.name.split("(")[0][-48:]
+    k = e.name.replace("(anonymous namespace)::", "").split("(")[0].split("<")[0][-48:]
     a = agg.setdefault(k, [0.0, 0])
     a[0] += e.time_range.end - e.time_range.start
     a[1] += 1
@@ -51,5 +51,5 @@ if len(mid) > blk + 2:
         if a <= e.time_range.start < b:
             gap = (e.time_range.start - prev) if prev is not None else 0
             print(f"{(e.time_range.start - a) / 1e3:8.3f} ms  +{gap:6.1f} us  {(e.time_range.end - e.time_range.start):8.1f} us  "
-                  f"{e.name.split('(')[0][-40:]}")
+                  f"{e.name.replace('(anonymous namespace)::', '').split('(')[0].split('<')[0][-40:]}  s{e.device_resource_id if hasattr(e, 'device_resource_id') else ''}")
             prev = e.time_range.end if prev is None else max(prev, e.time_range.end)  # gap < 0: overlapped
