@@ -276,9 +276,10 @@ struct Lookahead {
 // Each chain kernel goes first (high-priority stream; the GEMM's stream is
 // held until the kernel reports all CTAs resident, ResidentSig), the GEMM's
 // CTAs fill the SMs it leaves free and spread over the chip when it ends.
-// Per entry the arithmetic is that of the single merged sweep (same K order),
-// so results are bitwise unchanged.  The bulk GEMMs gate on a snapshot of
-// {stop, bhat} taken before finish_block, like Lookahead.
+// Per entry the arithmetic is that of the single merged sweep (same K order;
+// the early rows below apply P and J one after the other, as the reference
+// does).  The bulk GEMMs gate on a snapshot of {stop, bhat} taken before
+// finish_block, like Lookahead.
 struct Overlap {
   cudaStream_t side = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr;
@@ -336,8 +337,10 @@ inline int64_t early_rows2(int64_t mr, int64_t nt, int64_t bb, int64_t b, int64_
   if (off || nt - bb <= 0) return 0;
   const int64_t free_sms = 148 - cdiv(mr, 256);
   int64_t a2 = (int64_t)(kEarlyRowsWork2 * (double)free_sms / 148.0 / (double)(b * (nt - bb))) / 64 * 64;
+  static const bool force = env_flag("SQR_OVERLAP_FORCE");
+  if (force) a2 = std::max<int64_t>(a2, 64);
   a2 = std::min(a2, (ra - bb) / 2 / 64 * 64);  // leave rows for the K = 2b part beside the next sample QRCP
-  return a2 < 256 ? 0 : a2;
+  return a2 < (force ? 64 : 256) ? 0 : a2;
 }
 constexpr double kEarlyRowsWork = 1.0 * 31.4e12 * 0.66e-3 / 2.0;  // row x column x K products one sample QRCP hides
 constexpr int kResidentTimeoutUs = 100;
@@ -514,10 +517,15 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
   OverlapCarry cy;
   EarlyRows er;
   static const bool no_early_rows = env_flag("SQR_NO_EARLY_ROWS");
+  static const bool force_overlap = env_flag("SQR_OVERLAP_FORCE");
   auto will_split = [&](int64_t Jn) {  // the merged sweep of second block Jn runs split around the next chain
     const int64_t i0n = Jn * b, bbn = std::min(b, k - i0n), ntn = n - i0n, mrn = m - i0n, topn = std::min(bbn, mrn);
-    return overlap && (Jn & 1) && Jn + 1 < nblk && ntn > 1 && mrn - topn >= 1024 &&
-           (mrn - topn) * (ntn - bbn) >= (int64_t)3 << 22 && ntn - bbn <= 147 * 256 && mrn - bbn <= 147 * 256;
+    // worth it while the bulk rows outlast the chain kernels they hide (SQR_OVERLAP_FORCE: any size, tests),
+    // and those leave an SM for the waiting thread
+    const bool big = force_overlap ? mrn - topn >= 1
+                                   : mrn - topn >= 1024 && (mrn - topn) * (ntn - bbn) >= (int64_t)3 << 22;
+    return overlap && (Jn & 1) && Jn + 1 < nblk && ntn > 1 && big && ntn - bbn <= 147 * 256 &&
+           mrn - bbn <= 147 * 256;
   };
   if (overlap) {
     if ((rc = ov.init())) return rc;
@@ -620,8 +628,6 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       SQR_CUDA(cudaStreamWaitEvent(s, la.join, 0));
       continue;
     }
-    // Overlap: worth it while the bulk rows outlast the chain kernels they hide
-    // (and those leave an SM for the waiting thread).
     const int64_t top = std::min(bb, mr);
     const bool split = will_split(J);
     if (first)
@@ -649,9 +655,9 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
         return rc;
       if ((rc = ov.mark_join())) return rc;
       if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
-      const int64_t rB = er.ra > 0 ? er.ra : top + rup((mr - top) / 2, 64);
-      if ((rc = gemm_nn(rB - top, nt, b + bb, 1.0, Ypair + b + top, m, w.W, 2 * b, 1.0, P + top, lda, P + top, lda, s,
-                        dm)))
+      const int64_t rB = er.ra > 0 ? er.ra : std::min(mr, top + rup((mr - top) / 2, 64));
+      if (rB > top && (rc = gemm_nn(rB - top, nt, b + bb, 1.0, Ypair + b + top, m, w.W, 2 * b, 1.0, P + top, lda,
+                                    P + top, lda, s, dm)))
         return rc;
       cy.on = true;
       cy.i0p = i0;
@@ -672,8 +678,9 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     if (first && !no_early_rows && will_split(J + 1)) {
       const int64_t ntj = nt - bb, mrj = mr - bb, free_sms = 148 - cdiv(ntj, 256);
       early_rows = (int64_t)(kEarlyRowsWork * (double)free_sms / 148.0 / (double)(b * ntj)) / 64 * 64;
+      if (force_overlap) early_rows = std::max<int64_t>(early_rows, 64);
       early_rows = std::min(early_rows, (mrj - b) * 6 / 10 / 64 * 64);
-      if (early_rows < 256) early_rows = 0;
+      if (early_rows < (force_overlap ? 64 : 256)) early_rows = 0;
       if (early_rows) SQR_CUDA(cudaMemcpyAsync(w.snap2, st, 6 * sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
     }
     if ((rc = finish_block(st, nullptr, (int)i0, (int)bb, (int)k, (int)n, s, prep ? w.guard : nullptr))) return rc;
