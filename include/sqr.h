@@ -65,9 +65,12 @@ int sqr_device_sm_count(void);
 int64_t sqr_launch_count(void);
 /* Per-kernel-class CUDA-event timing of the next <= max_launches launches
  * (0 disables).  Classes: 0 gemm_tn, 1 gemm_nn, 2 sample_qrcp, 3 panel,
- * 4 build_t, 5 apply_moves, 6 sample_update, 7 gaussian, 8 misc. */
+ * 4 build_t, 5 apply_moves, 6 sample_update, 7 gaussian, 8 misc, 9 gemm_nn
+ * launches that share the chip with a sample QRCP / panel kernel (their event
+ * times measure the shared run; sqr_profile_flops gives their flops). */
 int sqr_profile_enable(int64_t max_launches);
 int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, int ntags);
+int sqr_profile_flops(double* flops_per_tag, int ntags);
 /* Debug: %globaltimer phase stamps of the cooperative kernels (NULL = off). */
 int sqr_debug_trace(void* device_buffer);
 

@@ -30,6 +30,7 @@ SIGNATURES = {
     "sqr_launch_count": (c_i64, []),
     "sqr_profile_enable": (c_int, [c_i64]),
     "sqr_profile_collect": (c_int, [c_ptr, c_ptr, c_int]),
+    "sqr_profile_flops": (c_int, [c_ptr, c_int]),
     "sqr_debug_trace": (c_int, [c_ptr]),
     "sqr_gaussian": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_u64, c_u64, c_int, c_ptr]),
     "sqr_gemm_tn": (c_int, [c_i64, c_i64, c_i64, c_dbl, c_ptr, c_i64, c_ptr, c_i64, c_dbl, c_ptr, c_i64,
@@ -134,7 +135,7 @@ def check(rc: int, what: str = "libsqr") -> None:
 
 
 PROFILE_TAGS = ["gemm_tn", "gemm_nn", "sample_qrcp", "panel", "build_t", "apply_moves", "sample_update",
-                "gaussian", "misc"]
+                "gaussian", "misc", "gemm_nn_beside_chain"]
 
 
 def profile_collect():
@@ -143,3 +144,10 @@ def profile_collect():
     cnt = (ctypes.c_int64 * 16)()
     lib().sqr_profile_collect(ms, cnt, 16)
     return {t: (ms[i], cnt[i]) for i, t in enumerate(PROFILE_TAGS)}
+
+
+def profile_flops():
+    """{class: flops} the drivers attributed since sqr_profile_enable (call before profile_collect resets)."""
+    fl = (ctypes.c_double * 16)()
+    lib().sqr_profile_flops(fl, 16)
+    return {t: fl[i] for i, t in enumerate(PROFILE_TAGS)}

@@ -41,10 +41,11 @@ int smem_optin(const void* fn, int bytes);
 // Launch accounting + optional per-kernel-class CUDA-event timing (bench.py
 // reads it through sqr_launch_count / sqr_profile_*).
 enum ProfTag { kTagGemmTn = 0, kTagGemmNn, kTagSample, kTagPanel, kTagBuildT, kTagMoves, kTagSampleUpd,
-               kTagGaussian, kTagMisc, kNumTags };
+               kTagGaussian, kTagMisc, kTagGemmNnBeside, kNumTags };
 void count_launch();
 void prof_begin(int tag, cudaStream_t s);
 void prof_end(int tag, cudaStream_t s);
+void prof_add_flops(int tag, double flops);  // only counted while profiling is on
 struct ProfScope {
   int tag;
   cudaStream_t s;
@@ -226,6 +227,10 @@ struct GemmDyn {
   // optional cap: N <= *limit - limit_off (dynamic panel width)
   const int32_t* limit = nullptr;
   int limit_off = 0;
+  // profiling class of this launch when >= 0 (gemm_nn: kTagGemmNnBeside for the
+  // bulk updates that share the chip with a chain kernel, whose event times
+  // measure the shared run)
+  int prof_tag = -1;
 };
 
 // "Every CTA of this launch is resident" signal of the whole-SM chain kernels

@@ -576,8 +576,11 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       if ((rc = ov.mark_join())) return rc;
       if (mB > 0 && nt - bb > 0) {
         if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
+        GemmDyn dsb = dsn;
+        dsb.prof_tag = kTagGemmNnBeside;
+        prof_add_flops(kTagGemmNnBeside, 2.0 * mB * (nt - bb) * kk);
         if ((rc = gemm_nn(mB, nt - bb, kk, 1.0, YB, m, Wm + bb * 2 * b, 2 * b, 1.0, PB + bb * lda, lda,
-                          PB + bb * lda, lda, s, dsn)))
+                          PB + bb * lda, lda, s, dsb)))
           return rc;
       }
       if ((rc = ov.join_to(s))) return rc;
@@ -595,8 +598,10 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       if ((rc = ov.mark_join())) return rc;
       if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
       double* Pa = P + ra2 + bb * lda;
-      if ((rc = gemm_nn(a2, nt - bb, b, 1.0, Ypair + b + ra2, m, w.W + bb * 2 * b, 2 * b, 1.0, Pa, lda, Pa, lda, s,
-                        GemmDyn{&w.snap2[0], nullptr, 0})))
+      GemmDyn da{&w.snap2[0], nullptr, 0};
+      da.prof_tag = kTagGemmNnBeside;
+      prof_add_flops(kTagGemmNnBeside, 2.0 * a2 * (nt - bb) * b);
+      if ((rc = gemm_nn(a2, nt - bb, b, 1.0, Ypair + b + ra2, m, w.W + bb * 2 * b, 2 * b, 1.0, Pa, lda, Pa, lda, s, da)))
         return rc;
       SQR_CUDA(cudaMemset2DAsync(Ypair + b + ra2, m * 8, 0, a2 * 8, b, s));
       if ((rc = ov.join_to(s))) return rc;
@@ -656,8 +661,11 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       if ((rc = ov.mark_join())) return rc;
       if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
       const int64_t rB = er.ra > 0 ? er.ra : std::min(mr, top + rup((mr - top) / 2, 64));
+      GemmDyn dma = dm;
+      dma.prof_tag = kTagGemmNnBeside;
+      prof_add_flops(kTagGemmNnBeside, 2.0 * (rB - top) * (nt - bb) * (b + bb));
       if (rB > top && (rc = gemm_nn(rB - top, nt, b + bb, 1.0, Ypair + b + top, m, w.W, 2 * b, 1.0, P + top, lda,
-                                    P + top, lda, s, dm)))
+                                    P + top, lda, s, dma)))
         return rc;
       cy.on = true;
       cy.i0p = i0;
@@ -696,8 +704,10 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       if ((rc = ov.mark_join())) return rc;
       if ((rc = wait_resident(sig, kResidentTimeoutUs, s))) return rc;
       const int64_t ra = mr - early_rows;  // relative to i0
-      if ((rc = gemm_nn(early_rows, nt, bb, 1.0, Ypair + ra, m, w.W, 2 * b, 1.0, P + ra, lda, P + ra, lda, s,
-                        GemmDyn{&w.snap2[0], &w.snap2[5], kShiftD})))
+      GemmDyn de{&w.snap2[0], &w.snap2[5], kShiftD};
+      de.prof_tag = kTagGemmNnBeside;
+      prof_add_flops(kTagGemmNnBeside, 2.0 * early_rows * (nt - bb) * bb);
+      if ((rc = gemm_nn(early_rows, nt, bb, 1.0, Ypair + ra, m, w.W, 2 * b, 1.0, P + ra, lda, P + ra, lda, s, de)))
         return rc;
       SQR_CUDA(cudaMemset2DAsync(Ypair + ra, m * 8, 0, early_rows * 8, bb, s));
       er.sample_launched = true;

@@ -725,7 +725,7 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
   const int kchunk = nsplit > 1 ? (int)rup(cdiv(K, nsplit), kBK) : std::max(K, 1);
   nsplit = nsplit > 1 ? (int)cdiv(K, kchunk) : 1;
   dim3 grid((unsigned)cdiv(M, Cfg::BM), (unsigned)cdiv(N, Cfg::BN), (unsigned)nsplit);
-  ProfScope ps(kTagGemmNn, s);
+  ProfScope ps(dyn.prof_tag >= 0 ? dyn.prof_tag : kTagGemmNn, s);
   gemm_nn_kernel<VEC, SQR_NN_BN><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, Y, ldy, beta, E, lde,
                                                                   D, ldd, dyn, kchunk, nsplit > 1 ? ws : nullptr);
   SQR_LAUNCH("gemm_nn_kernel");

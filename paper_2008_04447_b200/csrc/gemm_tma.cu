@@ -564,7 +564,7 @@ int launch_nn_tma(const CUtensorMap& mX, const CUtensorMap& mY, const CUtensorMa
   auto kern = gemm_nn_tma_kernel<BM, BN, WTN, NST, CTAS>;
   if (int rc = smem_optin((const void*)kern, Cfg::SMEM)) return rc;
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)cdiv(N, BN));
-  ProfScope ps(kTagGemmNn, s);
+  ProfScope ps(dyn.prof_tag >= 0 ? dyn.prof_tag : kTagGemmNn, s);
   kern<<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(mX, mY, mE, M, N, K, alpha, beta, D, ldd, dyn, x3d);
   SQR_LAUNCH("gemm_nn_tma_kernel");
   return SQR_OK;

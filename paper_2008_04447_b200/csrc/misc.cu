@@ -45,6 +45,7 @@ struct Profiler {
   std::vector<int> tags;
   size_t used = 0;
   cudaEvent_t pending[kNumTags] = {};
+  double flops[kNumTags] = {};
 };
 Profiler g_prof;
 std::mutex g_prof_mu;  // bench-only instrumentation, but callable from any thread
@@ -67,6 +68,12 @@ void prof_end(int tag, cudaStream_t s) {
   g_prof.tags.push_back(tag);
   g_prof.used += 2;
   g_prof.pending[tag] = nullptr;
+}
+
+void prof_add_flops(int tag, double flops) {
+  if (!g_prof.on) return;
+  std::lock_guard<std::mutex> lock(g_prof_mu);
+  g_prof.flops[tag] += flops;
 }
 
 // Device attributes, cached per device (thread-safe: atomics, idempotent fill).
@@ -717,6 +724,7 @@ extern "C" int sqr_profile_enable(int64_t max_launches) {
   g_prof.tags.clear();
   g_prof.used = 0;
   for (auto& p : g_prof.pending) p = nullptr;
+  for (auto& f : g_prof.flops) f = 0.0;
   g_prof.on = max_launches > 0;
   if (!g_prof.on) return SQR_OK;
   g_prof.ev.resize(2 * max_launches);
@@ -746,6 +754,16 @@ extern "C" int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, i
   }
   g_prof.tags.clear();
   g_prof.used = 0;
+  return SQR_OK;
+}
+
+// Flops the drivers attributed to a class since sqr_profile_enable (only the
+// launches whose share of a class the caller cannot derive from the shapes:
+// class 9, the bulk updates running beside a chain kernel).
+extern "C" int sqr_profile_flops(double* flops_per_tag, int ntags) {
+  using sqr::g_prof;
+  std::lock_guard<std::mutex> lock(sqr::g_prof_mu);
+  for (int t = 0; t < ntags; ++t) flops_per_tag[t] = t < sqr::kNumTags ? g_prof.flops[t] : 0.0;
   return SQR_OK;
 }
 
