@@ -335,8 +335,8 @@ constexpr double kEarlyRowsWork2 = 1.1 * 31.4e12 * 0.53e-3 / 2.0;  // ... one pa
 inline int64_t early_rows2(int64_t mr, int64_t nt, int64_t bb, int64_t b, int64_t ra) {
   static const bool off = env_flag("SQR_NO_EARLY_ROWS2");
   if (off || nt - bb <= 0) return 0;
-  const int64_t free_sms = 148 - cdiv(mr, 256);
-  int64_t a2 = (int64_t)(kEarlyRowsWork2 * (double)free_sms / 148.0 / (double)(b * (nt - bb))) / 64 * 64;
+  const int64_t sms = sm_count(), free_sms = std::max<int64_t>(0, sms - cdiv(mr, 256));
+  int64_t a2 = (int64_t)(kEarlyRowsWork2 * (double)free_sms / (double)sms / (double)(b * (nt - bb))) / 64 * 64;
   static const bool force = env_flag("SQR_OVERLAP_FORCE");
   if (force) a2 = std::max<int64_t>(a2, 64);
   a2 = std::min(a2, (ra - bb) / 2 / 64 * 64);  // leave rows for the K = 2b part beside the next sample QRCP
@@ -524,8 +524,8 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     // and those leave an SM for the waiting thread
     const bool big = force_overlap ? mrn - topn >= 1
                                    : mrn - topn >= 1024 && (mrn - topn) * (ntn - bbn) >= (int64_t)3 << 22;
-    return overlap && (Jn & 1) && Jn + 1 < nblk && ntn > 1 && big && ntn - bbn <= 147 * 256 &&
-           mrn - bbn <= 147 * 256;
+    const int64_t fit = (int64_t)(sm_count() - 1) * 256;  // chain kernels: 256 columns / rows per SM
+    return overlap && (Jn & 1) && Jn + 1 < nblk && ntn > 1 && big && ntn - bbn <= fit && mrn - bbn <= fit;
   };
   if (overlap) {
     if ((rc = ov.init())) return rc;
@@ -684,8 +684,9 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
     if (prep && (rc = ep.wait(s))) return rc;
     int64_t early_rows = 0;
     if (first && !no_early_rows && will_split(J + 1)) {
-      const int64_t ntj = nt - bb, mrj = mr - bb, free_sms = 148 - cdiv(ntj, 256);
-      early_rows = (int64_t)(kEarlyRowsWork * (double)free_sms / 148.0 / (double)(b * ntj)) / 64 * 64;
+      const int64_t ntj = nt - bb, mrj = mr - bb, sms = sm_count();
+      const int64_t free_sms = std::max<int64_t>(0, sms - cdiv(ntj, 256));
+      early_rows = (int64_t)(kEarlyRowsWork * (double)free_sms / (double)sms / (double)(b * ntj)) / 64 * 64;
       if (force_overlap) early_rows = std::max<int64_t>(early_rows, 64);
       early_rows = std::min(early_rows, (mrj - b) * 6 / 10 / 64 * 64);
       if (early_rows < (force_overlap ? 64 : 256)) early_rows = 0;
