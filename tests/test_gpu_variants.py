@@ -82,7 +82,8 @@ def oracle_results():
 
 
 def _run(env):
-    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, json.dumps(CASES)], env=dict(os.environ, **env),
+    base = {k: v for k, v in os.environ.items() if not k.startswith("SQR_")}  # only the switches under test
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, json.dumps(CASES)], env=dict(base, **env),
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     return json.loads(r.stdout.strip().splitlines()[-1])
