@@ -71,6 +71,8 @@ int64_t sqr_launch_count(void);
 int sqr_profile_enable(int64_t max_launches);
 int sqr_profile_collect(double* ms_per_tag, int64_t* count_per_tag, int ntags);
 int sqr_profile_flops(double* flops_per_tag, int ntags);
+/* Time only the classes whose bit is set in tag_mask (default: all). */
+int sqr_profile_select(uint32_t tag_mask);
 /* Debug: %globaltimer phase stamps of the cooperative kernels (NULL = off). */
 int sqr_debug_trace(void* device_buffer);
 

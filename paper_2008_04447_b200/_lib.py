@@ -31,6 +31,7 @@ SIGNATURES = {
     "sqr_profile_enable": (c_int, [c_i64]),
     "sqr_profile_collect": (c_int, [c_ptr, c_ptr, c_int]),
     "sqr_profile_flops": (c_int, [c_ptr, c_int]),
+    "sqr_profile_select": (c_int, [ctypes.c_uint32]),
     "sqr_debug_trace": (c_int, [c_ptr]),
     "sqr_gaussian": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_u64, c_u64, c_int, c_ptr]),
     "sqr_gemm_tn": (c_int, [c_i64, c_i64, c_i64, c_dbl, c_ptr, c_i64, c_ptr, c_i64, c_dbl, c_ptr, c_i64,
