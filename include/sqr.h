@@ -124,6 +124,18 @@ int sqr_sample_qrcp_ws(const double* B, int64_t ldb, int64_t ell, int64_t nt, in
                        int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st,
                        void* workspace, int64_t workspace_bytes, void* stream);
 
+/* sqr_sample_qrcp_ws that also stores resident_val to *resident_flag (device
+ * memory, zeroed by the caller, values increasing) once all of its CTAs are
+ * on the chip; sqr_wait_resident holds `stream` until then (at most
+ * timeout_us).  The sample QRCP owns ceil(nt / 256) whole SMs for its ~0.7 ms:
+ * a GEMM enqueued behind sqr_wait_resident on another stream runs on the
+ * other SMs meanwhile (no reference counterpart: scheduling only). */
+int sqr_sample_qrcp_ws_sig(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf,
+                           int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus, int first, sqr_status* st,
+                           void* workspace, int64_t workspace_bytes, uint32_t* resident_flag,
+                           uint32_t resident_val, void* stream);
+int sqr_wait_resident(uint32_t* resident_flag, uint32_t resident_val, int timeout_us, void* stream);
+
 /* Apply the block's column moves to rows [0, rows) of X (ld) starting at
  * column col0, and to the int64 vector perm (may be NULL) starting at col0
  * (randomized.py:194-195; trqrcp also permutes Wg, Rg at :301-302). */

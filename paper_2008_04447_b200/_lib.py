@@ -45,6 +45,9 @@ SIGNATURES = {
     "sqr_sample_qrcp_workspace": (c_i64, [c_i64, c_i64]),
     "sqr_sample_qrcp_ws": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_int,
                                    c_ptr, c_ptr, c_i64, c_ptr]),
+    "sqr_sample_qrcp_ws_sig": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_int,
+                                       c_ptr, c_ptr, c_i64, c_ptr, ctypes.c_uint32, c_ptr]),
+    "sqr_wait_resident": (c_int, [c_ptr, ctypes.c_uint32, c_int, c_ptr]),
     "sqr_apply_moves": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_i64, c_ptr]),
     "sqr_panel_qr": (c_int, [c_ptr, c_i64, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr, c_i64, c_int, c_ptr,
                              c_ptr]),

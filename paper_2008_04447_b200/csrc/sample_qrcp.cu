@@ -1384,3 +1384,21 @@ extern "C" int sqr_sample_qrcp_ws(const double* B, int64_t ldb, int64_t ell, int
   return sqr::sample_qrcp(B, ldb, ell, nt, bb, Bf, ldbf, lperm, moves, taus, first, st, workspace, workspace_bytes,
                           static_cast<cudaStream_t>(stream));
 }
+
+// The same with a residency signal: *resident_flag = resident_val once every
+// CTA of the sample QRCP is on the chip, so a caller can hold a GEMM on
+// another stream (sqr_wait_resident) until the whole-SM kernel has taken its
+// SMs and run the GEMM beside it (driver.cu Overlap; the multi-GPU driver's
+// deferred second-sweep rows).
+extern "C" int sqr_sample_qrcp_ws_sig(const double* B, int64_t ldb, int64_t ell, int64_t nt, int64_t bb, double* Bf,
+                                      int64_t ldbf, int64_t* lperm, int32_t* moves, double* taus, int first,
+                                      sqr_status* st, void* workspace, int64_t workspace_bytes,
+                                      uint32_t* resident_flag, uint32_t resident_val, void* stream) {
+  return sqr::sample_qrcp(B, ldb, ell, nt, bb, Bf, ldbf, lperm, moves, taus, first, st, workspace, workspace_bytes,
+                          static_cast<cudaStream_t>(stream), sqr::ResidentSig{resident_flag, resident_val});
+}
+
+extern "C" int sqr_wait_resident(uint32_t* resident_flag, uint32_t resident_val, int timeout_us, void* stream) {
+  return sqr::wait_resident(sqr::ResidentSig{resident_flag, resident_val}, timeout_us,
+                            static_cast<cudaStream_t>(stream));
+}

@@ -495,6 +495,9 @@ class GpuOps:
         self._stream = torch.cuda.current_stream(self.dev)
         self._sh = self._stream.cuda_stream
         self.lookahead = not os.environ.get("SQR_DIST_NO_LOOKAHEAD")
+        # the deferred rows run BESIDE the next sample QRCP (a whole-SM kernel on ceil(n_t / 256) SMs)
+        # on their own stream, released once that kernel is resident (csrc/driver.cu Overlap)
+        self.beside = self.lookahead and not os.environ.get("SQR_DIST_NO_BESIDE")
         self.plan_moves = bool(os.environ.get("SQR_DIST_PLAN_MOVES"))   # world 1: exercise the P2P plan path
         # SymmComm: panel broadcast and sample all-gather as device-initiated
         # NVLink puts into symmetric buffers (csrc/peer.cu)
@@ -584,6 +587,9 @@ class GpuOps:
         self.mbuf = torch.zeros(b * b, **f64)
         self.sws = torch.zeros(int(self.L.sqr_sample_qrcp_workspace(ell, n)), dtype=torch.uint8, device=self.dev)
         self.side = torch.cuda.Stream(self.dev, priority=-1)
+        self.bulk = torch.cuda.Stream(self.dev)
+        self.sig = torch.zeros(16, dtype=torch.int32, device=self.dev)
+        self._epoch = 0
         self.prep_done = None
         self.h_ctl = torch.zeros(self.ctl.numel(), dtype=torch.uint8).pin_memory()
         self.h_ctl_i32 = self.h_ctl.numpy().view(np.int32)
@@ -678,18 +684,39 @@ class GpuOps:
         if not first:  # the sample floor of the first block (randomized.py:179-180)
             st[32:40].view(torch.float64).fill_(self._floor)
         moves = self.ctl[128:].view(torch.int32)
-        self._chk(self.L.sqr_sample_qrcp_ws(B.data_ptr(), ell, ell, nt, bb, self.Bf.data_ptr(), ell,
-                                            self.lperm.data_ptr(), moves.data_ptr(), self.staus.data_ptr(),
-                                            1 if first else 0, st.data_ptr(), self.sws.data_ptr(), self.sws.numel(),
-                                            self._s()), "sample_qrcp")
+        beside = self.beside and self._tail is not None
+        if beside:
+            # deferred rows of the merged second sweep beside this kernel (see __init__)
+            self._epoch += 1
+            ready = torch.cuda.Event()
+            ready.record(self._cur())
+            self._chk(self.L.sqr_sample_qrcp_ws_sig(B.data_ptr(), ell, ell, nt, bb, self.Bf.data_ptr(), ell,
+                                                    self.lperm.data_ptr(), moves.data_ptr(), self.staus.data_ptr(),
+                                                    1 if first else 0, st.data_ptr(), self.sws.data_ptr(),
+                                                    self.sws.numel(), self.sig.data_ptr(), self._epoch, self._s()),
+                      "sample_qrcp")
+            self.bulk.wait_event(ready)
+            self._chk(self.L.sqr_wait_resident(self.sig.data_ptr(), self._epoch, 100, self.bulk.cuda_stream),
+                      "wait_resident")
+            self.run_tail(self.bulk.cuda_stream)
+            bulk_done = torch.cuda.Event()
+            bulk_done.record(self.bulk)
+        else:
+            self._chk(self.L.sqr_sample_qrcp_ws(B.data_ptr(), ell, ell, nt, bb, self.Bf.data_ptr(), ell,
+                                                self.lperm.data_ptr(), moves.data_ptr(), self.staus.data_ptr(),
+                                                1 if first else 0, st.data_ptr(), self.sws.data_ptr(),
+                                                self.sws.numel(), self._s()), "sample_qrcp")
         # one host synchronisation: status + moves, plus the previous panel's tail;
-        # the deferred rows of a merged second sweep run behind it (lookahead)
+        # without `beside` the deferred rows of a merged second sweep run behind it (lookahead)
         self.h_ctl.copy_(self.ctl, non_blocking=True)
         if pend_pan is not None:
             self.h_tail[:pend_pan.tail.numel()].copy_(pend_pan.tail, non_blocking=True)
         ev = torch.cuda.Event()
         ev.record(self._cur())
-        self.run_tail()
+        if beside:
+            self._cur().wait_event(bulk_done)   # the column moves that follow touch the same rows
+        else:
+            self.run_tail()
         ev.synchronize()
         self._synced()
         prev_tail = self._parse_tail(self.h_tail_np, pend_pan.Y.shape[0]) if pend_pan is not None else None
@@ -808,12 +835,15 @@ class GpuOps:
         self._synced()
         return out
 
-    def run_tail(self):
+    def run_tail(self, stream=None):
         """Enqueue the deferred rows >= i0 + bb of the last merged second sweep."""
         if self._tail is not None:
             M, N, K, X, ldx, W, ld, C = self._tail
             self._tail = None
-            self._gemm_nn(M, N, K, 1.0, X, ldx, W, ld, 1.0, C, ld, C, ld)
+            if stream is None:
+                self._gemm_nn(M, N, K, 1.0, X, ldx, W, ld, 1.0, C, ld, C, ld)
+            elif M > 0 and N > 0:
+                self._chk(self.L.sqr_gemm_nn(M, N, K, 1.0, X, ldx, W, ld, 1.0, C, ld, C, ld, stream), "gemm_nn")
 
     def finish(self):
         self.run_tail()
