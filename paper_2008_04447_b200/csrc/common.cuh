@@ -231,6 +231,10 @@ struct GemmDyn {
   // bulk updates that share the chip with a chain kernel, whose event times
   // measure the shared run)
   int prof_tag = -1;
+  // gemm_tn only, host side: recorded on the launch stream as soon as the
+  // first npre output columns (the Gram prefix) are final -- before the
+  // split-K reduction of the other columns -- so T can be built beside it
+  cudaEvent_t pre_ready = nullptr;
 };
 
 // "Every CTA of this launch is resident" signal of the whole-SM chain kernels

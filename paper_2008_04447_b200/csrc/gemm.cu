@@ -16,9 +16,15 @@
 // a separate reduce kernel, so results are bitwise deterministic.
 #include <algorithm>
 
+#include <climits>
+
 #include "common.cuh"
 
 namespace sqr {
+
+int splitk_reduce_launch(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
+                         const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, cudaStream_t s);
+
 
 namespace {
 
@@ -306,7 +312,8 @@ __global__ void __launch_bounds__(kThreads, SQR_TN_MINB)
 // beta * E(i, n), splits summed in index order, all SMs participating.
 __global__ void __launch_bounds__(256)
     splitk_reduce_kernel(int M, int N, int MT, int nsplit, double alpha, const double* __restrict__ part,
-                         double beta, const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn) {
+                         double beta, const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, int n_lo,
+                         int n_hi) {
   if (dyn.stop && *dyn.stop) return;
   if (dyn.shift) {
     const int sh = *dyn.shift;
@@ -318,9 +325,10 @@ __global__ void __launch_bounds__(256)
   }
   const int64_t stride = (int64_t)N * MT;  // partial layout uses N before the limit
   if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
-  const int64_t total = (int64_t)M * N;
+  N = min(N, n_hi);  // columns [n_lo, n_hi) of the output
+  const int64_t total = (int64_t)M * max(N - n_lo, 0);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e % M), n = (int)(e / M);
+    const int i = (int)(e % M), n = n_lo + (int)(e / M);
     const double* src = part + (int64_t)n * MT + i;
     double s = 0.0;
     int sp = 0;
@@ -675,12 +683,8 @@ int launch_tn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
   gemm_tn_kernel<MT, VEC><<<grid, kThreads, Cfg::SMEM, s>>>(M, N, K, alpha, X, ldx, C, ldc, beta, E,
                                                            lde, D, ldd, kchunk, part, nullptr, dyn);
   SQR_LAUNCH("gemm_tn_kernel");
-  if (nsplit > 1) {
-    const int64_t total = (int64_t)M * N;
-    const int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sm_count() * 8);
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn);
-    SQR_LAUNCH("splitk_reduce_kernel");
-  }
+  if (nsplit > 1) return splitk_reduce_launch(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, s);
+  if (dyn.pre_ready) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
   return SQR_OK;
 }
 
@@ -742,10 +746,22 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
 // Fixed-order split-K reduction shared with the TMA kernel (gemm_tma.cu).
 int splitk_reduce_launch(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
                          const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, cudaStream_t s) {
-  const int64_t total = (int64_t)M * N;
+  int n_lo = 0;
+  if (dyn.pre_ready && dyn.npre > 0 && dyn.npre < N) {
+    // the Gram prefix first: T is built beside the reduction of the other columns
+    const int blocks = (int)std::min<int64_t>(cdiv((int64_t)M * dyn.npre, 256), (int64_t)sm_count() * 8);
+    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, 0,
+                                                dyn.npre);
+    SQR_LAUNCH("splitk_reduce_kernel");
+    SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
+    n_lo = dyn.npre;
+  }
+  const int64_t total = (int64_t)M * (N - n_lo);
   const int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sm_count() * 8);
-  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn);
+  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, n_lo,
+                                              INT_MAX);
   SQR_LAUNCH("splitk_reduce_kernel");
+  if (dyn.pre_ready && n_lo == 0) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
   return SQR_OK;
 }
 

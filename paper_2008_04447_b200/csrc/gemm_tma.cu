@@ -531,6 +531,7 @@ int launch_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ld
                                                                kchunk, part, dyn);
   SQR_LAUNCH("gemm_tn_tma_kernel");
   if (nsplit > 1) return splitk_reduce_launch(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, s);
+  if (dyn.pre_ready) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
   return SQR_OK;
 }
 

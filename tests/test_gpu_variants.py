@@ -11,6 +11,7 @@ process) on the same inputs and is compared with the CPU oracle.
   SQR_NO_TMA             cp.async-staged GEMMs instead of the TMA / mbarrier ones
   SQR_NO_BLOCKPANEL      32-wide leaf kernel + WY GEMMs for every panel
   SQR_NO_LEAF            (with SQR_NO_BLOCKPANEL) the generic sub-panel kernel
+  SQR_NO_T_SIDE          T built on the main stream after the whole split-K reduction
   SQR_NO_OVERLAP         no chain / bulk overlap (the merged sweep in one launch)
   SQR_OVERLAP_FORCE      the overlapped schedule at every size (it is size-gated
                          otherwise), alone and with SQR_NO_EARLY_ROWS /
@@ -63,7 +64,8 @@ CASES = {"wide": (300, 420, 300, 32, 1, 0), "tall": (2000, 300, 300, 64, 2, 0), 
 VARIANTS = [{"SQR_NO_PAIRED_SWEEP": "1"}, {"SQR_NO_EARLY_PREP": "1"}, {"SQR_LOOKAHEAD": "1"},
             {"SQR_EPOCH_SAMPLE": "1"}, {"SQR_NO_CLUSTER_SAMPLE": "1"},
             {"SQR_NO_REGSAMPLE": "1"}, {"SQR_NO_TMA": "1"}, {"SQR_NO_BLOCKPANEL": "1"},
-            {"SQR_NO_BLOCKPANEL": "1", "SQR_NO_LEAF": "1"}, {"SQR_NO_OVERLAP": "1"}, {"SQR_OVERLAP_FORCE": "1"},
+            {"SQR_NO_BLOCKPANEL": "1", "SQR_NO_LEAF": "1"}, {"SQR_NO_OVERLAP": "1"}, {"SQR_NO_T_SIDE": "1"},
+            {"SQR_OVERLAP_FORCE": "1"},
             {"SQR_OVERLAP_FORCE": "1", "SQR_NO_EARLY_ROWS": "1"},
             {"SQR_OVERLAP_FORCE": "1", "SQR_NO_EARLY_ROWS2": "1"}]
 
