@@ -599,9 +599,19 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
                (rc = sample_qrcp(Bc, ell, ell, nt, bb, w.Bf, ell, w.lperm, w.moves, w.stau, J == 0, st, w.sample,
                                  w.sample_bytes, s)))
       return rc;
+    // the moves of the pending W rows (a few KB, latency-bound) beside the moves of A
+    const bool wside = overlap && (second || cy.on);
+    if (wside) {
+      if ((rc = ov.fork_from(s))) return rc;
+      const int64_t wrows = second ? b : b + cy.bbp - cy.koff;
+      double* Wmv = second ? w.W : w.W + cy.bbp * 2 * b + cy.koff;
+      if ((rc = apply_moves(Wmv, 2 * b, wrows, 0, nullptr, w.moves, st, 2 * bb, ov.side))) return rc;
+      if ((rc = ov.mark_join())) return rc;
+    }
     if ((rc = apply_moves(A, lda, m, i0, perm, w.moves, st, 2 * bb, s))) return rc;
+    if (wside && (rc = ov.join_to(s))) return rc;
     if (second) {
-      if ((rc = apply_moves(w.W, 2 * b, b, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
+      if (!wside && (rc = apply_moves(w.W, 2 * b, b, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
       if ((rc = pending_panel_update(P, lda, mr, bb, b, Ypair, m, w.W, 2 * b, st, s))) return rc;
     }
     PanelScratch sc{w.pscr, w.pscr + kLeaf * (kLeaf + b), w.pscr + kLeaf * (kLeaf + b) + kLeaf * b};
@@ -611,8 +621,7 @@ int rqrcp_impl(double* A, int64_t lda, int64_t m, int64_t n, int64_t k, int64_t 
       // runs beside the update of the other columns.
       cy.on = false;
       const int64_t kk = b + cy.bbp - cy.koff, mB = cy.mrp - cy.rB;
-      double* Wm = w.W + cy.bbp * 2 * b + cy.koff;  // column i0 of A
-      if ((rc = apply_moves(Wm, 2 * b, kk, 0, nullptr, w.moves, st, 2 * bb, s))) return rc;
+      double* Wm = w.W + cy.bbp * 2 * b + cy.koff;  // column i0 of A (its moves ran beside A's above)
       const double* YB = cy.Ycat + b + cy.rB + cy.koff * m;
       double* PB = A + (cy.i0p + cy.rB) + i0 * lda;
       const GemmDyn dsn{&w.snap[0], nullptr, 0};
