@@ -9,12 +9,12 @@ mkdir -p $out
 python bench.py > $out/bench.log 2>&1
 tail -1 $out/bench.log > $out/bench.json
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $out/launches.csv \
-    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary > $out/ncu_launches.log 2>&1
+    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary --no-profile > $out/ncu_launches.log 2>&1
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
     -k regex:"gemm|sample_qrcp|panel" --csv --log-file $out/traffic.csv \
-    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary > $out/ncu_traffic.log 2>&1
+    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary --no-profile > $out/ncu_traffic.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm_tn_tma -s 0 -c 2 -o $out/gemm_tn_full \
-    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary > $out/ncu_full_tn.log 2>&1
+    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary --no-profile > $out/ncu_full_tn.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:gemm_nn_tma -s 36 -c 4 -o $out/gemm_nn_full \
-    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary > $out/ncu_full.log 2>&1
+    python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline --no-secondary --no-profile > $out/ncu_full.log 2>&1
 ls -la $out
