@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(kThreads, SQR_TN_MINB)
 __global__ void __launch_bounds__(256)
     splitk_reduce_kernel(int M, int N, int MT, int nsplit, double alpha, const double* __restrict__ part,
                          double beta, const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, int n_lo,
-                         int n_hi) {
+                         int n_hi, int64_t pstride, int ncol0) {
   if (dyn.stop && *dyn.stop) return;
   if (dyn.shift) {
     const int sh = *dyn.shift;
@@ -323,13 +323,14 @@ __global__ void __launch_bounds__(256)
       if (E) E += (int64_t)sh * lde;
     }
   }
-  const int64_t stride = (int64_t)N * MT;  // partial layout uses N before the limit
+  // partial layout [split][column - ncol0][MT]: pstride elements per split (0: N * MT, N before the limit)
+  const int64_t stride = pstride ? pstride : (int64_t)N * MT;
   if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
   N = min(N, n_hi);  // columns [n_lo, n_hi) of the output
   const int64_t total = (int64_t)M * max(N - n_lo, 0);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
     const int i = (int)(e % M), n = n_lo + (int)(e / M);
-    const double* src = part + (int64_t)n * MT + i;
+    const double* src = part + (int64_t)(n - ncol0) * MT + i;
     double s = 0.0;
     int sp = 0;
     for (; sp + 8 <= nsplit; sp += 8) {
@@ -744,23 +745,29 @@ int launch_nn(int M, int N, int K, double alpha, const double* X, int64_t ldx, c
 }  // namespace
 
 // Fixed-order split-K reduction shared with the TMA kernel (gemm_tma.cu).
+int splitk_reduce_range(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
+                        const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, int n_lo, int n_hi,
+                        int64_t pstride, int ncol0, cudaStream_t s) {
+  const int64_t cols = std::max<int64_t>(1, (int64_t)std::min(N, n_hi) - n_lo);
+  const int blocks = (int)std::min<int64_t>(cdiv((int64_t)M * cols, 256), (int64_t)sm_count() * 8);
+  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, n_lo, n_hi,
+                                              pstride, ncol0);
+  SQR_LAUNCH("splitk_reduce_kernel");
+  return SQR_OK;
+}
+
 int splitk_reduce_launch(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
                          const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, cudaStream_t s) {
   int n_lo = 0;
   if (dyn.pre_ready && dyn.npre > 0 && dyn.npre < N) {
     // the Gram prefix first: T is built beside the reduction of the other columns
-    const int blocks = (int)std::min<int64_t>(cdiv((int64_t)M * dyn.npre, 256), (int64_t)sm_count() * 8);
-    splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, 0,
-                                                dyn.npre);
-    SQR_LAUNCH("splitk_reduce_kernel");
+    if (int rc = splitk_reduce_range(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, 0, dyn.npre, 0, 0, s))
+      return rc;
     SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
     n_lo = dyn.npre;
   }
-  const int64_t total = (int64_t)M * (N - n_lo);
-  const int blocks = (int)std::min<int64_t>(cdiv(total, 256), (int64_t)sm_count() * 8);
-  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, n_lo,
-                                              INT_MAX);
-  SQR_LAUNCH("splitk_reduce_kernel");
+  if (int rc = splitk_reduce_range(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, n_lo, INT_MAX, 0, 0, s))
+    return rc;
   if (dyn.pre_ready && n_lo == 0) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
   return SQR_OK;
 }

@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <climits>
 #include <cstdio>
 #include <mutex>
 #include <type_traits>
@@ -36,6 +37,9 @@ namespace sqr {
 
 int splitk_reduce_launch(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
                          const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, cudaStream_t s);
+int splitk_reduce_range(int M, int N, int MT, int nsplit, double alpha, const double* part, double beta,
+                        const double* E, int64_t lde, double* D, int64_t ldd, GemmDyn dyn, int n_lo, int n_hi,
+                        int64_t pstride, int ncol0, cudaStream_t s);
 
 namespace {
 
@@ -102,7 +106,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
     gemm_tn_tma_kernel(const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapP,
                        const __grid_constant__ CUtensorMap mapX, int M, int N, int K, double alpha, double beta,
                        const double* E, int64_t lde, double* D, int64_t ldd, int kchunk, double* part,
-                       GemmDyn dyn) {
+                       GemmDyn dyn, int tile0, int64_t pstride, int ncol0) {
   using Cfg = TmaCfg<MT>;
   constexpr int NST = Cfg::NST;
   extern __shared__ uint8_t smem_raw[];
@@ -119,7 +123,7 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   }
   const int Npart = N;  // split-K partial stride (before the limit, as in splitk_reduce)
   if (dyn.limit) N = min(N, *dyn.limit - dyn.limit_off);
-  const int n0 = blockIdx.x * kTmaBN;
+  const int n0 = (blockIdx.x + tile0) * kTmaBN;  // tile0: this launch covers the tiles from tile0 on
   if (n0 >= N) return;
   const int split = blockIdx.y, nsplit = gridDim.y;
   const int kbeg = split * kchunk;
@@ -203,7 +207,8 @@ __global__ void __launch_bounds__(kTmaThreads, 2)
   }
 
   if (nsplit > 1) {
-    double* mine = part + (int64_t)split * Npart * MT;
+    // partial layout [split][column - ncol0][MT]; pstride = elements per split (0: N * MT)
+    double* mine = part + (int64_t)split * (pstride ? pstride : (int64_t)Npart * MT) - (int64_t)ncol0 * MT;
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi)
 #pragma unroll
@@ -511,6 +516,72 @@ int launch_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ld
       best = sp;
     }
   }
+  // Two launches for long sweeps: with equal-length CTAs the last wave of tiles * sp CTAs leaves part of
+  // the chip idle for a whole CTA duration (3.2% of the C5 first sweeps).  The tiles that fill whole
+  // waves at split sp go first; the rest run at a higher split sp2, one more wave of shorter CTAs
+  // (0.5% left).  Only for wide outputs (the drivers' sweeps); other shapes keep the single launch,
+  // whose results are bitwise those of the cp.async kernel.
+  static const bool no_two = env_flag("SQR_NO_TN_TAIL_SPLIT");
+  int t1 = tiles, t2 = 0, sp2 = 1;
+  if (!no_two && dyn.limit == nullptr && tiles >= sms / 2 && ws != nullptr) {
+    const int pre_tiles = (int)cdiv(dyn.npre, kTmaBN);
+    for (int sp = 1; sp <= max_split; ++sp) {
+      if ((int64_t)tiles * sp > 8LL * sms) break;
+      const int full = (int)(((int64_t)tiles * sp) / sms);
+      if (full == 0) continue;
+      const int c1 = std::min(tiles, (int)(((int64_t)full * sms) / sp)), c2 = tiles - c1;
+      if (c2 == 0 || c1 < pre_tiles) continue;
+      const int s2 = std::min(max_split, sms / c2);
+      if (s2 <= sp) continue;
+      const double cost = (double)full / sp + 1.0 / s2 + 0.03;
+      const int64_t need = ((int64_t)sp * c1 + (int64_t)s2 * c2) * kTmaBN * MT * 8;
+      if (cost < best_cost - 1e-9 && need <= ws_bytes) {
+        best_cost = cost;
+        best = sp;
+        t1 = c1;
+        t2 = c2;
+        sp2 = s2;
+      }
+    }
+  }
+  auto chunk_of = [&](int sp, int* nsp) {
+    int kc = (int)rup(cdiv(K, sp), kTmaBK);
+    *nsp = std::max(1, (int)cdiv(K, kc));
+    if (*nsp == 1) kc = std::max(K, 1);
+    return kc;
+  };
+  if (t2 > 0) {
+    int ns1 = 1, ns2 = 1;
+    const int kc1 = chunk_of(best, &ns1), kc2 = chunk_of(sp2, &ns2);
+    const int64_t ps1 = (int64_t)t1 * kTmaBN * MT, ps2 = (int64_t)t2 * kTmaBN * MT;
+    double* part2 = ws + (int64_t)ns1 * ps1;
+    const int n1 = t1 * kTmaBN;
+    ProfScope ps(kTagGemmTn, s);
+    gemm_tn_tma_kernel<MT><<<dim3(t1, ns1), kTmaThreads, Cfg::SMEM, s>>>(mC, mP, mX, M, N, K, alpha, beta, E, lde, D,
+                                                                         ldd, kc1, ns1 > 1 ? ws : nullptr, dyn, 0,
+                                                                         ps1, 0);
+    SQR_LAUNCH("gemm_tn_tma_kernel");
+    if (ns1 == 1 && dyn.pre_ready) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
+    gemm_tn_tma_kernel<MT><<<dim3(t2, ns2), kTmaThreads, Cfg::SMEM, s>>>(mC, mP, mX, M, N, K, alpha, beta, E, lde, D,
+                                                                         ldd, kc2, ns2 > 1 ? part2 : nullptr, dyn,
+                                                                         t1, ps2, n1);
+    SQR_LAUNCH("gemm_tn_tma_kernel");
+    if (ns1 > 1) {
+      int lo = 0;
+      if (dyn.pre_ready && dyn.npre > 0 && dyn.npre < n1) {
+        if (int rc = splitk_reduce_range(M, N, MT, ns1, alpha, ws, beta, E, lde, D, ldd, dyn, 0, dyn.npre, ps1, 0, s))
+          return rc;
+        SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
+        lo = dyn.npre;
+      }
+      if (int rc = splitk_reduce_range(M, N, MT, ns1, alpha, ws, beta, E, lde, D, ldd, dyn, lo, n1, ps1, 0, s))
+        return rc;
+      if (dyn.pre_ready && lo == 0) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
+    }
+    if (ns2 > 1)
+      return splitk_reduce_range(M, N, MT, ns2, alpha, part2, beta, E, lde, D, ldd, dyn, n1, INT_MAX, ps2, n1, s);
+    return SQR_OK;
+  }
   int kchunk = (int)rup(cdiv(K, best), kTmaBK);
   int nsplit = (int)cdiv(K, kchunk);
   if (nsplit < 1) nsplit = 1;
@@ -528,7 +599,7 @@ int launch_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ld
   dim3 grid(tiles, nsplit);
   ProfScope ps(kTagGemmTn, s);
   gemm_tn_tma_kernel<MT><<<grid, kTmaThreads, Cfg::SMEM, s>>>(mC, mP, mX, M, N, K, alpha, beta, E, lde, D, ldd,
-                                                               kchunk, part, dyn);
+                                                               kchunk, part, dyn, 0, 0, 0);
   SQR_LAUNCH("gemm_tn_tma_kernel");
   if (nsplit > 1) return splitk_reduce_launch(M, N, MT, nsplit, alpha, part, beta, E, lde, D, ldd, dyn, s);
   if (dyn.pre_ready) SQR_CUDA(cudaEventRecord(dyn.pre_ready, s));
