@@ -26,6 +26,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <climits>
 #include <cstdio>
 #include <mutex>
@@ -522,6 +523,8 @@ int launch_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ld
   // (0.5% left).  Only for wide outputs (the drivers' sweeps); other shapes keep the single launch,
   // whose results are bitwise those of the cp.async kernel.
   static const bool no_two = env_flag("SQR_NO_TN_TAIL_SPLIT");
+  constexpr int kTailMinK = 512;       // shortest K chunk of the tail launch (1024: same; measured)
+  constexpr double kTailCost = 0.03;   // second launch + longer reduction, in CTA durations (0.01-0.06: +-2 ms)
   int t1 = tiles, t2 = 0, sp2 = 1;
   if (!no_two && dyn.limit == nullptr && tiles >= sms / 2 && ws != nullptr) {
     const int pre_tiles = (int)cdiv(dyn.npre, kTmaBN);
@@ -531,9 +534,9 @@ int launch_tn_tma(int M, int N, int K, double alpha, const double* X, int64_t ld
       if (full == 0) continue;
       const int c1 = std::min(tiles, (int)(((int64_t)full * sms) / sp)), c2 = tiles - c1;
       if (c2 == 0 || c1 < pre_tiles) continue;
-      const int s2 = std::min(max_split, sms / c2);
+      const int s2 = std::min(std::min(max_split, sms / c2), std::max(1, K / kTailMinK));
       if (s2 <= sp) continue;
-      const double cost = (double)full / sp + 1.0 / s2 + 0.03;
+      const double cost = (double)full / sp + 1.0 / s2 + kTailCost;
       const int64_t need = ((int64_t)sp * c1 + (int64_t)s2 * c2) * kTmaBN * MT * 8;
       if (cost < best_cost - 1e-9 && need <= ws_bytes) {
         best_cost = cost;

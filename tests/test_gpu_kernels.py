@@ -48,8 +48,11 @@ def test_gaussian_matches_stream(rows, cols, seed, offset):
 
 
 # ------------------------------------------------------------------ GEMMs
+# the last three are wide enough (>= 148 tiles of 64 columns) for the two-launch schedule of long sweeps
+# (whole waves at one split, the remaining tiles at a higher split; csrc/gemm_tma.cu)
 @pytest.mark.parametrize("M,N,K,off", [(40, 1000, 1000, 0), (136, 700, 5000, 0), (128, 300, 70001, 0),
-                                       (33, 129, 17, 1), (144, 1, 3, 0), (7, 513, 4096, 1), (128, 128, 32768, 0)])
+                                       (33, 129, 17, 1), (144, 1, 3, 0), (7, 513, 4096, 1), (128, 128, 32768, 0),
+                                       (128, 12000, 8192, 0), (64, 20224, 5000, 0), (32, 9500, 20000, 0)])
 def test_gemm_tn(M, N, K, off):
     rng = np.random.default_rng(M * N + K)
     X = rng.standard_normal((K + off, M))
