@@ -321,7 +321,11 @@ def run_ours(args):
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            traffic = (tj.get(dom + "_tma") or tj[dom])["bytes_per_launch"]  # TMA kernels since round 2
+            e = tj.get(dom + "_tma") or tj[dom]  # TMA kernels since round 2
+            # per gemm_tn CALL like `achieved` (a long sweep is two kernel launches, csrc/gemm_tma.cu):
+            # the class's DRAM bytes of one step / the calls of one step
+            calls = prof[dom][1] / args.steps
+            traffic = e["bytes_per_launch"] * e["launches"] / calls if calls else e["bytes_per_launch"]
         except Exception:
             traffic = None
     roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved_tf, "peak": PEAK_FP64_TFLOPS,
